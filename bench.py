@@ -1,0 +1,457 @@
+#!/usr/bin/env python
+"""Benchmark: refocused static frames/s of the EM background reconstruction.
+
+One step = one synthetic light-field frame through the whole hot path
+(descriptors, surface raster, support candidate lists, initial masks, EM with
+the reference's convergence rule (max 5 iterations at C2), Eq. 2 refocus,
+median) -- `FramePipeline.run` on frames already resident in HBM (`value`),
+and the public `reconstruct()` call from pinned host memory with the
+artefacts copied back (`e2e`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+N > 1 is launched by torchrun: one rank per GPU, each rank reconstructs its
+own frames (frame-parallel, BASELINE C5; no data-path collective), time =
+max over ranks.  `--impl reference` times the CPU oracle (the numpy
+restatement of the reference) on a bounded pixel sample of the same frame.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "refocused static frames/sec (and Gpix·plane/s) at 1/2/4/8 B200 vs CPU ref"
+CONFIGS = {  # name: (width, height, cameras, d_max, max_iters)
+    "C1": (640, 480, 5, 32.0, 5),
+    "C2": (1280, 720, 5, 64.0, 5),
+    "C3": (1920, 1080, 5, 128.0, 10),
+    "C4": (3840, 2160, 9, 128.0, 10),
+}
+SCENE = dict(coverage=0.25, seed=11, p_flip=0.1, blur_radius=2)
+L2_FLUSH_BYTES = 256 << 20
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# -- inputs -----------------------------------------------------------------------
+
+def load_inputs(cfg):
+    """Render the config's frame (bit-identical to the reference renderer) and
+    triangulate the support the reference harvested for it."""
+    import hashlib
+    from paper_2003_11076_b200 import synth
+    from paper_2003_11076_b200.prior import SupportPoint, triangulate
+    w, h, k, dmax, iters = CONFIGS[cfg]
+    spec = synth.occluder_scene(width=w, height=h, cameras=k, **SCENE)
+    frame, _ = synth.render(spec)
+    rig = spec.rig()
+    path = os.path.join(ROOT, "tests", "golden", f"bench_{cfg}.npz")
+    z = np.load(path)
+
+    def digest(arrs):
+        hh = hashlib.sha256()
+        for a in arrs:
+            hh.update(np.ascontiguousarray(a).tobytes())
+        return hh.hexdigest()
+
+    exact = (digest(frame.images) == str(z["image_digest"])
+             and digest(frame.priors) == str(z["prior_digest"]))
+    pts = [SupportPoint(int(u), int(v), float(d), int(s))
+           for (u, v), d, s in zip(z["support_uv"], z["support_d"], z["support_src"])]
+    tri = triangulate(pts, w, h)
+    return frame, rig, tri, exact
+
+
+def params_for(cfg):
+    import paper_2003_11076_b200 as st
+    w, h, k, dmax, iters = CONFIGS[cfg]
+    return st.SolverParams(max_iters=iters), st.PriorParams(d_max=dmax)
+
+
+# -- clocks ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -- CPU oracle sample ------------------------------------------------------------------
+
+def oracle_sample(frame, rig, tri, cfg, rows):
+    """Time the CPU oracle (numpy restatement of the reference) on a band of
+    `rows` reference rows; extrapolate to a full frame.
+
+    Full-frame per-frame parts (descriptors, mu raster) are timed in full;
+    the per-pixel parts (initial masks, EM, refocus, median) on the band.
+    """
+    import oracle
+    w, h, k, dmax, iters = CONFIGS[cfg]
+    sp, pp = params_for(cfg)
+    p = oracle.OracleParams(beta=sp.beta, threshold=sp.threshold, max_iters=sp.max_iters,
+                            min_static_rays=sp.min_static_rays, epsilon_prior=sp.epsilon_prior,
+                            sigma=pp.sigma, gamma=pp.gamma, d_max=pp.d_max,
+                            neighborhood_radius=pp.neighborhood_radius)
+    a = np.stack([rig.warp_coefficients(i)[0] for i in range(k)])
+    b = np.stack([rig.warp_coefficients(i)[1] for i in range(k)])
+    sup_uv, sup_d = tri.support_points()
+    t0 = time.perf_counter()
+    desc = [oracle.descriptors_of(im) for im in frame.images]
+    mu = oracle.mu_raster(tri.points, tri.disparities, tri.triangles, tri.planes, w, h)
+    t_full = time.perf_counter() - t0
+    r0 = max(0, (h - rows) // 2)
+    active = np.arange(r0 * w, (r0 + rows) * w, dtype=np.int64)
+    s = oracle.OracleSolver(frame.images, frame.priors, a, b, rig.ref_index, mu, sup_uv, sup_d,
+                            params=p, descriptors=desc)
+    t1 = time.perf_counter()
+    res = s.solve(active=active)
+    # refocus + median restricted to the band (+1 row halo for the median)
+    lo, hi = max(0, r0 - 1), min(h, r0 + rows + 1)
+    st_band = np.full((h, w), oracle.STATUS_LOW_TEXTURE, np.uint8)
+    st_band[r0:r0 + rows] = res["status"][r0:r0 + rows]
+    img, prov, nr = oracle.synthesize(frame.images, a, b, rig.ref_index, res["values"], st_band,
+                                      res["static_bits"], sp.min_static_rays, 0)
+    oracle.median_filter(img[lo:hi], 1)
+    t_band = time.perf_counter() - t1
+    frac = rows / h
+    t_frame = t_full + t_band / frac
+    return {"t_frame": t_frame, "t_full": t_full, "t_band": t_band, "rows": rows, "frac": frac,
+            "iterations": res["stats"]["iterations_run"]}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(cpu_cores())
+    except Exception:  # noqa: BLE001
+        pass
+    cfg = args.config
+    w, h, k, dmax, iters = CONFIGS[cfg]
+    frame, rig, tri, exact = load_inputs(cfg)
+    # calibrate the band so the whole run stays within ~args.budget seconds
+    probe = oracle_sample(frame, rig, tri, cfg, rows=8)
+    per_row = probe["t_band"] / 8
+    n_runs = args.steps + args.warmup
+    avail = max(1.0, args.budget / n_runs - probe["t_full"])
+    rows = int(max(8, min(h, avail / max(per_row, 1e-6))))
+    log(f"reference arm: {rows} rows per step (per-row {per_row:.3f}s, full parts "
+        f"{probe['t_full']:.2f}s)")
+    for _ in range(args.warmup):
+        oracle_sample(frame, rig, tri, cfg, rows=max(8, rows // 4))
+    times = []
+    for _ in range(args.steps):
+        r = oracle_sample(frame, rig, tri, cfg, rows=rows)
+        times.append(r["t_frame"])
+    t = float(np.mean(times))
+    fps = 1.0 / t
+    sample = (f"{rows} of {h} rows per step ({rows * w} px); descriptors + mu raster timed "
+              f"for the full frame, the per-pixel EM/refocus/median on the band, "
+              f"extrapolated by row fraction; numpy oracle")
+    out = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, args, exact),
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cpu_cores(),
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpix_plane_per_s": w * h * dmax * fps / 1e9,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def config_block(cfg, args, exact):
+    w, h, k, dmax, iters = CONFIGS[cfg]
+    return {"workload": f"{cfg}: {k}-camera linear array {w}x{h}, {int(dmax)} depth planes "
+                        f"(d_max), max {iters} EM iters with the reference convergence rule; "
+                        f"solve + refocus + median per frame",
+            "width": w, "height": h, "views": k, "d_max": dmax, "max_iters": iters,
+            "scene": "occluder_scene(coverage=0.25, seed=11, p_flip=0.1, blur_radius=2)",
+            "inputs_match_reference_digest": bool(exact),
+            "l2": "flushed between steps (256 MiB write)",
+            "parallelism": f"frame-parallel x{args.gpus}" if args.gpus > 1 else "1 GPU",
+            "forced_iters": args.forced_iters or None}
+
+
+# -- GPU arm ------------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import paper_2003_11076_b200 as st
+    from paper_2003_11076_b200 import _native as N
+    from paper_2003_11076_b200.prior import TriDevice
+    from paper_2003_11076_b200.reconstruct import FramePipeline
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    w, h, k, dmax, iters = CONFIGS[cfg]
+    sp, pp = params_for(cfg)
+    frame, rig, tri, exact = load_inputs(cfg)
+    lib = N.lib()
+
+    # device-resident inputs
+    pipe = FramePipeline(rig, w, h, sp, pp)
+    pipe.load(frame.images, frame.priors)
+    tdev = TriDevice(tri)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        pipe.run(tdev, forced_iters=args.forced_iters)
+    torch.cuda.synchronize()
+
+    # -- value: K steps on resident inputs, L2 flushed between steps ------------------
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stats = []
+    barrier()
+    launches0 = lib.st_launch_count()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)
+            starts[i].record(stream)
+            stats.append(pipe.run(tdev, forced_iters=args.forced_iters, timing=True))
+            ends[i].record(stream)
+        barrier()
+    launches = lib.st_launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(np.sum(step_ms))
+    if dist is not None:
+        tt = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    fps = world * args.steps / (total_ms / 1e3)
+
+    # -- e2e: public API from pinned host memory, artefacts back to the host ----------
+    pin_imgs = [st.device.pinned_empty(im.shape, np.uint8) for im in frame.images]
+    pin_pris = [st.device.pinned_empty(p.shape, np.float32) for p in frame.priors]
+    for d, s in zip(pin_imgs, frame.images):
+        d[...] = s
+    for d, s in zip(pin_pris, frame.priors):
+        d[...] = s
+    host_frame = st.LightFieldFrame(images=pin_imgs, priors=pin_pris)
+    e2e_steps = max(3, args.steps // 2)
+    for _ in range(2):
+        st.reconstruct(host_frame, rig, tri, sp, pp, forced_iters=args.forced_iters)
+    barrier()
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for _ in range(e2e_steps):
+        out = st.reconstruct(host_frame, rig, tri, sp, pp, forced_iters=args.forced_iters)
+    e_end.record(stream)
+    barrier()
+    e2e_ms = e_start.elapsed_time(e_end)
+    if dist is not None:
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_fps = world * e2e_steps / (e2e_ms / 1e3)
+    tdv = TriDevice(tri)
+    h2d = sum(a.nbytes for a in pin_imgs) + sum(a.nbytes for a in pin_pris) + tdv.nbytes
+    d2h = pipe.output_bytes()
+
+    # -- forced-5 (non-reference bench mode): exactly max_iters EM iterations -----------
+    forced = None
+    if not args.forced_iters and args.forced_steps > 0:
+        pipe.run(tdev, forced_iters=iters)
+        torch.cuda.synchronize()
+        fs = torch.cuda.Event(enable_timing=True)
+        fe = torch.cuda.Event(enable_timing=True)
+        fms = 0.0
+        for _ in range(args.forced_steps):
+            flush.fill_(1)
+            fs.record(stream)
+            pipe.run(tdev, forced_iters=iters)
+            fe.record(stream)
+            fe.synchronize()
+            fms += fs.elapsed_time(fe)
+        forced = {"iterations": iters, "fps_per_gpu": args.forced_steps / (fms / 1e3),
+                  "ms_per_frame": fms / args.forced_steps}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # -- roofline of the dominant kernel (k_m_step) ---------------------------------------
+    s0 = stats[-1]
+    ms_m = float(np.mean([s.kernel_ms[0] for s in stats]))
+    n_m = s0.kernel_launches[0]
+    samples_m = s0.candidates_total + s0.prev_evals     # candidate energies the model charges
+    bytes_m = samples_m * k * 16                          # 16 B per (candidate, view)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peak = float(json.load(open(peaks_path))["hbm_gbs"])
+        peak_src = "measured"
+    else:
+        peak, peak_src = 6650.0, "fallback"
+    achieved = bytes_m / (ms_m / 1e3) / 1e9
+    npx = w * h
+    c_bar = s0.candidates_total / max(1, npx * s0.iterations_run)
+    frame_bytes = npx * (s0.iterations_run * (c_bar * k * 16 + k * 20) + 7 * k)
+    step_ms_mean = total_ms / args.steps
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get("k_m_step_dram_bytes_per_launch")
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rows = args.cpu_rows
+        r = oracle_sample(frame, rig, tri, cfg, rows=rows)
+        cpu = {"value": 1.0 / r["t_frame"], "unit": "frames/s", "cores": cpu_cores(),
+               "kind": "port",
+               "sample": f"{rows} of {h} rows ({rows * w} px) through the numpy oracle "
+                         f"(initial masks, EM, refocus, median), descriptors + mu raster on "
+                         f"the full frame, extrapolated by row fraction "
+                         f"({r['t_frame']:.1f} s/frame)"}
+
+    out = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_mean,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference renderer, reference support harvest; "
+                f"digest match {exact})",
+        "config": config_block(cfg, args, exact),
+        "roofline": {"bound": "hbm", "kernel": "k_m_step", "achieved": achieved, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "algorithmic_bytes_per_launch": bytes_m / max(1, n_m),
+                     "launch_ms": ms_m / max(1, n_m), "launches_per_step": n_m,
+                     "share_of_step": ms_m / step_ms_mean},
+        "frame_roofline": {"model_bytes": frame_bytes, "achieved_gbs":
+                           frame_bytes / (step_ms_mean / 1e3) / 1e9,
+                           "frac": frame_bytes / (step_ms_mean / 1e3) / 1e9 / peak},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / e2e_steps},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "em": {"iterations_run": s0.iterations_run, "converged_after": s0.converged_after,
+               "candidates_per_px_iter": c_bar,
+               "energy_evals_per_px_iter": s0.energy_evals / max(1, npx * s0.iterations_run),
+               "kernel_ms": {"m_step": ms_m,
+                             "e_step": float(np.mean([s.kernel_ms[1] for s in stats])),
+                             "initial_masks": float(np.mean([s.kernel_ms[2] for s in stats])),
+                             "reduce": float(np.mean([s.kernel_ms[3] for s in stats]))}},
+        "gpix_plane_per_s": w * h * dmax * fps / 1e9,
+        "forced_iters_mode": forced,
+    }
+    print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--forced-iters", type=int, default=0)
+    ap.add_argument("--forced-steps", type=int, default=5)
+    ap.add_argument("--cpu-rows", type=int, default=96)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--budget", type=float, default=150.0,
+                    help="reference arm: seconds for the whole run")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,244 @@
+/*
+ * seethrough_b200 -- C ABI of the B200-native EM light-field background
+ * reconstruction (arXiv 2003.11076).
+ *
+ * The reference (`seethrough`, pure Python/numpy) has no native FFI; its
+ * public entry points for this path are Python functions.  Each entry point
+ * below is the native replacement a ctypes binding calls in place of the
+ * reference function cited next to it (paths relative to
+ * /root/reference/pkg/src/seethrough/).  See INTEGRATION.md for the binding.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers (caller-owned; the Python layer
+ *     allocates them as torch CUDA tensors).  Calls are ordered on `stream`
+ *     (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *   - Images are (K, H, W, 3) uint8, priors (K, H, W) float32, descriptors
+ *     (K, H, W, 16) uint8, per-pixel maps are row-major H*W.
+ *   - Return 0 on success, a negative ST_E* code on failure; the message is
+ *     available from st_last_error() (thread-local).  Validation errors carry
+ *     the reference's exact ValueError text.
+ *   - No CPU fallback exists: every compute entry point launches sm_100a
+ *     kernels and fails with ST_ECUDA when no device is usable.
+ */
+#ifndef SEETHROUGH_B200_H
+#define SEETHROUGH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ST_MAX_VIEWS 12   /* solver.py:46 MAX_ENUMERATED_VIEWS */
+#define ST_DESC_LEN 16    /* features.py:19 */
+#define ST_DESC_MARGIN 3  /* features.py:20 */
+
+enum {
+  ST_OK = 0,
+  ST_EINVAL = -1,  /* bad argument (ValueError in the reference) */
+  ST_ECUDA = -2,   /* CUDA runtime / launch failure */
+  ST_ENOMEM = -3,  /* workspace too small */
+};
+
+/* solver.py:48-50 */
+enum { ST_STATUS_VALID = 0, ST_STATUS_LOW_TEXTURE = 1, ST_STATUS_NO_STATIC_EVIDENCE = 2 };
+/* refocus.py:19-21 */
+enum { ST_PROV_FALLBACK = 0, ST_PROV_COPIED = 128, ST_PROV_REFOCUSED = 255 };
+
+/* CameraRig warp tables (geometry.py:156-172, 200-202): the homogeneous warp
+ * of reference pixel (u, v) at disparity d into view k is
+ * h = A_k (u, v, 1) + d b_k, evaluated left to right in fp64. */
+typedef struct {
+  int32_t num_views;
+  int32_t ref_index;
+  int32_t width, height;                    /* frame size (every view) */
+  double warp_a[ST_MAX_VIEWS][9];           /* row-major 3x3 */
+  double warp_b[ST_MAX_VIEWS][3];
+  int32_t view_w[ST_MAX_VIEWS];             /* rig intrinsics size, for the margin test */
+  int32_t view_h[ST_MAX_VIEWS];             /* (solver.py:197-204 uses rig dims)        */
+} st_rig;
+
+/* SolverParams (solver.py:56-62) + PriorParams (prior.py:33-40). */
+typedef struct {
+  double beta;
+  double threshold;
+  int32_t max_iters;
+  int32_t min_static_rays;
+  double epsilon_prior;
+  double sigma;
+  double gamma;
+  double d_max;
+  double neighborhood_radius;
+  int32_t forced_iters; /* >0: run exactly this many iterations (bench mode, non-reference) */
+  int32_t timing;       /* 1: st_solve brackets its kernels with CUDA events (st_stats.kernel_ms) */
+} st_params;
+
+/* EMStats (solver.py:84-90) */
+typedef struct {
+  int32_t iterations_run;
+  int32_t converged_after;           /* -1 == None */
+  double mean_energy[64];
+  double prev_energy[64];
+  double changed_fraction[64];
+  int64_t active_pixels;
+  int64_t support_records;           /* diagnostic: (tile, value) records built */
+  int64_t candidates_total;          /* sum over iterations/pixels of candidates in range */
+  int64_t energy_evals;              /* sum of candidate energies actually evaluated */
+  int64_t prev_evals;                /* previous-disparity energies (iterations >= 2) */
+  /* with st_params.timing: summed CUDA-event durations per kernel family
+   * [0] k_m_step, [1] k_e_step_at, [2] k_initial_masks, [3] the rest */
+  double kernel_ms[4];
+  int32_t kernel_launches[4];
+} st_stats;
+
+const char* st_last_error(void);
+int st_version(void);
+int st_device_count(void);
+/* Cumulative number of __global__ launches issued by this library (all
+ * threads; CUB's internal launches inside st_support_build / st_solve count
+ * as one per CUB call). */
+int64_t st_launch_count(void);
+
+/* ---- L1 primitives ---------------------------------------------------- */
+
+/* features.py:81-104 compute_descriptors (with rgb_to_gray :29-36 and
+ * sobel_responses :39-58) for K views at once.  channels = 3 (RGB) or 1. */
+int st_descriptors(const uint8_t* images, int32_t K, int32_t H, int32_t W, int32_t channels,
+                   uint8_t* desc_out, uint8_t* gray_out /* nullable (K,H,W) */,
+                   uint8_t* sobel_out /* nullable (K,H,W,2): biased gx, gy */, void* stream);
+
+/* sampling.py:21-55 bilinear on an (h*w, c) float32 plane; out (n, c) f64. */
+int st_bilinear(const float* plane, int32_t h, int32_t w, int32_t c, const double* u,
+                const double* v, int64_t n, double* out, void* stream);
+
+/* geometry.py:204-219 CameraRig.warp for view k; ok is uint8. */
+int st_warp(const st_rig* rig, int32_t k, const double* u, const double* v, const double* d,
+            int64_t n, double* pu, double* pv, uint8_t* ok, void* stream);
+
+/* TriangulationPrior (prior.py:265-315) on the device, with the Qhull tables
+ * scipy's Delaunay.find_simplex walks (scipy.spatial.Delaunay: neighbors,
+ * transform, equations, paraboloid_scale/shift, min/max_bound). */
+typedef struct {
+  const double* points;       /* (n_pts,2) vertex coordinates (u, v) */
+  const double* disparities;  /* (n_pts) */
+  const int32_t* simplices;   /* (n_tri,3) */
+  const double* planes;       /* (n_tri,3) d = a u + b v + c */
+  const int32_t* neighbors;   /* (n_tri,3) Qhull neighbour opposite vertex k, -1 on the hull */
+  const double* transform;    /* (n_tri,3,2) barycentric transforms */
+  const double* equations;    /* (n_tri,4) lifted facet hyperplanes */
+  int32_t n_pts, n_tri;
+  double paraboloid_scale, paraboloid_shift;
+  double min_bound[2], max_bound[2];
+} st_tri;
+
+/* prior.py:276-310 TriangulationPrior.disparity_map -- the containing
+ * triangle's plane at every pixel centre, choosing the triangle exactly as
+ * scipy's find_simplex walk does for a raster-order batch -- then the
+ * solver's clip to [1e-6, d_max] (solver.py:185-186) when clip_dmax > 0.
+ * mu out (H*W) f64. */
+int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip_dmax, double* mu_out,
+                 void* workspace, int64_t workspace_bytes, void* stream);
+int64_t st_mu_raster_workspace(int32_t W, int32_t H);
+
+/* ---- solver pieces (DisparitySolver API, solver.py:162-432) ----------- */
+
+/* Per-frame device context the solver entry points share. */
+typedef struct {
+  const uint8_t* images;   /* (K,H,W,3) */
+  const float* priors;     /* (K,H,W)   */
+  const uint8_t* desc;     /* (K,H,W,16) */
+  const double* mu;        /* (H*W) clipped surface */
+  /* support tile lists built by st_support_build (SoA, sorted by tile then value) */
+  const uint32_t* sup_tile_start;  /* (n_tiles+1) */
+  const float* sup_value;          /* (n_records) fp32-rounded support disparity */
+  const uint32_t* sup_uv;          /* (n_records) u | v << 16 */
+} st_frame;
+
+/* Build per-tile support candidate lists (solver.py:286-321 semantics).
+ * support_uv (n,2) f64 pixel coords, support_d (n) f64.  Writes into
+ * workspace; fills the sup_* pointers of *frame.  Returns records count via
+ * *n_records. */
+int st_support_build(const double* support_uv, const double* support_d, int32_t n,
+                     int32_t W, int32_t H, const st_params* params, st_frame* frame,
+                     void* workspace, int64_t workspace_bytes, int64_t* n_records,
+                     void* stream);
+int64_t st_support_workspace(int32_t n, int32_t W, int32_t H, double radius);
+
+/* solver.py:421-432 initial_masks over pix (nullable = all H*W pixels). */
+int st_initial_masks(const st_frame* f, const st_rig* rig, const st_params* p,
+                     const int64_t* pix, int64_t n, uint32_t* static_out,
+                     uint32_t* valid_out, void* stream);
+
+/* solver.py:206-227 gather_rays: desc (n,K,16) f64, valid (n,K) u8, q (n,K) f64. */
+int st_gather_rays(const st_frame* f, const st_rig* rig, const int64_t* pix,
+                   const double* d, int64_t n, double* desc, uint8_t* valid, double* q,
+                   void* stream);
+
+/* solver.py:229-260 _energy: energy (n) f64 and real (n) u8. */
+int st_energy(const st_frame* f, const st_rig* rig, const st_params* p, const int64_t* pix,
+              const double* d, const uint32_t* bits, int64_t n, double* energy,
+              uint8_t* real, void* stream);
+
+/* solver.py:325-407 m_step over active pixels (sorted; nullable = all).
+ * static_all is the full H*W mask map.  Outputs per active pixel. */
+int st_m_step(const st_frame* f, const st_rig* rig, const st_params* p, const int64_t* active,
+              int64_t n, const uint32_t* static_all, double* d_out, double* e_out,
+              uint8_t* status_out, void* stream);
+
+/* solver.py:409-419 e_step_at: mask reassignment at d (per listed pixel). */
+int st_e_step_at(const st_frame* f, const st_rig* rig, const st_params* p, const int64_t* pix,
+                 const double* d, int64_t n, uint32_t* static_out, uint32_t* valid_out,
+                 void* stream);
+
+/* solver.py:115-157 e_step on gathered rays: desc (n,K,16) f64,
+ * valid (n,K) u8, q (n,K) f64 -> out (n) u32. */
+int st_e_step(const double* desc, const uint8_t* valid, const double* q, int64_t n, int32_t K,
+              const st_params* p, uint32_t* out, void* stream);
+
+/* solver.py:93-107 masked_variance, batched: desc (n,K,16) f64, mask (n,K) u8 -> var (n). */
+int st_masked_variance(const double* desc, const uint8_t* mask, int64_t n, int32_t K,
+                       double* out, void* stream);
+
+/* ---- the fused solve (solver.py:436-508) ------------------------------ */
+
+int64_t st_solve_workspace(int32_t W, int32_t H, int32_t K);
+
+/* Full EM: initial masks, M/E alternation with the reference's global
+ * convergence rule (or forced_iters), outputs values f32 / status u8 /
+ * static u32 / valid u32 (H*W each).  dynamic_only selects active pixels
+ * with ref prior < threshold (solver.py:449-452).  The optional reduce
+ * callback all-reduces (sum, in place) `n` per-iteration values (energy sums
+ * and integer counts, exact below 2^53) across row-band shards for the
+ * global convergence rule and EMStats means; NULL on a single device. */
+typedef int (*st_reduce_fn)(double* values, int32_t n, void* user);
+int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t dynamic_only,
+             const uint8_t* active_mask /* nullable: explicit H*W active map */,
+             float* values, uint8_t* status, uint32_t* static_bits, uint32_t* valid_bits,
+             st_stats* stats, void* workspace, int64_t workspace_bytes,
+             st_reduce_fn reduce, void* reduce_user, void* stream);
+
+/* ---- refocus (refocus.py:24-148) ------------------------------------- */
+
+/* synthesize: Eq. 2 static-ray average + provenance + n_rays, then the
+ * clipped median rewrite of every non-COPIED pixel.  copy_mask nullable. */
+int st_synthesize(const uint8_t* images, const st_rig* rig, const float* values,
+                  const uint8_t* status, const uint32_t* static_bits, int32_t min_static_rays,
+                  int32_t median_radius, const uint8_t* copy_mask, uint8_t* image_out,
+                  uint8_t* prov_out, uint8_t* n_rays_out, uint8_t* scratch /* H*W*3 */,
+                  void* stream);
+
+/* refocus.py:52-65 refocus_pixel / :24-49 gather_static_colors, batched
+ * over listed pixels: rgb (n,3) u8, count (n), prov (n), totals (n,3) f64
+ * (nullable). */
+int st_refocus_pixels(const uint8_t* images, const st_rig* rig, const int64_t* pix,
+                      const double* d, const uint32_t* bits, int64_t n, int32_t min_static_rays,
+                      uint8_t* rgb, int32_t* count, uint8_t* prov, double* totals, void* stream);
+
+/* refocus.py:68-106 median_filter on an (H,W,C) uint8 image. */
+int st_median(const uint8_t* image, int32_t H, int32_t W, int32_t C, int32_t radius,
+              uint8_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEETHROUGH_B200_H */

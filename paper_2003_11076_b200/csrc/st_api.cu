@@ -1,0 +1,519 @@
+// C ABI entry points and the native EM driver (solver.py:436-508).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cub/cub.cuh>
+#include <vector>
+
+#include "st_common.cuh"
+#include "st_em.cuh"
+
+#define ST_VERSION 10000
+
+namespace sthost {
+
+static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return ST_ECUDA;
+}
+
+}  // namespace sthost
+
+namespace {
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+int check_views(int K) {
+  if (K > ST_MAX_VIEWS) {
+    sthost::set_error("mask enumeration is exponential; refusing %d views (limit %d)", K,
+                      ST_MAX_VIEWS);
+    return ST_EINVAL;
+  }
+  if (K < 1) {
+    sthost::set_error("a light-field frame needs at least two views");
+    return ST_EINVAL;
+  }
+  return ST_OK;
+}
+
+// solver.py:187-192: band offsets nearest-first, coarse sweep length.
+int make_ctx(const st_frame* f, const st_rig* rig, const st_params* p, st::EmCtx& c) {
+  int rc = check_views(rig->num_views);
+  if (rc) return rc;
+  memset(&c, 0, sizeof(c));
+  c.rig = *rig;
+  c.p = *p;
+  c.W = rig->width;
+  c.H = rig->height;
+  c.HW = (int64_t)c.W * c.H;
+  c.desc = reinterpret_cast<const uint4*>(f->desc);
+  c.priors = f->priors;
+  c.mu = f->mu;
+  const int jm = (int)floor(2.0 * p->sigma / 0.5 + 1e-12);
+  if (2 * jm + 1 > ST_MAX_BAND) {
+    sthost::set_error("sigma too large for the candidate band (%d offsets > %d)", 2 * jm + 1,
+                      ST_MAX_BAND);
+    return ST_EINVAL;
+  }
+  std::vector<double> band;
+  for (int j = -jm; j <= jm; ++j) band.push_back(0.5 * j);
+  std::stable_sort(band.begin(), band.end(), [](double a, double b) {
+    return fabs(a) < fabs(b) || (fabs(a) == fabs(b) && a < b);
+  });
+  c.n_band = (int)band.size();
+  for (int j = 0; j < c.n_band; ++j) c.band[j] = band[j];
+  // len(np.arange(1.0, d_max + 1e-9, 4.0))
+  const double span = ceil(((p->d_max + 1e-9) - 1.0) / 4.0);
+  c.n_coarse = span > 0 ? (int)span : 0;
+  c.sup_tile_start = f->sup_tile_start;
+  c.sup_value = f->sup_value;
+  c.sup_uv = f->sup_uv;
+  c.tiles_x = (c.W + ST_TW - 1) / ST_TW;
+  c.sup_ir = (int)floor(p->neighborhood_radius);
+  c.sup_r2 = p->neighborhood_radius * p->neighborhood_radius;
+  return ST_OK;
+}
+
+unsigned blocks_for(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+// Optional CUDA-event brackets around the solve's kernels (st_params.timing).
+struct EventSet {
+  bool on;
+  cudaEvent_t e[6];
+  explicit EventSet(bool enable) : on(enable) {
+    if (on)
+      for (auto& x : e) cudaEventCreate(&x);
+  }
+  ~EventSet() {
+    if (on)
+      for (auto& x : e) cudaEventDestroy(x);
+  }
+  void record(int i, cudaStream_t s) {
+    if (on) cudaEventRecord(e[i], s);
+  }
+  double ms(int a, int b) {
+    if (!on) return 0.0;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e[a], e[b]);
+    return (double)t;
+  }
+};
+
+int estep_smem(int K) { return ESTEP_BLOCK * K * 16 * (int)sizeof(double); }
+
+int prepare_estep_kernels() {
+  static bool done = false;
+  if (done) return ST_OK;
+  const int max_smem = estep_smem(ST_MAX_VIEWS);
+  ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_at, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     max_smem));
+  ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_rays,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+  done = true;
+  return ST_OK;
+}
+
+}  // namespace
+
+namespace st {
+
+__global__ void k_bilinear(const float* __restrict__ plane, int h, int w, int c,
+                           const double* __restrict__ u, const double* __restrict__ v, int64_t n,
+                           double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Taps t = taps_of(u[i], v[i], w, h);
+  const size_t b = ((size_t)t.iv * w + t.iu) * c;
+  const size_t bu = b + (size_t)t.su * c, bv = b + (size_t)t.sv * c, bvu = bu + (size_t)t.sv * c;
+  for (int ch = 0; ch < c; ++ch) {
+    double top = lerp_f32(plane[b + ch], plane[bu + ch], t.fu);
+    if (t.fv != 0.0) {
+      const double bot = lerp_f32(plane[bv + ch], plane[bvu + ch], t.fu);
+      top = dadd(top, dmul(t.fv, dsub(bot, top)));
+    }
+    out[(size_t)i * c + ch] = top;
+  }
+}
+
+__global__ void k_warp(st_rig rig, int k, const double* __restrict__ u,
+                       const double* __restrict__ v, const double* __restrict__ d, int64_t n,
+                       double* __restrict__ pu, double* __restrict__ pv, uint8_t* __restrict__ ok) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* a = rig.warp_a[k];
+  const double* b = rig.warp_b[k];
+  const double uu = u[i], vv = v[i], dd = d[i];
+  const double hx = dadd(dadd(dadd(dmul(a[0], uu), dmul(a[1], vv)), a[2]), dmul(dd, b[0]));
+  const double hy = dadd(dadd(dadd(dmul(a[3], uu), dmul(a[4], vv)), a[5]), dmul(dd, b[1]));
+  const double hz = dadd(dadd(dadd(dmul(a[6], uu), dmul(a[7], vv)), a[8]), dmul(dd, b[2]));
+  pu[i] = ddiv(hx, hz);
+  pv[i] = ddiv(hy, hz);
+  ok[i] = hz > 0.0 ? 1 : 0;
+}
+
+}  // namespace st
+
+extern "C" {
+
+const char* st_last_error(void) { return sthost::g_err; }
+int st_version(void) { return ST_VERSION; }
+int64_t st_launch_count(void) { return sthost::g_launches.load(); }
+
+int st_device_count(void) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    sthost::cuda_fail(e, "cudaGetDeviceCount");
+    return 0;
+  }
+  return n;
+}
+
+int st_bilinear(const float* plane, int32_t h, int32_t w, int32_t c, const double* u,
+                const double* v, int64_t n, double* out, void* stream) {
+  if (n <= 0) return ST_OK;
+  st::k_bilinear<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(plane, h, w, c, u, v, n,
+                                                                        out);
+  ST_LAUNCH_CHECK("k_bilinear");
+  return ST_OK;
+}
+
+int st_warp(const st_rig* rig, int32_t k, const double* u, const double* v, const double* d,
+            int64_t n, double* pu, double* pv, uint8_t* ok, void* stream) {
+  if (k < 0 || k >= rig->num_views) {
+    sthost::set_error("view index %d out of range", k);
+    return ST_EINVAL;
+  }
+  if (n <= 0) return ST_OK;
+  st::k_warp<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*rig, k, u, v, d, n, pu, pv,
+                                                                    ok);
+  ST_LAUNCH_CHECK("k_warp");
+  return ST_OK;
+}
+
+int st_initial_masks(const st_frame* f, const st_rig* rig, const st_params* p, const int64_t* pix,
+                     int64_t n, uint32_t* static_out, uint32_t* valid_out, void* stream) {
+  st::EmCtx c;
+  int rc = make_ctx(f, rig, p, c);
+  if (rc) return rc;
+  if (!pix) n = c.HW;
+  if (n <= 0) return ST_OK;
+  st::k_initial_masks<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(c, pix, n, static_out,
+                                                                             valid_out);
+  ST_LAUNCH_CHECK("k_initial_masks");
+  return ST_OK;
+}
+
+int st_gather_rays(const st_frame* f, const st_rig* rig, const int64_t* pix, const double* d,
+                   int64_t n, double* desc, uint8_t* valid, double* q, void* stream) {
+  st::EmCtx c;
+  st_params p = {};
+  p.sigma = 1.0;
+  int rc = make_ctx(f, rig, &p, c);
+  if (rc) return rc;
+  if (n <= 0) return ST_OK;
+  st::k_gather_rays<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(c, pix, d, n, desc,
+                                                                           valid, q);
+  ST_LAUNCH_CHECK("k_gather_rays");
+  return ST_OK;
+}
+
+int st_energy(const st_frame* f, const st_rig* rig, const st_params* p, const int64_t* pix,
+              const double* d, const uint32_t* bits, int64_t n, double* energy, uint8_t* real,
+              void* stream) {
+  st::EmCtx c;
+  int rc = make_ctx(f, rig, p, c);
+  if (rc) return rc;
+  if (n <= 0) return ST_OK;
+  st::k_energy<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(c, pix, d, bits, n, energy,
+                                                                      real);
+  ST_LAUNCH_CHECK("k_energy");
+  return ST_OK;
+}
+
+int st_m_step(const st_frame* f, const st_rig* rig, const st_params* p, const int64_t* active,
+              int64_t n, const uint32_t* static_all, double* d_out, double* e_out,
+              uint8_t* status_out, void* stream) {
+  st::EmCtx c;
+  int rc = make_ctx(f, rig, p, c);
+  if (rc) return rc;
+  if (!active) n = c.HW;
+  if (n <= 0) return ST_OK;
+  st::MStepArgs a = {};
+  a.active = active;
+  a.n = n;
+  a.static_all = static_all;
+  a.d_out = d_out;
+  a.e_out = e_out;
+  a.status_out = status_out;
+  st::k_m_step<<<blocks_for(n, EM_BLOCK), EM_BLOCK, 0, (cudaStream_t)stream>>>(c, a);
+  ST_LAUNCH_CHECK("k_m_step");
+  return ST_OK;
+}
+
+int st_e_step_at(const st_frame* f, const st_rig* rig, const st_params* p, const int64_t* pix,
+                 const double* d, int64_t n, uint32_t* static_out, uint32_t* valid_out,
+                 void* stream) {
+  st::EmCtx c;
+  int rc = make_ctx(f, rig, p, c);
+  if (rc) return rc;
+  if ((rc = prepare_estep_kernels())) return rc;
+  if (!pix) n = c.HW;
+  if (n <= 0) return ST_OK;
+  st::EStepArgs a = {};
+  a.pix = pix;
+  a.n = n;
+  a.d = d;
+  a.static_out = static_out;
+  a.valid_out = valid_out;
+  a.scatter = 0;
+  st::k_e_step_at<<<blocks_for(n, ESTEP_BLOCK), ESTEP_BLOCK, estep_smem(rig->num_views),
+                    (cudaStream_t)stream>>>(c, a);
+  ST_LAUNCH_CHECK("k_e_step_at");
+  return ST_OK;
+}
+
+int st_e_step(const double* desc, const uint8_t* valid, const double* q, int64_t n, int32_t K,
+              const st_params* p, uint32_t* out, void* stream) {
+  int rc = check_views(K);
+  if (rc) return rc;
+  if ((rc = prepare_estep_kernels())) return rc;
+  if (n <= 0) return ST_OK;
+  st::k_e_step_rays<<<blocks_for(n, ESTEP_BLOCK), ESTEP_BLOCK, estep_smem(K),
+                      (cudaStream_t)stream>>>(desc, valid, q, n, K, *p, out);
+  ST_LAUNCH_CHECK("k_e_step_rays");
+  return ST_OK;
+}
+
+int st_masked_variance(const double* desc, const uint8_t* mask, int64_t n, int32_t K, double* out,
+                       void* stream) {
+  if (n <= 0) return ST_OK;
+  st::k_masked_variance<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(desc, mask, n, K,
+                                                                               out);
+  ST_LAUNCH_CHECK("k_masked_variance");
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fused solve
+
+struct SolveLayout {
+  size_t d0, d1, e, st_act, active, flags, offs, partials, reduced, cub, total;
+  size_t cub_bytes;
+  int max_blocks;
+};
+
+static SolveLayout solve_layout(int W, int H) {
+  SolveLayout L;
+  const int64_t npx = (int64_t)W * H;
+  L.max_blocks = (int)blocks_for(npx, EM_BLOCK);
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                (int)(npx + 1));
+  L.cub_bytes = scan_bytes;
+  size_t o = 0;
+  L.d0 = o;       o += align_up(sizeof(double) * npx);
+  L.d1 = o;       o += align_up(sizeof(double) * npx);
+  L.e = o;        o += align_up(sizeof(double) * npx);
+  L.st_act = o;   o += align_up(npx);
+  L.active = o;   o += align_up(sizeof(int64_t) * npx);
+  L.flags = o;    o += align_up(sizeof(uint32_t) * (npx + 1));
+  L.offs = o;     o += align_up(sizeof(uint32_t) * (npx + 1));
+  L.partials = o; o += align_up(sizeof(st::Partial) * L.max_blocks);
+  L.reduced = o;  o += align_up(sizeof(st::Partial) * 66);
+  L.cub = o;      o += align_up(L.cub_bytes);
+  L.total = o;
+  return L;
+}
+
+int64_t st_solve_workspace(int32_t W, int32_t H, int32_t K) {
+  (void)K;
+  return (int64_t)solve_layout(W, H).total;
+}
+
+int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t dynamic_only,
+             const uint8_t* active_mask, float* values, uint8_t* status, uint32_t* static_bits,
+             uint32_t* valid_bits, st_stats* stats, void* workspace, int64_t workspace_bytes,
+             st_reduce_fn reduce, void* reduce_user, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  st::EmCtx c;
+  int rc = make_ctx(f, rig, p, c);
+  if (rc) return rc;
+  if ((rc = prepare_estep_kernels())) return rc;
+  const int W = c.W, H = c.H;
+  const int64_t npx = c.HW;
+  const SolveLayout L = solve_layout(W, H);
+  if ((int64_t)L.total > workspace_bytes) {
+    sthost::set_error("solve workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                      (long long)L.total);
+    return ST_ENOMEM;
+  }
+  char* ws = (char*)workspace;
+  double* dbuf[2] = {(double*)(ws + L.d0), (double*)(ws + L.d1)};
+  double* e_act = (double*)(ws + L.e);
+  uint8_t* st_act = (uint8_t*)(ws + L.st_act);
+  int64_t* active = (int64_t*)(ws + L.active);
+  uint32_t* flags = (uint32_t*)(ws + L.flags);
+  uint32_t* offs = (uint32_t*)(ws + L.offs);
+  st::Partial* partials = (st::Partial*)(ws + L.partials);
+  st::Partial* reduced = (st::Partial*)(ws + L.reduced);
+
+  memset(stats, 0, sizeof(*stats));
+  stats->converged_after = -1;
+  EventSet ev(p->timing != 0);
+
+  // initial masks for every pixel at the surface disparity (solver.py:455)
+  ev.record(4, s);
+  st::k_initial_masks<<<blocks_for(npx, 128), 128, 0, s>>>(c, nullptr, npx, static_bits,
+                                                           valid_bits);
+  ST_LAUNCH_CHECK("k_initial_masks");
+  ev.record(5, s);
+  stats->kernel_launches[2] += 1;
+
+  // active set (solver.py:447-452)
+  const bool dense = !dynamic_only && !active_mask;
+  int64_t n_act = npx;
+  if (!dense) {
+    const float* ref_prior = f->priors + (size_t)rig->ref_index * npx;
+    st::k_flag_active<<<blocks_for(npx, 256), 256, 0, s>>>(ref_prior, active_mask, npx,
+                                                          p->threshold, flags);
+    ST_LAUNCH_CHECK("k_flag_active");
+    ST_CUDA_CHECK(cudaMemsetAsync(flags + npx, 0, sizeof(uint32_t), s));
+    size_t tb = L.cub_bytes;
+    ST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws + L.cub, tb, flags, offs, (int)(npx + 1), s));
+    sthost::count_launch();
+    st::k_scatter_active<<<blocks_for(npx, 256), 256, 0, s>>>(flags, offs, npx, active);
+    ST_LAUNCH_CHECK("k_scatter_active");
+    uint32_t cnt = 0;
+    ST_CUDA_CHECK(cudaMemcpyAsync(&cnt, offs + npx, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    ST_CUDA_CHECK(cudaStreamSynchronize(s));
+    n_act = cnt;
+  }
+  stats->active_pixels = n_act;
+  const int64_t* act_ptr = dense ? nullptr : active;
+
+  // global active count across shards (for changed_fraction)
+  double n_act_global = (double)n_act;
+  if (reduce) {
+    double v = n_act_global;
+    if (reduce(&v, 1, reduce_user)) {
+      sthost::set_error("shard reduction failed");
+      return ST_EINVAL;
+    }
+    n_act_global = v;
+  }
+
+  const int iters = p->forced_iters > 0 ? p->forced_iters : p->max_iters;
+  const int nblk = (int)blocks_for(n_act, EM_BLOCK);
+  int last = -1;  // buffer holding the final d
+  for (int it = 1; it <= iters && it <= 64; ++it) {
+    if (n_act_global == 0) {
+      stats->converged_after = 0;
+      break;
+    }
+    stats->iterations_run = it;
+    double* d_cur = dbuf[it & 1];
+    const double* d_prev = it > 1 ? dbuf[(it - 1) & 1] : nullptr;
+    if (n_act > 0) {
+      st::MStepArgs a = {};
+      a.active = act_ptr;
+      a.n = n_act;
+      a.static_all = static_bits;
+      a.d_prev = d_prev;
+      a.d_out = d_cur;
+      a.e_out = e_act;
+      a.status_out = st_act;
+      a.partials = partials;
+      ev.record(0, s);
+      st::k_m_step<<<nblk, EM_BLOCK, 0, s>>>(c, a);
+      ST_LAUNCH_CHECK("k_m_step");
+      ev.record(1, s);
+      st::k_reduce_partials<<<1, 256, 0, s>>>(partials, nblk, reduced + it);
+      ST_LAUNCH_CHECK("k_reduce_partials");
+      ev.record(2, s);
+      stats->kernel_launches[0] += 1;
+      stats->kernel_launches[1] += 1;
+      stats->kernel_launches[3] += 1;
+      // E-step on solved pixels, in place (each pixel owns its slot)
+      st::EStepArgs e = {};
+      e.pix = act_ptr;
+      e.n = n_act;
+      e.d = d_cur;
+      e.status = st_act;
+      e.static_out = static_bits;
+      e.valid_out = valid_bits;
+      e.scatter = 1;
+      st::k_e_step_at<<<blocks_for(n_act, ESTEP_BLOCK), ESTEP_BLOCK, estep_smem(rig->num_views),
+                        s>>>(c, e);
+      ST_LAUNCH_CHECK("k_e_step_at");
+      ev.record(3, s);
+    } else {
+      ST_CUDA_CHECK(cudaMemsetAsync(reduced + it, 0, sizeof(st::Partial), s));
+    }
+    last = it & 1;
+    st::Partial r;
+    ST_CUDA_CHECK(cudaMemcpyAsync(&r, reduced + it, sizeof(r), cudaMemcpyDeviceToHost, s));
+    ST_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (n_act > 0) {
+      stats->kernel_ms[0] += ev.ms(0, 1);
+      stats->kernel_ms[3] += ev.ms(1, 2);
+      stats->kernel_ms[1] += ev.ms(2, 3);
+    }
+    if (it == 1) stats->kernel_ms[2] += ev.ms(4, 5);
+    double v[7] = {r.sum_e, (double)r.n_fin, r.sum_pe, (double)r.n_pfin, (double)r.n_changed,
+                   (double)r.n_cand, (double)r.n_eval};
+    if (reduce && reduce(v, 7, reduce_user)) {
+      sthost::set_error("shard reduction failed");
+      return ST_EINVAL;
+    }
+    stats->mean_energy[it - 1] = v[1] > 0 ? v[0] / v[1] : NAN;
+    stats->candidates_total += (int64_t)v[5];
+    stats->energy_evals += (int64_t)v[6];
+    stats->prev_evals += (int64_t)v[3];
+    if (it > 1) {
+      stats->prev_energy[it - 2] = v[3] > 0 ? v[2] / v[3] : NAN;
+      const double changed = v[4] / n_act_global;
+      stats->changed_fraction[it - 2] = changed;
+      if (p->forced_iters <= 0 && changed < 1e-3) {
+        stats->converged_after = it - 1;
+        break;
+      }
+    }
+  }
+
+  // outputs (solver.py:491-500)
+  if (dense) {
+    st::k_pack_outputs<<<blocks_for(npx, 256), 256, 0, s>>>(
+        f->mu, npx, nullptr, npx, last >= 0 ? dbuf[last] : nullptr, st_act, values, status, 1);
+    ST_LAUNCH_CHECK("k_pack_outputs");
+  } else {
+    st::k_fill_mu<<<blocks_for(npx, 256), 256, 0, s>>>(f->mu, npx, values, status);
+    ST_LAUNCH_CHECK("k_fill_mu");
+    if (last >= 0 && n_act > 0) {
+      st::k_pack_outputs<<<blocks_for(n_act, 256), 256, 0, s>>>(f->mu, npx, active, n_act,
+                                                                dbuf[last], st_act, values,
+                                                                status, 0);
+      ST_LAUNCH_CHECK("k_pack_outputs");
+    }
+  }
+  return ST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// Shared device helpers for the seethrough_b200 kernels (sm_100a).
+//
+// Numerics follow the reference recipe bit for bit where IEEE allows it:
+// every fp64 product/sum is an explicit __dmul_rn/__dadd_rn (no FMA
+// contraction), evaluation order is the reference's left-to-right order.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/seethrough_b200.h"
+
+#define ST_TW 32  // support tile width  (pixels)
+#define ST_TH 8   // support tile height (pixels)
+
+namespace st {
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// Exact small-integer -> double through the 2^52 magic constant: one DADD
+// instead of an I2F conversion.  Valid for -2^31 < x < 2^31.
+__device__ __forceinline__ double i2d_exact(int x) {
+  return __dsub_rn(__hiloint2double(0x43300000, (unsigned)(x + 0x40000000)),
+                   4503600701112320.0);  // 2^52 + 2^30
+}
+__device__ __forceinline__ double u8d(uint32_t word, int byte) {
+  return __dsub_rn(__hiloint2double(0x43300000, __byte_perm(word, 0u, 0x4440 | byte)),
+                   4503599627370496.0);  // 2^52
+}
+
+// geometry.py:204-219 -- h = A (u, v, 1) + d b, left to right, separate roundings.
+struct WarpOut {
+  double pu, pv;
+  bool front;
+};
+
+__device__ __forceinline__ WarpOut warp_to(const st_rig& r, int k, double u, double v, double d) {
+  const double* a = r.warp_a[k];
+  const double* b = r.warp_b[k];
+  double hx = dadd(dadd(dadd(dmul(a[0], u), dmul(a[1], v)), a[2]), dmul(d, b[0]));
+  double hy = dadd(dadd(dadd(dmul(a[3], u), dmul(a[4], v)), a[5]), dmul(d, b[1]));
+  double hz = dadd(dadd(dadd(dmul(a[6], u), dmul(a[7], v)), a[8]), dmul(d, b[2]));
+  WarpOut o;
+  o.front = hz > 0.0;
+  if (hz == 1.0) {  // rectified rigs: x / 1 == x exactly
+    o.pu = hx;
+    o.pv = hy;
+  } else {
+    o.pu = ddiv(hx, hz);
+    o.pv = ddiv(hy, hz);
+  }
+  return o;
+}
+
+// solver.py:197-204 -- descriptor-support margin test on rig dims.
+__device__ __forceinline__ bool in_margin(const st_rig& r, int k, const WarpOut& w) {
+  const double m = (double)ST_DESC_MARGIN;
+  return w.front && w.pu >= m && w.pu <= (double)(r.view_w[k] - ST_DESC_MARGIN - 1) &&
+         w.pv >= m && w.pv <= (double)(r.view_h[k] - ST_DESC_MARGIN - 1);
+}
+
+// sampling.py:21-55 tap selection: nan/inf -> 0, clip, floor, min(., n-2).
+struct Taps {
+  int iu, iv;        // top-left tap
+  int su, sv;        // steps to the right / lower tap (0 on 1-px axes)
+  double fu, fv;     // fp64 weights
+};
+
+__device__ __forceinline__ double clean_coord(double x, double hi) {
+  if (!isfinite(x)) x = 0.0;   // nan_to_num(nan=0, posinf=0, neginf=0)
+  return fmin(fmax(x, 0.0), hi);
+}
+
+__device__ __forceinline__ Taps taps_of(double u, double v, int w, int h) {
+  Taps t;
+  u = clean_coord(u, (double)w - 1.0);
+  v = clean_coord(v, (double)h - 1.0);
+  double fiu = w > 1 ? fmin(floor(u), (double)w - 2.0) : 0.0;
+  double fiv = h > 1 ? fmin(floor(v), (double)h - 2.0) : 0.0;
+  t.fu = dsub(u, fiu);
+  t.fv = dsub(v, fiv);
+  t.iu = (int)fiu;
+  t.iv = (int)fiv;
+  t.su = w > 1 ? 1 : 0;
+  t.sv = h > 1 ? w : 0;
+  return t;
+}
+
+// fp64 lerp of fp32 taps with an fp32 tap difference (sampling.py:49-55).
+__device__ __forceinline__ double lerp_f32(float g0, float g1, double f) {
+  return dadd((double)g0, dmul(f, (double)__fsub_rn(g1, g0)));
+}
+
+// One byte channel of a descriptor / colour, exact integer taps.
+__device__ __forceinline__ double lerp_u8(int g0, int g1, double f) {
+  return dadd(i2d_exact(g0), dmul(f, i2d_exact(g1 - g0)));
+}
+
+// prior.py:365-370 -- log(gamma + exp(-z^2/2)), z = (d - mu)/sigma.
+__device__ __forceinline__ double log_prior(double d, double mu, double sigma, double gamma) {
+  double z = ddiv(dsub(d, mu), sigma);
+  return log(dadd(gamma, exp(dmul(dmul(-0.5, z), z))));
+}
+
+__device__ __forceinline__ double variance_ceiling() { return 16.0 * 127.5 * 127.5; }
+
+}  // namespace st
+
+// CUDA error plumbing shared by the host side of every .cu file.
+namespace sthost {
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+void count_launch();
+}  // namespace sthost
+
+#define ST_CUDA_CHECK(call)                                       \
+  do {                                                            \
+    cudaError_t _e = (call);                                      \
+    if (_e != cudaSuccess) return sthost::cuda_fail(_e, #call);   \
+  } while (0)
+
+// Every kernel launch site is followed by ST_LAUNCH_CHECK: it both checks the
+// launch and counts it for st_launch_count().
+#define ST_LAUNCH_CHECK(name)                                     \
+  do {                                                            \
+    sthost::count_launch();                                       \
+    cudaError_t _e = cudaGetLastError();                          \
+    if (_e != cudaSuccess) return sthost::cuda_fail(_e, name);    \
+  } while (0)

@@ -1,0 +1,679 @@
+// EM core of the seethrough_b200 hot path (sm_100a).
+//
+// Reference: solver.py (DisparitySolver) -- gather_rays :206-227, _energy
+// :229-260, m_step :325-407, e_step :115-157, e_step_at :409-419,
+// initial_masks :421-432.  One thread owns one reference pixel (the
+// reference's per-pixel independence, solver.py:30-32); candidate energies
+// never leave registers (no cost volume in HBM).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "st_common.cuh"
+#include "st_em.cuh"
+
+namespace st {
+
+// ---------------------------------------------------------------------------
+// sampling
+
+// 16-channel bilinear descriptor sample, fp64 recipe (sampling.py:49-55 on
+// the float32 copy of the uint8 map: tap differences are exact integers).
+// Calls `sink(c, f)` for each channel in order.
+template <typename Sink>
+__device__ __forceinline__ void sample_desc(const uint4* __restrict__ plane, int W, const Taps& t,
+                                            Sink&& sink) {
+  const size_t base = (size_t)t.iv * W + t.iu;
+  const uint4 a = __ldg(plane + base);
+  const uint4 b = __ldg(plane + base + t.su);
+  const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+  const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+  if (t.fv == 0.0) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const int g0 = (aw[c >> 2] >> (8 * (c & 3))) & 0xff;
+      const int g1 = (bw[c >> 2] >> (8 * (c & 3))) & 0xff;
+      sink(c, lerp_u8(g0, g1, t.fu));
+    }
+  } else {
+    const uint4 e = __ldg(plane + base + t.sv);
+    const uint4 g = __ldg(plane + base + t.sv + t.su);
+    const uint32_t ew[4] = {e.x, e.y, e.z, e.w};
+    const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const int sh = 8 * (c & 3);
+      const double top = lerp_u8((aw[c >> 2] >> sh) & 0xff, (bw[c >> 2] >> sh) & 0xff, t.fu);
+      const double bot = lerp_u8((ew[c >> 2] >> sh) & 0xff, (gw[c >> 2] >> sh) & 0xff, t.fu);
+      sink(c, dadd(top, dmul(t.fv, dsub(bot, top))));
+    }
+  }
+}
+
+// Prior-plane sample (float32 plane, one channel).
+__device__ __forceinline__ double sample_prior(const float* __restrict__ plane, int W,
+                                               const Taps& t) {
+  const size_t base = (size_t)t.iv * W + t.iu;
+  const double top = lerp_f32(__ldg(plane + base), __ldg(plane + base + t.su), t.fu);
+  if (t.fv == 0.0) return top;
+  const double bot =
+      lerp_f32(__ldg(plane + base + t.sv), __ldg(plane + base + t.sv + t.su), t.fu);
+  return dadd(top, dmul(t.fv, dsub(bot, top)));
+}
+
+// ---------------------------------------------------------------------------
+// energy (solver.py:229-260)
+
+struct Energy {
+  double e;
+  bool real;
+};
+
+__device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, double d,
+                                            uint32_t bits, double mu) {
+  double s1[16], s2[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    s1[i] = 0.0;
+    s2[i] = 0.0;
+  }
+  int cnt = 0;
+  for (int k = 0; k < c.rig.num_views; ++k) {
+    if (!((bits >> k) & 1u)) continue;
+    const WarpOut w = warp_to(c.rig, k, u, v, d);
+    if (!in_margin(c.rig, k, w)) continue;
+    const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
+    sample_desc(c.desc + (size_t)k * c.HW, c.W, t, [&](int ch, double f) {
+      s1[ch] = dadd(s1[ch], f);
+      s2[ch] = dadd(s2[ch], dmul(f, f));
+    });
+    ++cnt;
+  }
+  Energy out;
+  out.real = cnt >= c.p.min_static_rays;
+  double var;
+  if (out.real) {
+    const double nn = (double)(cnt > 1 ? cnt : 1);
+    double t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = dsub(s2[i], ddiv(dmul(s1[i], s1[i]), nn));
+    // numpy's contiguous 16-wide reduction: r_j = t_j + t_{j+8}, then the
+    // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) tree.
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = dadd(t[j], t[j + 8]);
+    const double sum = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])),
+                            dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+    var = fmax(ddiv(sum, nn), 0.0);
+  } else {
+    var = variance_ceiling();
+  }
+  out.e = dsub(dmul(c.p.beta, var), log_prior(d, mu, c.p.sigma, c.p.gamma));
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// block-deterministic reductions
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Sum over the block in a fixed order; result valid in thread 0.
+template <typename T>
+__device__ T block_sum(T x, T* smem) {
+  x = warp_sum(x);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) smem[wid] = x;
+  __syncthreads();
+  T s = T(0);
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int i = 0; i < nw; ++i) s += smem[i];
+  }
+  __syncthreads();
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// M-step (solver.py:325-407), with the iteration bookkeeping of solve()
+// (solver.py:463-475) fused in: energy of the previous disparity under the
+// current masks and the changed count.
+
+__global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
+  __shared__ double sh_d[EM_BLOCK / 32];
+  __shared__ long long sh_i[EM_BLOCK / 32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < a.n;
+
+  double e_fin = 0.0, pe_fin = 0.0;
+  long long n_fin = 0, n_pfin = 0, n_changed = 0, n_cand = 0, n_eval = 0;
+
+  if (live) {
+    const int64_t pix = a.active ? a.active[i] : i;
+    const int x = (int)(pix % c.W), y = (int)(pix / c.W);
+    const double u = (double)x, v = (double)y;
+    const double mu = c.mu[pix];
+    const uint32_t bits = a.static_all[pix];
+    const double dmax = c.p.d_max;
+
+    double be = INFINITY, bd = INFINITY;
+    bool br = false;
+    auto offer = [&](double d) {
+      ++n_cand;
+      // -log prior bounds the energy from below (var >= 0): exact pruning
+      const double bound = -log_prior(d, mu, c.p.sigma, c.p.gamma);
+      if (!(bound <= be)) return;
+      ++n_eval;
+      const Energy E = energy_at(c, u, v, d, bits, mu);
+      if (E.e < be || (E.e == be && d < bd)) {
+        be = E.e;
+        bd = d;
+        br = E.real;
+      }
+    };
+
+    // band mu + 0.5 j, nearest first (solver.py:187-191, 360-363)
+    for (int j = 0; j < c.n_band; ++j) {
+      const double d = dadd(mu, c.band[j]);
+      if (d > 0.0 && d <= dmax) offer(d);
+    }
+    // coarse sweep 1, 5, 9, ... (solver.py:192, 364-365)
+    for (int j = 0; j < c.n_coarse; ++j) offer(dadd(1.0, dmul(4.0, (double)j)));
+    // support disparities within the radius (solver.py:286-321, 373-400)
+    if (c.sup_tile_start) {
+      const int tile = (y / ST_TH) * c.tiles_x + (x / ST_TW);
+      const uint32_t r1 = c.sup_tile_start[tile + 1];
+      uint32_t r = c.sup_tile_start[tile];
+      const int ir = c.sup_ir;
+      while (r < r1) {
+        const float val = c.sup_value[r];
+        bool hit = false;
+        do {
+          if (!hit) {
+            const uint32_t uv = c.sup_uv[r];
+            const int dx = x - (int)(int16_t)(uv & 0xffffu);
+            const int dy = y - (int)(int16_t)(uv >> 16);
+            hit = abs(dx) <= ir && abs(dy) <= ir && (double)(dx * dx + dy * dy) <= c.sup_r2;
+          }
+          ++r;
+        } while (r < r1 && c.sup_value[r] == val);
+        if (hit) offer((double)val);
+      }
+    }
+
+    uint8_t status = ST_STATUS_VALID;
+    if (!isfinite(be)) {
+      status = ST_STATUS_LOW_TEXTURE;
+      bd = NAN;
+    } else if (!br) {
+      status = ST_STATUS_NO_STATIC_EVIDENCE;
+    }
+    a.d_out[i] = bd;
+    a.e_out[i] = be;
+    a.status_out[i] = status;
+    if (isfinite(be)) {
+      e_fin = be;
+      n_fin = 1;
+    }
+    if (a.d_prev) {
+      const double dp = a.d_prev[i];
+      if (!isnan(dp)) {
+        const Energy P = energy_at(c, u, v, dp, bits, mu);
+        if (isfinite(P.e)) {
+          pe_fin = P.e;
+          n_pfin = 1;
+        }
+      }
+      // |d - d_prev| > 0.5 with NaN -> False (solver.py:472-475)
+      if (fabs(bd - dp) > 0.5) n_changed = 1;
+    }
+  }
+  if (a.partials) {
+    const double s_e = block_sum(e_fin, sh_d);
+    const double s_pe = block_sum(pe_fin, sh_d);
+    const long long c_fin = block_sum(n_fin, sh_i);
+    const long long c_pfin = block_sum(n_pfin, sh_i);
+    const long long c_ch = block_sum(n_changed, sh_i);
+    const long long c_cand = block_sum(n_cand, sh_i);
+    const long long c_eval = block_sum(n_eval, sh_i);
+    if (threadIdx.x == 0) {
+      Partial& P = a.partials[blockIdx.x];
+      P.sum_e = s_e;
+      P.sum_pe = s_pe;
+      P.n_fin = c_fin;
+      P.n_pfin = c_pfin;
+      P.n_changed = c_ch;
+      P.n_cand = c_cand;
+      P.n_eval = c_eval;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// E-step (solver.py:115-157)
+
+// Gathered ray state for one pixel; descriptors live in shared memory,
+// element (k, ch) of thread t at smem[(k * 16 + ch) * blockDim + t].
+struct RayPriors {
+  double l1[ST_MAX_VIEWS];
+  double l0[ST_MAX_VIEWS];
+};
+
+__device__ __forceinline__ void clamp_logs(double q, double eps, double& l1, double& l0) {
+  const double qc = fmin(fmax(q, eps), dsub(1.0, eps));  // np.clip(q, eps, 1 - eps)
+  l1 = log(qc);
+  l0 = log(dsub(1.0, qc));
+}
+
+// Mask preference (solver.py:110-112, 156): higher score, then larger
+// popcount, then smaller encoding -- the first maximum in _mask_order.
+__device__ __forceinline__ bool prefer(double s, int pop, uint32_t m, double bs, int bpop,
+                                       uint32_t bm) {
+  if (s > bs) return true;
+  if (s < bs || !(s == bs)) return false;
+  if (pop != bpop) return pop > bpop;
+  return m < bm;
+}
+
+__device__ __forceinline__ double div_n(double x, int n) {
+  // powers of two scale exactly; other counts need the IEEE division
+  switch (n) {
+    case 1: return x;
+    case 2: return dmul(x, 0.5);
+    case 4: return dmul(x, 0.25);
+    case 8: return dmul(x, 0.125);
+    default: return ddiv(x, (double)n);
+  }
+}
+
+// Register path for K <= 5 (<= 32 masks, fully unrolled).
+template <int K>
+__device__ __forceinline__ uint32_t estep_small(const double* __restrict__ f, int stride,
+                                                const double* l1, const double* l0,
+                                                uint32_t vbits, const st_params& p) {
+  constexpr int M = 1 << K;
+  double var[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) var[m] = 0.0;
+  for (int ch = 0; ch < 16; ++ch) {
+    double fk[K], sq[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      fk[k] = f[(k * 16 + ch) * stride];
+      sq[k] = dmul(fk[k], fk[k]);
+    }
+#pragma unroll
+    for (int m = 1; m < M; ++m) {
+      double a1 = 0.0, a2 = 0.0;
+      int n = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if ((m >> k) & 1) {
+          a1 = n ? dadd(a1, fk[k]) : fk[k];
+          a2 = n ? dadd(a2, sq[k]) : sq[k];
+          ++n;
+        }
+      // (s2 - s1*s1/n), summed over channels in order (axis-1 reduce)
+      var[m] = dadd(var[m], dsub(a2, div_n(dmul(a1, a1), n)));
+    }
+  }
+  double best = -INFINITY;
+  int bpop = -1;
+  uint32_t bm = 0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    if ((uint32_t)m & ~vbits) continue;  // touches an invalid ray
+    const int pop = __popc(m);
+    double vr;
+    if (pop < p.min_static_rays) {
+      vr = variance_ceiling();
+    } else {
+      vr = fmax(div_n(var[m], pop > 0 ? pop : 1), 0.0);
+    }
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if ((m >> k) & 1)
+        a = dadd(a, l1[k]);
+      else
+        b = dadd(b, l0[k]);
+    }
+    const double s = dsub(dadd(a, b), dmul(p.beta, vr));
+    if (prefer(s, pop, (uint32_t)m, best, bpop, bm)) {
+      best = s;
+      bpop = pop;
+      bm = (uint32_t)m;
+    }
+  }
+  return bm;
+}
+
+// Generic path for 6 <= K <= 12: one mask at a time, same arithmetic order.
+__device__ uint32_t estep_generic(int K, const double* __restrict__ f, int stride,
+                                  const double* l1, const double* l0, uint32_t vbits,
+                                  const st_params& p) {
+  const uint32_t M = 1u << K;
+  double best = -INFINITY;
+  int bpop = -1;
+  uint32_t bm = 0;
+  for (uint32_t m = 0; m < M; ++m) {
+    if (m & ~vbits) continue;
+    const int pop = __popc(m);
+    double vr;
+    if (pop < p.min_static_rays) {
+      vr = variance_ceiling();
+    } else {
+      double acc = 0.0;
+      for (int ch = 0; ch < 16; ++ch) {
+        double a1 = 0.0, a2 = 0.0;
+        int n = 0;
+        for (uint32_t r = m; r; r &= r - 1) {
+          const int k = __ffs(r) - 1;
+          const double x = f[(k * 16 + ch) * stride];
+          a1 = n ? dadd(a1, x) : x;
+          const double x2 = dmul(x, x);
+          a2 = n ? dadd(a2, x2) : x2;
+          ++n;
+        }
+        acc = dadd(acc, dsub(a2, div_n(dmul(a1, a1), n)));
+      }
+      vr = fmax(div_n(acc, pop), 0.0);
+    }
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < K; ++k) {
+      if ((m >> k) & 1)
+        a = dadd(a, l1[k]);
+      else
+        b = dadd(b, l0[k]);
+    }
+    const double s = dsub(dadd(a, b), dmul(p.beta, vr));
+    if (prefer(s, pop, m, best, bpop, bm)) {
+      best = s;
+      bpop = pop;
+      bm = m;
+    }
+  }
+  return bm;
+}
+
+__device__ __forceinline__ uint32_t estep_dispatch(int K, const double* f, int stride,
+                                                   const double* l1, const double* l0,
+                                                   uint32_t vbits, const st_params& p) {
+  switch (K) {
+    case 2: return estep_small<2>(f, stride, l1, l0, vbits, p);
+    case 3: return estep_small<3>(f, stride, l1, l0, vbits, p);
+    case 4: return estep_small<4>(f, stride, l1, l0, vbits, p);
+    case 5: return estep_small<5>(f, stride, l1, l0, vbits, p);
+    default: return estep_generic(K, f, stride, l1, l0, vbits, p);
+  }
+}
+
+// Gather one pixel's rays at disparity d into smem (solver.py:206-227) and
+// return the valid bits; q of invalid rays is 0.5, descriptors 0.
+__device__ __forceinline__ uint32_t gather_pixel(const EmCtx& c, double u, double v, double d,
+                                                 double* f, int stride, double* q) {
+  uint32_t vb = 0;
+  for (int k = 0; k < c.rig.num_views; ++k) {
+    const WarpOut w = warp_to(c.rig, k, u, v, d);
+    if (in_margin(c.rig, k, w)) {
+      const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
+      sample_desc(c.desc + (size_t)k * c.HW, c.W, t,
+                  [&](int ch, double x) { f[(k * 16 + ch) * stride] = x; });
+      q[k] = sample_prior(c.priors + (size_t)k * c.HW, c.W, t);
+      vb |= 1u << k;
+    } else {
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) f[(k * 16 + ch) * stride] = 0.0;
+      q[k] = 0.5;
+    }
+  }
+  return vb;
+}
+
+__global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a) {
+  extern __shared__ double sh_f[];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) return;  // solver.py:476-478
+  const int64_t pix = a.pix ? a.pix[i] : i;
+  const double u = (double)(pix % c.W), v = (double)(pix / c.W);
+  double* f = sh_f + threadIdx.x;
+  double q[ST_MAX_VIEWS], l1[ST_MAX_VIEWS], l0[ST_MAX_VIEWS];
+  const uint32_t vb = gather_pixel(c, u, v, a.d[i], f, blockDim.x, q);
+  for (int k = 0; k < c.rig.num_views; ++k) clamp_logs(q[k], c.p.epsilon_prior, l1[k], l0[k]);
+  const uint32_t m = estep_dispatch(c.rig.num_views, f, blockDim.x, l1, l0, vb, c.p);
+  const int64_t o = a.scatter ? pix : i;
+  a.static_out[o] = m;
+  a.valid_out[o] = vb;
+}
+
+// initial_masks (solver.py:421-432): valid & q >= threshold at mu.
+__global__ void k_initial_masks(EmCtx c, const int64_t* __restrict__ pix_list, int64_t n,
+                                uint32_t* __restrict__ static_out,
+                                uint32_t* __restrict__ valid_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t pix = pix_list ? pix_list[i] : i;
+  const double u = (double)(pix % c.W), v = (double)(pix / c.W);
+  const double d = c.mu[pix];
+  uint32_t sb = 0, vb = 0;
+  for (int k = 0; k < c.rig.num_views; ++k) {
+    const WarpOut w = warp_to(c.rig, k, u, v, d);
+    if (!in_margin(c.rig, k, w)) continue;
+    const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
+    const double q = sample_prior(c.priors + (size_t)k * c.HW, c.W, t);
+    vb |= 1u << k;
+    if (q >= c.p.threshold) sb |= 1u << k;
+  }
+  static_out[i] = sb;
+  valid_out[i] = vb;
+}
+
+// gather_rays API (solver.py:206-227).
+__global__ void k_gather_rays(EmCtx c, const int64_t* __restrict__ pix, const double* __restrict__ d,
+                              int64_t n, double* __restrict__ desc, uint8_t* __restrict__ valid,
+                              double* __restrict__ q) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int K = c.rig.num_views;
+  const int64_t p = pix[i];
+  const double u = (double)(p % c.W), v = (double)(p / c.W);
+  for (int k = 0; k < K; ++k) {
+    double* out = desc + ((size_t)i * K + k) * 16;
+    const WarpOut w = warp_to(c.rig, k, u, v, d[i]);
+    if (in_margin(c.rig, k, w)) {
+      const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
+      sample_desc(c.desc + (size_t)k * c.HW, c.W, t, [&](int ch, double x) { out[ch] = x; });
+      q[(size_t)i * K + k] = sample_prior(c.priors + (size_t)k * c.HW, c.W, t);
+      valid[(size_t)i * K + k] = 1;
+    } else {
+      for (int ch = 0; ch < 16; ++ch) out[ch] = 0.0;
+      q[(size_t)i * K + k] = 0.5;
+      valid[(size_t)i * K + k] = 0;
+    }
+  }
+}
+
+// _energy API (solver.py:229-260) on explicit (pixel, d, mask) triples.
+__global__ void k_energy(EmCtx c, const int64_t* __restrict__ pix, const double* __restrict__ d,
+                         const uint32_t* __restrict__ bits, int64_t n, double* __restrict__ e,
+                         uint8_t* __restrict__ real) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t p = pix[i];
+  const Energy E = energy_at(c, (double)(p % c.W), (double)(p / c.W), d[i], bits[i], c.mu[p]);
+  e[i] = E.e;
+  real[i] = E.real ? 1 : 0;
+}
+
+// Standalone e_step on caller-gathered rays (n, K, 16) f64.
+__global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_rays(const double* __restrict__ desc,
+                                                             const uint8_t* __restrict__ valid,
+                                                             const double* __restrict__ q, int64_t n,
+                                                             int K, st_params p,
+                                                             uint32_t* __restrict__ out) {
+  extern __shared__ double sh_f[];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* f = sh_f + threadIdx.x;
+  double l1[ST_MAX_VIEWS], l0[ST_MAX_VIEWS];
+  uint32_t vb = 0;
+  for (int k = 0; k < K; ++k) {
+    for (int ch = 0; ch < 16; ++ch) f[(k * 16 + ch) * blockDim.x] = desc[((size_t)i * K + k) * 16 + ch];
+    if (valid[(size_t)i * K + k]) vb |= 1u << k;
+    clamp_logs(q[(size_t)i * K + k], p.epsilon_prior, l1[k], l0[k]);
+  }
+  out[i] = estep_dispatch(K, f, blockDim.x, l1, l0, vb, p);
+}
+
+// masked_variance (solver.py:93-107): two-pass in double precision.
+__global__ void k_masked_variance(const double* __restrict__ desc, const uint8_t* __restrict__ mask,
+                                  int64_t n, int K, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int cnt = 0;
+  for (int k = 0; k < K; ++k) cnt += mask[(size_t)i * K + k] ? 1 : 0;
+  if (cnt == 0) {
+    out[i] = NAN;
+    return;
+  }
+  // sel.sum(axis=0) / n: pairwise over rows is sequential for < 8 rows;
+  // numpy sums axis 0 of a (n, 16) array row by row.
+  double mean[16];
+  for (int ch = 0; ch < 16; ++ch) mean[ch] = 0.0;
+  bool first = true;
+  for (int k = 0; k < K; ++k) {
+    if (!mask[(size_t)i * K + k]) continue;
+    for (int ch = 0; ch < 16; ++ch) {
+      const double x = desc[((size_t)i * K + k) * 16 + ch];
+      mean[ch] = first ? x : dadd(mean[ch], x);
+    }
+    first = false;
+  }
+  for (int ch = 0; ch < 16; ++ch) mean[ch] = ddiv(mean[ch], (double)cnt);
+  // ((sel - mean) ** 2).sum(): one contiguous reduction over cnt*16 values
+  // (numpy pairwise: 8 accumulators over blocks of 128, then the tree).
+  double acc[8];
+  for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+  const int total = cnt * 16;
+  int idx = 0;
+  double tail = 0.0;
+  bool tail_first = true;
+  const int main_n = total < 8 ? 0 : total - (total % 8);
+  for (int k = 0; k < K; ++k) {
+    if (!mask[(size_t)i * K + k]) continue;
+    for (int ch = 0; ch < 16; ++ch, ++idx) {
+      const double dlt = dsub(desc[((size_t)i * K + k) * 16 + ch], mean[ch]);
+      const double sq = dmul(dlt, dlt);
+      if (idx < main_n) {
+        acc[idx & 7] = idx < 8 ? sq : dadd(acc[idx & 7], sq);
+      } else {
+        tail = tail_first ? sq : dadd(tail, sq);
+        tail_first = false;
+      }
+    }
+  }
+  double s = dadd(dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3])),
+                  dadd(dadd(acc[4], acc[5]), dadd(acc[6], acc[7])));
+  if (!tail_first) s = dadd(s, tail);
+  out[i] = ddiv(s, (double)cnt);
+}
+
+// solve() output packing (solver.py:491-500).
+__global__ void k_pack_outputs(const double* __restrict__ mu, int64_t npx,
+                               const int64_t* __restrict__ active, int64_t n_active,
+                               const double* __restrict__ d_act,
+                               const uint8_t* __restrict__ st_act, float* __restrict__ values,
+                               uint8_t* __restrict__ status, int dense) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (dense) {
+    if (i >= npx) return;
+    if (d_act) {
+      const double d = d_act[i];
+      values[i] = isnan(d) ? 0.0f : (float)d;
+      status[i] = st_act[i];
+    } else {
+      values[i] = (float)mu[i];
+      status[i] = ST_STATUS_VALID;
+    }
+    return;
+  }
+  // sparse: first pass (fill) is done by k_fill_mu; scatter active results
+  if (i >= n_active || !d_act) return;
+  const int64_t p = active[i];
+  const double d = d_act[i];
+  values[p] = isnan(d) ? 0.0f : (float)d;
+  status[p] = st_act[i];
+}
+
+__global__ void k_fill_mu(const double* __restrict__ mu, int64_t npx, float* __restrict__ values,
+                          uint8_t* __restrict__ status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npx) return;
+  values[i] = (float)mu[i];
+  status[i] = ST_STATUS_VALID;
+}
+
+// Fixed-order sum of the per-block partials into slot `it` of the stats.
+__global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
+                                  Partial* __restrict__ out) {
+  __shared__ double sd[2][256];
+  __shared__ long long si[5][256];
+  double a = 0.0, b = 0.0;
+  long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+  // thread t sums parts t, t+256, ... in order
+  for (int j = threadIdx.x; j < nparts; j += blockDim.x) {
+    a += parts[j].sum_e;
+    b += parts[j].sum_pe;
+    c0 += parts[j].n_fin;
+    c1 += parts[j].n_pfin;
+    c2 += parts[j].n_changed;
+    c3 += parts[j].n_cand;
+    c4 += parts[j].n_eval;
+  }
+  sd[0][threadIdx.x] = a;
+  sd[1][threadIdx.x] = b;
+  si[0][threadIdx.x] = c0;
+  si[1][threadIdx.x] = c1;
+  si[2][threadIdx.x] = c2;
+  si[3][threadIdx.x] = c3;
+  si[4][threadIdx.x] = c4;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Partial r = {};
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      r.sum_e += sd[0][t];
+      r.sum_pe += sd[1][t];
+      r.n_fin += si[0][t];
+      r.n_pfin += si[1][t];
+      r.n_changed += si[2][t];
+      r.n_cand += si[3][t];
+      r.n_eval += si[4][t];
+    }
+    *out = r;
+  }
+}
+
+// dynamic_only / explicit active-set compaction: count then scatter, in
+// pixel order (the reference's `active` is ascending).
+__global__ void k_flag_active(const float* __restrict__ ref_prior, const uint8_t* __restrict__ mask,
+                              int64_t npx, double threshold, uint32_t* __restrict__ flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npx) return;
+  // numpy compares the float32 prior against the Python float in float32 (NEP 50)
+  flags[i] = mask ? (mask[i] ? 1u : 0u) : (ref_prior[i] < (float)threshold ? 1u : 0u);
+}
+
+__global__ void k_scatter_active(const uint32_t* __restrict__ flags,
+                                 const uint32_t* __restrict__ offs, int64_t npx,
+                                 int64_t* __restrict__ active) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npx) return;
+  if (flags[i]) active[offs[i]] = i;
+}
+
+}  // namespace st

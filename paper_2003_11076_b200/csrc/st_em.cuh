@@ -1,0 +1,82 @@
+// Kernel-side context and kernel declarations of the EM core.
+#pragma once
+
+#include <stdint.h>
+
+#include "st_common.cuh"
+
+#define EM_BLOCK 128
+#define ESTEP_BLOCK 64
+#define ST_MAX_BAND 64
+
+namespace st {
+
+// Everything a pixel thread needs, passed by value (lands in the constant bank).
+struct EmCtx {
+  st_rig rig;
+  st_params p;
+  int W, H;
+  int64_t HW;
+  const uint4* desc;     // (K, H*W) 16-byte descriptors
+  const float* priors;   // (K, H*W)
+  const double* mu;      // (H*W) clipped surface
+  double band[ST_MAX_BAND];
+  int n_band;
+  int n_coarse;
+  const uint32_t* sup_tile_start;
+  const float* sup_value;
+  const uint32_t* sup_uv;
+  int tiles_x;
+  int sup_ir;
+  double sup_r2;
+};
+
+struct Partial {
+  double sum_e, sum_pe;
+  long long n_fin, n_pfin, n_changed, n_cand, n_eval;
+};
+
+struct MStepArgs {
+  const int64_t* active;     // nullable: dense over all pixels
+  int64_t n;
+  const uint32_t* static_all;
+  const double* d_prev;      // nullable: first iteration
+  double* d_out;
+  double* e_out;
+  uint8_t* status_out;
+  Partial* partials;         // nullable: one per block
+};
+
+struct EStepArgs {
+  const int64_t* pix;        // nullable: dense
+  int64_t n;
+  const double* d;
+  const uint8_t* status;     // nullable; LOW_TEXTURE rows are skipped
+  uint32_t* static_out;
+  uint32_t* valid_out;
+  int scatter;               // 1: write at pixel index, 0: at row i
+};
+
+__global__ void k_m_step(EmCtx c, MStepArgs a);
+__global__ void k_e_step_at(EmCtx c, EStepArgs a);
+__global__ void k_initial_masks(EmCtx c, const int64_t* pix, int64_t n, uint32_t* static_out,
+                                uint32_t* valid_out);
+__global__ void k_gather_rays(EmCtx c, const int64_t* pix, const double* d, int64_t n,
+                              double* desc, uint8_t* valid, double* q);
+__global__ void k_energy(EmCtx c, const int64_t* pix, const double* d, const uint32_t* bits,
+                         int64_t n, double* e, uint8_t* real);
+__global__ void k_e_step_rays(const double* desc, const uint8_t* valid, const double* q,
+                              int64_t n, int K, st_params p, uint32_t* out);
+__global__ void k_masked_variance(const double* desc, const uint8_t* mask, int64_t n, int K,
+                                  double* out);
+__global__ void k_pack_outputs(const double* mu, int64_t npx, const int64_t* active,
+                               int64_t n_active, const double* d_act, const uint8_t* st_act,
+                               float* values, uint8_t* status, int dense);
+__global__ void k_fill_mu(const double* mu, int64_t npx, float* values, uint8_t* status);
+__global__ void k_reduce_partials(const Partial* parts, int nparts, Partial* out);
+__global__ void k_flag_active(const float* ref_prior, const uint8_t* mask, int64_t npx,
+                              double threshold, uint32_t* flags);
+__global__ void k_scatter_active(const uint32_t* flags, const uint32_t* offs, int64_t npx,
+                                 int64_t* active);
+
+}  // namespace st

@@ -1,0 +1,389 @@
+// Surface raster mu on the device (prior.py:276-310 disparity_map, then the
+// solver's clip, solver.py:185-186) -- bit-exact with the reference.
+//
+// The reference evaluates the plane of the triangle scipy's Qhull
+// `find_simplex` returns.  ~40 % of pixel centres lie on triangle edges or
+// vertices (support points sit on an integer grid), and which of the touching
+// triangles Qhull returns depends on its directed walk, which starts from the
+// simplex found for the PREVIOUS query point (raster order).  The planes of
+// the touching triangles differ by ulps, and those ulps move warped rays
+// across the integer margin boundaries downstream, so the walk is emulated
+// exactly:
+//   1. k_claim: every triangle tests the pixel centres in its bbox with
+//      Qhull's barycentric inclusion test (eps = 100 DBL_EPSILON, same
+//      arithmetic); per pixel we keep the claim count and min/max claimer.
+//      A pixel with exactly one claimer has a start-independent answer.
+//   2. k_walk_chunks: runs of ambiguous pixels are cut into chunks at pixels
+//      whose predecessor has <= 2 claimers; each chunk is walked once per
+//      possible incoming start (the predecessor's claimers), replaying
+//      _find_simplex / _find_simplex_directed step by step.
+//   3. k_resolve_runs: one thread per run links its chunks (a few lookups).
+//   4. k_mu_eval: pick the resolved simplex, evaluate its plane left to
+//      right, clip.
+#include <cuda_runtime.h>
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "st_common.cuh"
+
+namespace st {
+
+#define MU_CHUNK 32
+#define QH_EPS (100.0 * DBL_EPSILON)
+
+struct TriDev {
+  const double *pts, *disp, *planes, *transform, *equations;
+  const int32_t *simp, *nb;
+  int n_pts, n_tri;
+  double ps, psh, lo0, lo1, hi0, hi1;
+};
+
+struct MuWs {
+  unsigned *cnt, *tmin, *tmax;
+  int32_t *res0, *res1, *final_s, *chunk_of, *len, *end0, *end1;
+  uint8_t* chosen;
+};
+
+// scipy _barycentric_inside (ndim = 2), same operation order.
+__device__ __forceinline__ bool bary_inside(const double* __restrict__ T, double x0, double x1) {
+  const double eps = QH_EPS;
+  double c2 = 1.0;
+  double c0 = 0.0;
+  c0 = dadd(c0, dmul(T[0], dsub(x0, T[4])));
+  c0 = dadd(c0, dmul(T[1], dsub(x1, T[5])));
+  c2 = dsub(c2, c0);
+  if (!(-eps <= c0 && c0 <= 1.0 + eps)) return false;
+  double c1 = 0.0;
+  c1 = dadd(c1, dmul(T[2], dsub(x0, T[4])));
+  c1 = dadd(c1, dmul(T[3], dsub(x1, T[5])));
+  c2 = dsub(c2, c1);
+  if (!(-eps <= c1 && c1 <= 1.0 + eps)) return false;
+  return -eps <= c2 && c2 <= 1.0 + eps;
+}
+
+__global__ void k_claim(TriDev d, int W, int H, MuWs w) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d.n_tri) return;
+  const int a = d.simp[3 * t], b = d.simp[3 * t + 1], c = d.simp[3 * t + 2];
+  const double ax = d.pts[2 * a], ay = d.pts[2 * a + 1];
+  const double bx = d.pts[2 * b], by = d.pts[2 * b + 1];
+  const double cx = d.pts[2 * c], cy = d.pts[2 * c + 1];
+  const double* T = d.transform + 6 * t;
+  if (!(T[0] == T[0])) return;  // degenerate simplex: nan transform
+  const int x0 = max(0, (int)ceil(fmin(ax, fmin(bx, cx)) - 1e-6));
+  const int x1 = min(W - 1, (int)floor(fmax(ax, fmax(bx, cx)) + 1e-6));
+  const int y0 = max(0, (int)ceil(fmin(ay, fmin(by, cy)) - 1e-6));
+  const int y1 = min(H - 1, (int)floor(fmax(ay, fmax(by, cy)) + 1e-6));
+  for (int y = y0; y <= y1; ++y)
+    for (int x = x0; x <= x1; ++x)
+      if (bary_inside(T, (double)x, (double)y)) {
+        const size_t p = (size_t)y * W + x;
+        atomicAdd(w.cnt + p, 1u);
+        atomicMin(w.tmin + p, (unsigned)t);
+        atomicMax(w.tmax + p, (unsigned)t);
+      }
+}
+
+// scipy _distplane on the lifted point.
+__device__ __forceinline__ double distplane(const TriDev& d, int s, double z0, double z1,
+                                            double z2) {
+  const double* e = d.equations + 4 * s;
+  double dist = e[3];
+  dist = dadd(dist, dmul(e[0], z0));
+  dist = dadd(dist, dmul(e[1], z1));
+  dist = dadd(dist, dmul(e[2], z2));
+  return dist;
+}
+
+// _find_simplex + _find_simplex_directed for one query; `start` in/out.
+// The brute-force fallback (lowest-index including simplex) is the claim
+// pass's tmin.
+__device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0, double x1,
+                            int& start) {
+  const double eps = QH_EPS;
+  if (x0 < d.lo0 - eps || x0 > d.hi0 + eps || x1 < d.lo1 - eps || x1 > d.hi1 + eps) return -1;
+  if (d.n_tri <= 0) return -1;
+  double z2 = 0.0;
+  z2 = dadd(z2, dmul(x0, x0));
+  z2 = dadd(z2, dmul(x1, x1));
+  z2 = dmul(z2, d.ps);
+  z2 = dadd(z2, d.psh);
+  int s = start;
+  if (s < 0 || s >= d.n_tri) s = 0;
+  double best = distplane(d, s, x0, x1, z2);
+  bool changed = true;
+  while (changed) {
+    if (best > 0.0) break;
+    changed = false;
+    for (int k = 0; k < 3; ++k) {
+      const int m = d.nb[3 * s + k];  // s may have moved within this loop (as in scipy)
+      if (m == -1) continue;
+      const double dd = distplane(d, m, x0, x1, z2);
+      if (dd > dadd(best, dmul(eps, dadd(1.0, fabs(best))))) {
+        s = m;
+        best = dd;
+        changed = true;
+      }
+    }
+  }
+  start = s;
+  const int cycles = 1 + d.n_tri / 4;
+  for (int cyc = 0; cyc < cycles; ++cyc) {
+    if (s == -1) {
+      start = s;
+      return s;
+    }
+    const double* T = d.transform + 6 * s;
+    int inside = 1;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      double ck;
+      if (k == 0) {
+        c0 = dadd(c0, dmul(T[0], dsub(x0, T[4])));
+        c0 = dadd(c0, dmul(T[1], dsub(x1, T[5])));
+        ck = c0;
+      } else if (k == 1) {
+        c1 = dadd(c1, dmul(T[2], dsub(x0, T[4])));
+        c1 = dadd(c1, dmul(T[3], dsub(x1, T[5])));
+        ck = c1;
+      } else {
+        c2 = 1.0;
+        c2 = dsub(c2, c0);
+        c2 = dsub(c2, c1);
+        ck = c2;
+      }
+      if (ck < -eps) {
+        const int m = d.nb[3 * s + k];
+        if (m == -1) {
+          start = s;  // outside the triangulation: bail out
+          return -1;
+        }
+        s = m;
+        inside = -1;
+        break;
+      } else if (ck <= 1.0 + eps) {
+        // inside along this coordinate
+      } else {
+        inside = 0;  // outside or nan (degenerate)
+      }
+    }
+    if (inside == -1) continue;
+    if (inside == 1) {
+      start = s;
+      return s;
+    }
+    s = w.cnt[p] ? (int)w.tmin[p] : -1;  // brute force
+    start = s;
+    return s;
+  }
+  s = w.cnt[p] ? (int)w.tmin[p] : -1;  // walk did not converge: brute force
+  start = s;
+  return s;
+}
+
+__device__ __forceinline__ bool ambiguous(const MuWs& w, int64_t p) { return w.cnt[p] != 1u; }
+
+// A chunk starts at an ambiguous pixel whose predecessor is unambiguous, at
+// pixel 0, or every MU_CHUNK pixels where the predecessor has exactly two
+// claimers (then the incoming start is one of those two).
+__device__ __forceinline__ bool chunk_start(const MuWs& w, int64_t p) {
+  if (!ambiguous(w, p)) return false;
+  if (p == 0) return true;
+  if (!ambiguous(w, p - 1)) return true;
+  return (p % MU_CHUNK) == 0 && w.cnt[p - 1] == 2u;
+}
+
+__global__ void k_walk_chunks(TriDev d, int W, int64_t npx, MuWs w) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npx || !chunk_start(w, p)) return;
+  int opts[2];
+  int nopt;
+  if (p == 0) {
+    opts[0] = 0;  // find_simplex starts every batch at simplex 0
+    nopt = 1;
+  } else if (!ambiguous(w, p - 1)) {
+    opts[0] = (int)w.tmin[p - 1];
+    nopt = 1;
+  } else {
+    opts[0] = (int)w.tmin[p - 1];
+    opts[1] = (int)w.tmax[p - 1];
+    nopt = 2;
+  }
+  int64_t q = p;
+  int st0 = opts[0], st1 = nopt > 1 ? opts[1] : 0;
+  do {
+    const double x0 = (double)(q % W), x1 = (double)(q / W);
+    w.res0[q] = find_simplex(d, w, q, x0, x1, st0);
+    if (nopt > 1) w.res1[q] = find_simplex(d, w, q, x0, x1, st1);
+    w.chunk_of[q] = (int32_t)p;
+    ++q;
+  } while (q < npx && ambiguous(w, q) && !chunk_start(w, q));
+  w.len[p] = (int32_t)(q - p);
+  w.end0[p] = st0;
+  w.end1[p] = nopt > 1 ? st1 : st0;
+}
+
+__global__ void k_resolve_runs(TriDev d, int W, int64_t npx, MuWs w) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npx || !ambiguous(w, p) || (p > 0 && ambiguous(w, p - 1))) return;
+  int64_t c = p;
+  w.chosen[c] = 0;
+  int carry = w.end0[c];
+  for (;;) {
+    const int64_t nxt = c + w.len[c];
+    if (nxt >= npx || !ambiguous(w, nxt)) break;
+    // nxt starts a chunk of the same run; its predecessor has two claimers
+    uint8_t pick;
+    if ((int)w.tmin[nxt - 1] == carry) {
+      pick = 0;
+    } else if ((int)w.tmax[nxt - 1] == carry) {
+      pick = 1;
+    } else {
+      // the incoming start is not a claimer of the predecessor (never seen
+      // in practice): replay this chunk sequentially from the true start
+      int st = carry;
+      int64_t q = nxt;
+      const int64_t e = nxt + w.len[nxt];
+      for (; q < e; ++q) w.final_s[q] = find_simplex(d, w, q, (double)(q % W), (double)(q / W), st);
+      w.chosen[nxt] = 2;
+      carry = st;
+      c = nxt;
+      continue;
+    }
+    w.chosen[nxt] = pick;
+    carry = pick ? w.end1[nxt] : w.end0[nxt];
+    c = nxt;
+  }
+}
+
+__global__ void k_mu_eval(TriDev d, int W, int64_t npx, MuWs w, double clip_dmax,
+                          double* __restrict__ mu) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npx) return;
+  int s;
+  if (!ambiguous(w, p)) {
+    s = (int)w.tmin[p];
+  } else {
+    const int64_t c = w.chunk_of[p];
+    const uint8_t ch = w.chosen[c];
+    s = ch == 0 ? w.res0[p] : ch == 1 ? w.res1[p] : w.final_s[p];
+  }
+  const double u = (double)(p % W), v = (double)(p / W);
+  double m;
+  if (s >= 0) {
+    // prior.py:296: pl[:, 0] * u + pl[:, 1] * v + pl[:, 2]
+    const double* pl = d.planes + 3 * s;
+    m = dadd(dadd(dmul(pl[0], u), dmul(pl[1], v)), pl[2]);
+  } else {
+    // prior.py:298-301: nearest vertex (only reachable off the hull)
+    double best = INFINITY;
+    int bi = 0;
+    for (int i = 0; i < d.n_pts; ++i) {
+      const double dx = d.pts[2 * i] - u, dy = d.pts[2 * i + 1] - v;
+      const double d2 = dx * dx + dy * dy;
+      if (d2 < best) {
+        best = d2;
+        bi = i;
+      }
+    }
+    m = d.disp[bi];
+  }
+  if (clip_dmax > 0.0) m = fmin(fmax(m, 1e-6), clip_dmax);
+  mu[p] = m;
+}
+
+}  // namespace st
+
+namespace {
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct MuLayout {
+  size_t off[11];
+  size_t total;
+};
+
+MuLayout mu_layout(int W, int H) {
+  MuLayout L;
+  const size_t npx = (size_t)W * H;
+  size_t o = 0;
+  const size_t sz[11] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 1};
+  for (int i = 0; i < 11; ++i) {
+    L.off[i] = o;
+    o += align_up(sz[i] * npx);
+  }
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+
+extern "C" int64_t st_mu_raster_workspace(int32_t W, int32_t H) {
+  return (int64_t)mu_layout(W, H).total;
+}
+
+extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip_dmax,
+                            double* mu_out, void* workspace, int64_t workspace_bytes,
+                            void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const MuLayout L = mu_layout(W, H);
+  if ((int64_t)L.total > workspace_bytes) {
+    sthost::set_error("mu raster workspace too small");
+    return ST_ENOMEM;
+  }
+  if (tri->n_pts < 1) {
+    sthost::set_error("degenerate support set: no support points");
+    return ST_EINVAL;
+  }
+  if (!tri->neighbors || !tri->transform || !tri->equations) {
+    sthost::set_error("st_mu_raster needs the Delaunay walk tables (neighbors, transform, "
+                      "equations)");
+    return ST_EINVAL;
+  }
+  char* ws = (char*)workspace;
+  st::MuWs w;
+  w.cnt = (unsigned*)(ws + L.off[0]);
+  w.tmin = (unsigned*)(ws + L.off[1]);
+  w.tmax = (unsigned*)(ws + L.off[2]);
+  w.res0 = (int32_t*)(ws + L.off[3]);
+  w.res1 = (int32_t*)(ws + L.off[4]);
+  w.final_s = (int32_t*)(ws + L.off[5]);
+  w.chunk_of = (int32_t*)(ws + L.off[6]);
+  w.len = (int32_t*)(ws + L.off[7]);
+  w.end0 = (int32_t*)(ws + L.off[8]);
+  w.end1 = (int32_t*)(ws + L.off[9]);
+  w.chosen = (uint8_t*)(ws + L.off[10]);
+  st::TriDev d;
+  d.pts = tri->points;
+  d.disp = tri->disparities;
+  d.planes = tri->planes;
+  d.transform = tri->transform;
+  d.equations = tri->equations;
+  d.simp = tri->simplices;
+  d.nb = tri->neighbors;
+  d.n_pts = tri->n_pts;
+  d.n_tri = tri->n_tri;
+  d.ps = tri->paraboloid_scale;
+  d.psh = tri->paraboloid_shift;
+  d.lo0 = tri->min_bound[0];
+  d.lo1 = tri->min_bound[1];
+  d.hi0 = tri->max_bound[0];
+  d.hi1 = tri->max_bound[1];
+  const int64_t npx = (int64_t)W * H;
+  ST_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned) * npx, s));
+  ST_CUDA_CHECK(cudaMemsetAsync(w.tmin, 0xff, sizeof(unsigned) * npx, s));
+  ST_CUDA_CHECK(cudaMemsetAsync(w.tmax, 0, sizeof(unsigned) * npx, s));
+  if (d.n_tri > 0) {
+    st::k_claim<<<(d.n_tri + 127) / 128, 128, 0, s>>>(d, W, H, w);
+    ST_LAUNCH_CHECK("k_claim");
+  }
+  const unsigned blocks = (unsigned)((npx + 255) / 256);
+  st::k_walk_chunks<<<blocks, 256, 0, s>>>(d, W, npx, w);
+  ST_LAUNCH_CHECK("k_walk_chunks");
+  st::k_resolve_runs<<<blocks, 256, 0, s>>>(d, W, npx, w);
+  ST_LAUNCH_CHECK("k_resolve_runs");
+  st::k_mu_eval<<<blocks, 256, 0, s>>>(d, W, npx, w, clip_dmax, mu_out);
+  ST_LAUNCH_CHECK("k_mu_eval");
+  return ST_OK;
+}

@@ -1,0 +1,223 @@
+// See-through composition (refocus.py:24-148) on the device.
+//
+// k_refocus: per reference pixel, the Eq. 2 fp64 average of the static,
+// in-bounds rays' bilinear colours (view order), provenance and n_rays.
+// k_median: per-channel median over the clipped (2r+1)^2 window, applied to
+// every non-COPIED pixel.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "st_common.cuh"
+
+namespace st {
+
+struct RefocusOut {
+  double tot[3];
+  int count;
+};
+
+// gather_static_colors for one pixel (refocus.py:24-49).
+__device__ __forceinline__ RefocusOut gather_colors(const uint8_t* __restrict__ images,
+                                                    const st_rig& rig, int W, int H, double u,
+                                                    double v, double d, uint32_t bits) {
+  RefocusOut r;
+  r.tot[0] = r.tot[1] = r.tot[2] = 0.0;
+  r.count = 0;
+  const size_t plane = (size_t)W * H * 3;
+  for (int k = 0; k < rig.num_views; ++k) {
+    if (!((bits >> k) & 1u)) continue;
+    const WarpOut w = warp_to(rig, k, u, v, d);
+    // refocus.py:42: margin 0 against the frame size
+    if (!(w.front && w.pu >= 0.0 && w.pu <= (double)W - 1.0 && w.pv >= 0.0 &&
+          w.pv <= (double)H - 1.0))
+      continue;
+    const Taps t = taps_of(w.pu, w.pv, W, H);
+    const uint8_t* img = images + k * plane;
+    const size_t b = ((size_t)t.iv * W + t.iu) * 3;
+    const size_t bu = b + (size_t)t.su * 3;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      double f = lerp_u8(img[b + ch], img[bu + ch], t.fu);
+      if (t.fv != 0.0) {
+        const size_t bv = b + (size_t)t.sv * 3, bvu = bu + (size_t)t.sv * 3;
+        const double bot = lerp_u8(img[bv + ch], img[bvu + ch], t.fu);
+        f = dadd(f, dmul(t.fv, dsub(bot, f)));
+      }
+      r.tot[ch] = dadd(r.tot[ch], f);
+    }
+    ++r.count;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint8_t round_u8(double x) {
+  // np.clip(np.rint(x), 0, 255).astype(uint8)
+  return (uint8_t)fmin(fmax(rint(x), 0.0), 255.0);
+}
+
+__global__ void k_refocus(const uint8_t* __restrict__ images, st_rig rig, int W, int H,
+                          const float* __restrict__ values, const uint8_t* __restrict__ status,
+                          const uint32_t* __restrict__ static_bits, int min_static_rays,
+                          const uint8_t* __restrict__ copy_mask, uint8_t* __restrict__ out,
+                          uint8_t* __restrict__ prov, uint8_t* __restrict__ n_rays) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (int64_t)W * H) return;
+  const uint8_t* ref = images + (size_t)rig.ref_index * W * H * 3 + (size_t)p * 3;
+  uint8_t c0 = ref[0], c1 = ref[1], c2 = ref[2];
+  const bool copied = copy_mask && copy_mask[p];
+  uint8_t pv = copied ? ST_PROV_COPIED : ST_PROV_FALLBACK;
+  uint8_t nr = 0;
+  if (!copied && status[p] == ST_STATUS_VALID) {
+    const double d = (double)values[p];  // refocus.py:133
+    const RefocusOut r = gather_colors(images, rig, W, H, (double)(p % W), (double)(p / W), d,
+                                       static_bits[p]);
+    nr = (uint8_t)min(r.count, 255);
+    if (r.count >= min_static_rays) {
+      const double n = (double)r.count;
+      c0 = round_u8(ddiv(r.tot[0], n));
+      c1 = round_u8(ddiv(r.tot[1], n));
+      c2 = round_u8(ddiv(r.tot[2], n));
+      pv = ST_PROV_REFOCUSED;
+    }
+  }
+  out[(size_t)p * 3] = c0;
+  out[(size_t)p * 3 + 1] = c1;
+  out[(size_t)p * 3 + 2] = c2;
+  prov[p] = pv;
+  n_rays[p] = nr;
+}
+
+// refocus_pixel, batched (refocus.py:52-65).
+__global__ void k_refocus_pixels(const uint8_t* __restrict__ images, st_rig rig, int W, int H,
+                                 const int64_t* __restrict__ pix, const double* __restrict__ d,
+                                 const uint32_t* __restrict__ bits, int64_t n,
+                                 int min_static_rays, uint8_t* __restrict__ rgb,
+                                 int32_t* __restrict__ count, uint8_t* __restrict__ prov,
+                                 double* __restrict__ totals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t p = pix[i];
+  const RefocusOut r = gather_colors(images, rig, W, H, (double)(p % W), (double)(p / W), d[i],
+                                     bits[i]);
+  count[i] = r.count;
+  if (totals)
+    for (int ch = 0; ch < 3; ++ch) totals[3 * i + ch] = r.tot[ch];
+  if (r.count >= min_static_rays) {
+    const double c = (double)r.count;
+    for (int ch = 0; ch < 3; ++ch) rgb[3 * i + ch] = round_u8(ddiv(r.tot[ch], c));
+    prov[i] = ST_PROV_REFOCUSED;
+  } else {
+    const uint8_t* ref = images + (size_t)rig.ref_index * W * H * 3 + (size_t)p * 3;
+    for (int ch = 0; ch < 3; ++ch) rgb[3 * i + ch] = ref[ch];
+    prov[i] = ST_PROV_FALLBACK;
+  }
+}
+
+// Median of the clipped window: the values are uint8, so the i-th smallest
+// is found by counting (no sort), then 0.5 * (v[i0] + v[i1]) in fp32 and
+// rint half-even -- refocus.py:98-105.
+__device__ __forceinline__ int kth_smallest(const uint8_t* __restrict__ img, int W, int C, int ch,
+                                            int ylo, int yhi, int xlo, int xhi, int kth) {
+  // smallest value v with count(<= v) > kth
+  int lo = 0, hi = 255;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    int cnt = 0;
+    for (int y = ylo; y <= yhi; ++y)
+      for (int x = xlo; x <= xhi; ++x) cnt += img[((size_t)y * W + x) * C + ch] <= mid;
+    if (cnt > kth)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void k_median_small(const uint8_t* __restrict__ src, int H, int W, int C, int radius,
+                               const uint8_t* __restrict__ prov, uint8_t* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (int64_t)W * H) return;
+  const int x = (int)(p % W), y = (int)(p / W);
+  if (prov && prov[p] == ST_PROV_COPIED) {
+    for (int ch = 0; ch < C; ++ch) out[(size_t)p * C + ch] = src[(size_t)p * C + ch];
+    return;
+  }
+  const int ylo = max(y - radius, 0), yhi = min(y + radius, H - 1);
+  const int xlo = max(x - radius, 0), xhi = min(x + radius, W - 1);
+  const int cnt = (yhi - ylo + 1) * (xhi - xlo + 1);
+  for (int ch = 0; ch < C; ++ch) {
+    int v0, v1;
+    if (radius == 1) {
+      // <= 9 values: insertion sort in registers
+      int a[9];
+      int n = 0;
+      for (int yy = ylo; yy <= yhi; ++yy)
+        for (int xx = xlo; xx <= xhi; ++xx) {
+          int val = src[((size_t)yy * W + xx) * C + ch];
+          int j = n++;
+          while (j > 0 && a[j - 1] > val) {
+            a[j] = a[j - 1];
+            --j;
+          }
+          a[j] = val;
+        }
+      v0 = a[(cnt - 1) / 2];
+      v1 = a[cnt / 2];
+    } else {
+      v0 = kth_smallest(src, W, C, ch, ylo, yhi, xlo, xhi, (cnt - 1) / 2);
+      v1 = kth_smallest(src, W, C, ch, ylo, yhi, xlo, xhi, cnt / 2);
+    }
+    const float m = __fmul_rn(0.5f, __fadd_rn((float)v0, (float)v1));
+    out[(size_t)p * C + ch] = (uint8_t)fminf(fmaxf(rintf(m), 0.0f), 255.0f);
+  }
+}
+
+}  // namespace st
+
+extern "C" int st_median(const uint8_t* image, int32_t H, int32_t W, int32_t C, int32_t radius,
+                         uint8_t* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t npx = (int64_t)W * H;
+  if (radius <= 0) {
+    ST_CUDA_CHECK(cudaMemcpyAsync(out, image, (size_t)npx * C, cudaMemcpyDeviceToDevice, s));
+    return ST_OK;
+  }
+  st::k_median_small<<<(unsigned)((npx + 255) / 256), 256, 0, s>>>(image, H, W, C, radius,
+                                                                   nullptr, out);
+  ST_LAUNCH_CHECK("k_median_small");
+  return ST_OK;
+}
+
+extern "C" int st_synthesize(const uint8_t* images, const st_rig* rig, const float* values,
+                             const uint8_t* status, const uint32_t* static_bits,
+                             int32_t min_static_rays, int32_t median_radius,
+                             const uint8_t* copy_mask, uint8_t* image_out, uint8_t* prov_out,
+                             uint8_t* n_rays_out, uint8_t* scratch, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int W = rig->width, H = rig->height;
+  const int64_t npx = (int64_t)W * H;
+  const unsigned blocks = (unsigned)((npx + 127) / 128);
+  uint8_t* stage = median_radius > 0 ? scratch : image_out;
+  st::k_refocus<<<blocks, 128, 0, s>>>(images, *rig, W, H, values, status, static_bits,
+                                       min_static_rays, copy_mask, stage, prov_out, n_rays_out);
+  ST_LAUNCH_CHECK("k_refocus");
+  if (median_radius > 0) {
+    st::k_median_small<<<(unsigned)((npx + 255) / 256), 256, 0, s>>>(
+        scratch, H, W, 3, median_radius, prov_out, image_out);
+    ST_LAUNCH_CHECK("k_median_small");
+  }
+  return ST_OK;
+}
+
+extern "C" int st_refocus_pixels(const uint8_t* images, const st_rig* rig, const int64_t* pix,
+                                 const double* d, const uint32_t* bits, int64_t n,
+                                 int32_t min_static_rays, uint8_t* rgb, int32_t* count,
+                                 uint8_t* prov, double* totals, void* stream) {
+  if (n <= 0) return ST_OK;
+  st::k_refocus_pixels<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      images, *rig, rig->width, rig->height, pix, d, bits, n, min_static_rays, rgb, count, prov,
+      totals);
+  ST_LAUNCH_CHECK("k_refocus_pixels");
+  return ST_OK;
+}

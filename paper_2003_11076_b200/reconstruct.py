@@ -1,0 +1,173 @@
+"""Frame reconstruction: solve + see-through refocus, device-resident.
+
+`FramePipeline` is the fused form of the reference pipeline's two hot stages
+(pipeline.py:247-261: `DisparitySolver(...).solve()` then `synthesize(...)`)
+for a stream of frames of one shape: every device buffer (descriptors, mu,
+support lists, EM state, outputs, workspaces) is allocated once and reused,
+so a frame costs its H2D copy, the kernels and the D2H of the artefacts.
+`reconstruct` is the one-call host API on top of it.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .device import download, empty, require_cuda, upload
+from .prior import PriorParams, TriDevice
+from .solver import (DisparityMap, EMStats, SegmentationState, SolverParams, _check_views,
+                     _stats_of)
+
+
+@dataclass
+class Reconstruction:
+    disparity: DisparityMap
+    segmentation: SegmentationState
+    stats: EMStats
+    image: np.ndarray
+    provenance: np.ndarray
+    n_rays: np.ndarray
+
+
+class FramePipeline:
+    """Persistent device buffers for frames of shape (K, H, W)."""
+
+    def __init__(self, rig, width, height, params=None, prior_params=None):
+        t = require_cuda()
+        self.t = t
+        self.K = len(rig)
+        _check_views(self.K)
+        self.W, self.H = int(width), int(height)
+        self.params = params or SolverParams()
+        self.prior_params = prior_params or PriorParams()
+        self.rig_obj = rig
+        self.rig = N.make_rig(rig, self.W, self.H)
+        K, H, W = self.K, self.H, self.W
+        self.images = empty((K, H, W, 3), t.uint8)
+        self.priors = empty((K, H, W), t.float32)
+        self.desc = empty((K, H, W, 16), t.uint8)
+        self.mu = empty((H * W,), t.float64)
+        self.mu_ws = empty((int(N.lib().st_mu_raster_workspace(W, H)),), t.uint8)
+        self.sup_ws = empty((1,), t.uint8)
+        self.solve_ws = empty((int(N.lib().st_solve_workspace(W, H, K)),), t.uint8)
+        self.values = empty((H, W), t.float32)
+        self.status = empty((H, W), t.uint8)
+        self.sbits = empty((H, W), t.int32)
+        self.vbits = empty((H, W), t.int32)
+        self.image = empty((H, W, 3), t.uint8)
+        self.prov = empty((H, W), t.uint8)
+        self.n_rays = empty((H, W), t.uint8)
+        self.scratch = empty((H, W, 3), t.uint8)
+        self.copy = empty((H, W), t.uint8)
+        self.frame = N.StFrame()
+        self.frame.images = self.images.data_ptr()
+        self.frame.priors = self.priors.data_ptr()
+        self.frame.desc = self.desc.data_ptr()
+        self.frame.mu = self.mu.data_ptr()
+
+    # -- inputs ---------------------------------------------------------------------
+
+    def load(self, images, priors):
+        """Copy a frame into the input buffers (async DMA when the host side is pinned)."""
+        t = self.t
+        for dst, src, dt in ((self.images, images, np.uint8), (self.priors, priors, np.float32)):
+            if isinstance(src, t.Tensor):
+                dst.copy_(src, non_blocking=True)
+            elif isinstance(src, np.ndarray):
+                dst.copy_(t.from_numpy(np.ascontiguousarray(src, dtype=dt)), non_blocking=True)
+            else:
+                for k, a in enumerate(src):
+                    dst[k].copy_(t.from_numpy(np.ascontiguousarray(a, dtype=dt)),
+                                 non_blocking=True)
+
+    # -- the frame --------------------------------------------------------------------
+
+    def run(self, tri_dev, dynamic_only=False, forced_iters=0, median_radius=1, timing=False,
+            reduce=None):
+        """Descriptors, mu, support lists, EM, refocus + median for the loaded frame."""
+        p = N.make_params(self.params, self.prior_params, forced_iters, timing)
+        K, H, W = self.K, self.H, self.W
+        N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
+        N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max), self.mu,
+                 self.mu_ws, self.mu_ws.numel())
+        need = int(N.lib().st_support_workspace(tri_dev.n_sup, W, H,
+                                                float(self.prior_params.neighborhood_radius)))
+        if self.sup_ws.numel() < need:
+            self.sup_ws = empty((need,), self.t.uint8)
+        rec = N.C.c_int64(0)
+        N.invoke("st_support_build", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W, H, p,
+                 self.frame, self.sup_ws, self.sup_ws.numel(), rec)
+        stats = N.StStats()
+        cb = N.REDUCE_FN(reduce) if reduce is not None else N.REDUCE_FN()
+        N.invoke("st_solve", self.frame, self.rig, p, int(bool(dynamic_only)), None,
+                 self.values, self.status, self.sbits, self.vbits, stats, self.solve_ws,
+                 self.solve_ws.numel(), cb, None)
+        stats.support_records = rec.value
+        copy = None
+        if dynamic_only:
+            # pipeline.py:254-255: copy_mask = ref prior >= threshold (float32 compare)
+            thr = self.t.tensor(np.float32(self.params.threshold), device=self.priors.device)
+            self.copy.copy_(self.priors[self.rig_obj.ref_index] >= thr)
+            copy = self.copy
+        N.invoke("st_synthesize", self.images, self.rig, self.values, self.status, self.sbits,
+                 int(self.params.min_static_rays), int(median_radius), copy, self.image,
+                 self.prov, self.n_rays, self.scratch)
+        return _stats_of(stats)
+
+    # -- outputs ------------------------------------------------------------------------
+
+    def output_bytes(self):
+        return self.H * self.W * (4 + 1 + 4 + 4 + 3 + 1 + 1)
+
+    def fetch(self):
+        """D2H of every artefact into fresh pinned host buffers (torch's caching
+        host allocator recycles them once the caller drops the arrays)."""
+        t = self.t
+        outs = []
+        for d in (self.values, self.status, self.sbits, self.vbits, self.image, self.prov,
+                  self.n_rays):
+            h = t.empty(d.shape, dtype=d.dtype, pin_memory=True)
+            h.copy_(d, non_blocking=True)
+            outs.append(h)
+        t.cuda.current_stream().synchronize()
+        return [h.numpy() for h in outs]
+
+
+_PIPES = {}
+
+
+def _pipeline_for(rig, w, h, params, prior_params):
+    key = (id(rig), w, h, repr(params), repr(prior_params))
+    p = _PIPES.get(key)
+    if p is None:
+        if len(_PIPES) > 8:
+            _PIPES.clear()
+        p = _PIPES[key] = FramePipeline(rig, w, h, params, prior_params)
+    return p
+
+
+def reconstruct(frame, rig, tri, params=None, prior_params=None, dynamic_only=False,
+                median_radius=1, forced_iters=0):
+    """em_solve + synthesize in one device pass: host frame in, host artefacts out.
+
+    dynamic_only follows pipeline.py:252-258 (only pixels whose reference
+    prior is below the threshold are solved; the rest are copied through).
+    forced_iters > 0 runs exactly that many EM iterations (non-reference
+    bench mode).  Returned arrays are fresh copies (the reference's "new
+    arrays out" contract).
+    """
+    params = params or SolverParams()
+    prior_params = prior_params or PriorParams()
+    if frame.num_views != len(rig):
+        raise ValueError("frame view count does not match the rig")
+    h, w = frame.shape
+    pipe = _pipeline_for(rig, w, h, params, prior_params)
+    pipe.load(frame.images, frame.priors)
+    stats = pipe.run(TriDevice(tri), dynamic_only=dynamic_only, forced_iters=forced_iters,
+                     median_radius=median_radius)
+    values, status, sbits, vbits, img, prov, nr = pipe.fetch()
+    return Reconstruction(
+        disparity=DisparityMap(values=values, status=status),
+        segmentation=SegmentationState(static_bits=sbits.view(np.uint32),
+                                       valid_bits=vbits.view(np.uint32)),
+        stats=stats, image=img, provenance=prov, n_rays=nr)

@@ -1,0 +1,310 @@
+"""GPU parity: the CUDA path against the reference-generated golden fixtures.
+
+Every call goes through the C ABI (via the package's ctypes binding).  Bars:
+bit-exact for integer / byte / index work and for the fp64 sampling recipe;
+for the EM decisions (argmin disparity, argmax masks) exact wherever the
+reference's decision margin exceeds 1e-5 and >= 99.9 % overall
+(BASELINE.json north_star).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_io import SCENES, cases, load, oracle_solver, support
+
+pytestmark = pytest.mark.gpu
+
+MARGIN = 1e-5        # north_star: exact wherever the cost margin exceeds 1e-5
+AGREE = 0.999        # north_star: >= 99.9 % agreement overall
+
+
+@pytest.fixture(scope="module")
+def st():
+    import paper_2003_11076_b200 as pkg
+    from paper_2003_11076_b200.device import require_cuda
+    require_cuda()
+    return pkg
+
+
+class _Tri:
+    """Duck-typed TriangulationPrior built from a golden fixture."""
+
+    def __init__(self, g):
+        self.points = g["tri_points"]
+        self.disparities = g["tri_disp"]
+        self.triangles = g["tri_triangles"]
+        self.planes = g["tri_planes"]
+        self.num_anchors = int(g["tri_num_anchors"])
+
+    def support_points(self):
+        n = self.points.shape[0] - self.num_anchors
+        return self.points[:n], self.disparities[:n]
+
+
+class _Intr:
+    def __init__(self, h, w):
+        self.height, self.width = int(h), int(w)
+
+
+class _Rig:
+    """Duck-typed CameraRig exposing the golden warp tables."""
+
+    def __init__(self, g):
+        self.a, self.b, self.dims = g["warp_a"], g["warp_b"], g["dims"]
+        self.ref_index = int(g["ref_index"])
+
+    def __len__(self):
+        return self.a.shape[0]
+
+    def warp_coefficients(self, k):
+        return self.a[k], self.b[k]
+
+    def intrinsics(self, k):
+        return _Intr(*self.dims[k])
+
+
+def _frame(st, g):
+    return st.LightFieldFrame(images=list(g["images"]), priors=list(g["priors"]))
+
+
+def _params(st, g):
+    p = g["params"]
+    sp = st.SolverParams(beta=p["beta"], threshold=p["threshold"], max_iters=p["max_iters"],
+                         min_static_rays=p["min_static_rays"], epsilon_prior=p["epsilon_prior"])
+    pp = st.PriorParams(sigma=p["sigma"], gamma=p["gamma"], d_max=p["d_max"],
+                        neighborhood_radius=p["neighborhood_radius"])
+    return sp, pp
+
+
+def _solver(st, g):
+    sp, pp = _params(st, g)
+    return st.DisparitySolver(_frame(st, g), _Rig(g), _Tri(g), params=sp, prior_params=pp)
+
+
+# -- L1 primitives -------------------------------------------------------------------
+
+def test_descriptors_gray_sobel_exact(st):
+    z = cases("sampling_cases")
+    for im, g, d in zip(z["desc_images"], z["desc_gray"], z["desc_out"]):
+        assert np.array_equal(st.rgb_to_gray(im), g)
+        assert np.array_equal(st.compute_descriptors(im).data, d)
+        assert np.array_equal(st.compute_descriptors(g).data, d)
+        gx, gy = st.sobel_responses(g)
+        ox, oy = oracle.sobel_of(g)
+        assert np.array_equal(gx, ox) and np.array_equal(gy, oy)
+
+
+def test_bilinear_bit_exact(st):
+    z = cases("sampling_cases")
+    for i in range(5):
+        img = z[f"b{i}_img"]
+        flat, h, w = st.flatten_channels(img)
+        got = st.bilinear(flat, h, w, z[f"b{i}_u"], z[f"b{i}_v"])
+        assert np.array_equal(got.view(np.uint64), z[f"b{i}_out"].view(np.uint64)), i
+
+
+def test_median_exact(st):
+    z = cases("sampling_cases")
+    assert np.array_equal(st.median_filter(z["median_in"], 1), z["median_r1"])
+    assert np.array_equal(st.median_filter(z["median_in"], 2), z["median_r2"])
+    g = z["median_in"][..., 0].copy()
+    assert np.array_equal(st.median_filter(g, 1), oracle.median_filter(g, 1))
+    assert np.array_equal(st.median_filter(g, 3), oracle.median_filter(g, 3))
+
+
+def test_e_step_golden_exact(st):
+    z = cases("estep_cases")
+    p = st.SolverParams()
+    for k in (5, 3, 4, 9):
+        got = st.e_step(z[f"k{k}_desc"].astype(np.float64), z[f"k{k}_valid"], z[f"k{k}_q"], p)
+        assert got.dtype == np.uint32
+        assert np.array_equal(got, z[f"k{k}_out"]), k
+
+
+def test_e_step_errors_and_edge_cases(st):
+    p = st.SolverParams()
+    with pytest.raises(ValueError, match="exponential"):
+        st.e_step(np.zeros((1, 13, 16)), np.ones((1, 13), bool), np.full((1, 13), 0.5), p)
+    assert st.e_step(np.zeros((0, 5, 16)), np.zeros((0, 5), bool), np.zeros((0, 5)), p).shape == (0,)
+    # all identical rays, neutral priors -> full mask; two pairs -> smaller encoding
+    desc = np.full((1, 4, 16), 100.0)
+    valid = np.ones((1, 4), bool)
+    q = np.full((1, 4), 0.5)
+    assert st.e_step(desc, valid, q, p)[0] == 0b1111
+    a, b = np.full(16, 50.0), np.full(16, 200.0)
+    assert st.e_step(np.stack([a, a, b, b])[None], valid, q, p)[0] == 0b0011
+    # K = 12, random, against the oracle
+    rng = np.random.default_rng(12)
+    d = rng.integers(0, 256, size=(40, 12, 16)).astype(np.float64)
+    v = rng.random((40, 12)) < 0.8
+    qq = rng.random((40, 12))
+    assert np.array_equal(st.e_step(d, v, qq, p), oracle.e_step(d, v, qq, oracle.OracleParams()))
+
+
+def test_masked_variance(st):
+    rng = np.random.default_rng(60)
+    for _ in range(20):
+        k = int(rng.integers(1, 8))
+        desc = rng.integers(0, 256, size=(k, 16)).astype(np.float64)
+        mask = rng.random(k) < 0.6
+        mask[0] = True
+        sel = desc[mask]
+        want = float(((sel - sel.sum(axis=0) / len(sel)) ** 2).sum() / len(sel))
+        assert st.masked_variance(desc, mask) == want
+    with pytest.raises(ValueError, match="at least one"):
+        st.masked_variance(np.zeros((3, 16)), np.zeros(3, bool))
+
+
+def test_warp_matches_oracle(st):
+    g = load("occ160_tilt")
+    rig = st.CameraRig.__new__(st.CameraRig)
+    rng = np.random.default_rng(3)
+    u = rng.uniform(0, 159, 500)
+    v = rng.uniform(0, 119, 500)
+    d = rng.uniform(0.5, 60, 500)
+    from paper_2003_11076_b200.geometry import _apply_warp
+    for k in range(5):
+        pu, pv, ok = _apply_warp(g["warp_a"][k], g["warp_b"][k], u, v, d)
+        ou, ov, ook = oracle.warp(g["warp_a"][k], g["warp_b"][k], u, v, d)
+        assert np.array_equal(pu, ou) and np.array_equal(pv, ov) and np.array_equal(ok, ook)
+    del rig
+
+
+# -- solver pieces -----------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", SCENES)
+def test_mu_raster(st, name):
+    g = load(name)
+    h, w = g["images"].shape[1:3]
+    mu = _Tri(g)
+    got = st.TriangulationPrior(mu.points, mu.disparities, mu.triangles, mu.planes,
+                                mu.num_anchors).disparity_map(w, h)
+    # bit-exact: the kernel replays Qhull's find_simplex walk for edge pixels
+    assert np.array_equal(got.view(np.uint64), g["mu_raw"].view(np.uint64)), \
+        int((got != g["mu_raw"]).sum())
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_initial_masks_and_first_iteration(st, name):
+    g = load(name)
+    s = _solver(st, g)
+    h, w = g["images"].shape[1:3]
+    allp = np.arange(h * w, dtype=np.int64)
+    s0, v0 = s.initial_masks(allp)
+    assert np.array_equal(v0, g["init_valid"])
+    assert np.array_equal(s0, g["init_static"])
+    d1, e1, st1 = s.m_step(allp, g["init_static"])
+    o = oracle_solver(g)
+    _, _, margin = o.m_margins(allp, g["init_static"])
+    clear = margin > MARGIN
+    same = d1.astype(np.float32) == g["m1_d"].astype(np.float32)
+    assert same[clear].all(), np.flatnonzero(~same & clear)[:10]
+    assert same.mean() >= AGREE
+    assert (st1 == g["m1_status"]).mean() >= AGREE
+    assert np.allclose(e1, g["m1_e"], rtol=1e-12, atol=1e-12)
+    pix = g["e1_pix"]
+    s1, v1 = s.e_step_at(pix, g["m1_d"][pix])
+    em = o.e_margins(pix, g["m1_d"][pix])
+    ok = s1 == g["e1_static"]
+    assert ok[em > MARGIN].all()
+    assert ok.mean() >= AGREE
+    assert np.array_equal(v1, g["e1_valid"])
+
+
+def test_gather_rays_and_energy(st):
+    g = load("occ160_tilt")
+    s = _solver(st, g)
+    o = oracle_solver(g)
+    rng = np.random.default_rng(5)
+    pix = rng.integers(0, 160 * 120, 400).astype(np.int64)
+    d = rng.uniform(0.5, 60, 400)
+    desc, valid, q = s.gather_rays(pix, d)
+    od, ov, oq = o.gather_rays(pix, d)
+    assert np.array_equal(valid, ov)
+    assert np.array_equal(desc.view(np.uint64), od.view(np.uint64))
+    assert np.array_equal(q.view(np.uint64), oq.view(np.uint64))
+    bits = rng.integers(0, 32, 400).astype(np.uint32)
+    e, real = s._energy(pix, d, bits)
+    oe, oreal = o.energy(pix, d, bits)
+    assert np.array_equal(real, oreal)
+    assert np.allclose(e, oe, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_full_solve_matches_reference(st, name):
+    g = load(name)
+    for tag, dyn in (("full", False), ("dyn", True)):
+        s = _solver(st, g)
+        dmap, seg, stats = s.solve(dynamic_only=dyn)
+        want_v = g[f"{tag}_values"]
+        assert dmap.values.dtype == np.float32 and seg.static_bits.dtype == np.uint32
+        assert (dmap.values == want_v).mean() >= AGREE
+        assert (dmap.status == g[f"{tag}_status"]).mean() >= AGREE
+        assert (seg.static_bits == g[f"{tag}_static"]).mean() >= AGREE
+        assert (seg.valid_bits == g[f"{tag}_valid"]).mean() >= AGREE
+        ref = g[f"{tag}_stats"]
+        assert stats.iterations_run == ref["iterations_run"]
+        assert stats.converged_after == ref["converged_after"]
+        assert np.allclose(stats.mean_energy, ref["mean_energy"], rtol=1e-9)
+        assert np.allclose(stats.prev_energy, ref["prev_energy"], rtol=1e-9)
+        assert np.allclose(stats.changed_fraction, ref["changed_fraction"], atol=2e-4)
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_synthesize_exact_on_reference_solution(st, name):
+    g = load(name)
+    frame = _frame(st, g)
+    rig = _Rig(g)
+    for tag in ("full", "dyn"):
+        dmap = st.DisparityMap(values=g[f"{tag}_values"], status=g[f"{tag}_status"])
+        seg = st.SegmentationState(static_bits=g[f"{tag}_static"], valid_bits=g[f"{tag}_valid"])
+        copy = (g["priors"][int(g["ref_index"])] >= g["params"]["threshold"]) if tag == "dyn" else None
+        for r in (0, 1):
+            img, prov, nr = st.synthesize(frame, rig, dmap, seg, median_radius=r, copy_mask=copy)
+            assert np.array_equal(img, g[f"{tag}_synth{r}_img"])
+            assert np.array_equal(prov, g[f"{tag}_synth{r}_prov"])
+            assert np.array_equal(nr, g[f"{tag}_synth{r}_nrays"])
+
+
+@pytest.mark.parametrize("name", ["occ160_noisy", "occ320_noisy", "occ128_k9"])
+def test_reconstruct_end_to_end(st, name):
+    g = load(name)
+    sp, pp = _params(st, g)
+    frame = _frame(st, g)
+    for tag, dyn in (("full", False), ("dyn", True)):
+        r = st.reconstruct(frame, _Rig(g), _Tri(g), params=sp, prior_params=pp,
+                           dynamic_only=dyn)
+        assert (r.disparity.values == g[f"{tag}_values"]).mean() >= AGREE
+        assert (r.image == g[f"{tag}_synth1_img"]).all(axis=2).mean() >= AGREE
+        assert (r.provenance == g[f"{tag}_synth1_prov"]).mean() >= AGREE
+
+
+def test_solver_errors(st):
+    g = load("occ160")
+    sp, pp = _params(st, g)
+    frame = _frame(st, g)
+    rig = _Rig(g)
+    rig.a = rig.a[:4]
+    with pytest.raises(ValueError, match="view count"):
+        st.DisparitySolver(frame, rig, _Tri(g))
+    with pytest.raises(ValueError, match="subset"):
+        st.SegmentationState(static_bits=np.array([[4]], np.uint32),
+                             valid_bits=np.array([[3]], np.uint32))
+
+
+def test_refocus_pixel_matches_dense(st):
+    g = load("occ160")
+    frame = _frame(st, g)
+    rig = _Rig(g)
+    dmap = st.DisparityMap(values=g["full_values"], status=g["full_status"])
+    seg = st.SegmentationState(static_bits=g["full_static"], valid_bits=g["full_valid"])
+    img, prov, nr = st.synthesize(frame, rig, dmap, seg, median_radius=0)
+    rng = np.random.default_rng(72)
+    for _ in range(60):
+        u, v = int(rng.integers(0, 160)), int(rng.integers(0, 120))
+        if dmap.status[v, u] != 0:
+            continue
+        rgb, n, p = st.refocus_pixel(frame, rig, u, v, float(dmap.values[v, u]),
+                                     int(seg.static_bits[v, u]))
+        assert n == nr[v, u] and p == prov[v, u] and np.array_equal(rgb, img[v, u])
