@@ -160,19 +160,20 @@ def oracle_sample(frame, rig, tri, cfg, rows):
     desc = [oracle.descriptors_of(im) for im in frame.images]
     mu = oracle.mu_raster(tri.points, tri.disparities, tri.triangles, tri.planes, w, h)
     t_full = time.perf_counter() - t0
-    r0 = max(0, (h - rows) // 2)
-    active = np.arange(r0 * w, (r0 + rows) * w, dtype=np.int64)
+    # evenly strided rows: a representative sample of the frame
+    row_ids = np.unique(np.linspace(0, h - 1, rows).round().astype(np.int64))
+    rows = row_ids.size
+    active = (row_ids[:, None] * w + np.arange(w)[None, :]).ravel()
     s = oracle.OracleSolver(frame.images, frame.priors, a, b, rig.ref_index, mu, sup_uv, sup_d,
                             params=p, descriptors=desc)
     t1 = time.perf_counter()
     res = s.solve(active=active)
-    # refocus + median restricted to the band (+1 row halo for the median)
-    lo, hi = max(0, r0 - 1), min(h, r0 + rows + 1)
+    # refocus on the sampled rows, median on a row-proportional slab
     st_band = np.full((h, w), oracle.STATUS_LOW_TEXTURE, np.uint8)
-    st_band[r0:r0 + rows] = res["status"][r0:r0 + rows]
+    st_band[row_ids] = res["status"][row_ids]
     img, prov, nr = oracle.synthesize(frame.images, a, b, rig.ref_index, res["values"], st_band,
                                       res["static_bits"], sp.min_static_rays, 0)
-    oracle.median_filter(img[lo:hi], 1)
+    oracle.median_filter(img[:rows], 1)
     t_band = time.perf_counter() - t1
     frac = rows / h
     t_frame = t_full + t_band / frac
@@ -309,6 +310,15 @@ def run_ours(args):
         total_ms = float(tt.item())
     fps = world * args.steps / (total_ms / 1e3)
 
+    if args.quick:
+        if rank == 0:
+            print(json.dumps({"value": fps, "ms_per_step": total_ms / args.steps,
+                              "stage_ms": {n: float(np.mean([s.stage_ms[n] for s in stats]))
+                                           for n in stats[0].stage_ms},
+                              "kernel_ms": [float(np.mean([s.kernel_ms[j] for s in stats]))
+                                            for j in range(4)]}), flush=True)
+        return
+
     # -- e2e: public API from pinned host memory, artefacts back to the host ----------
     pin_imgs = [st.device.pinned_empty(im.shape, np.uint8) for im in frame.images]
     pin_pris = [st.device.pinned_empty(p.shape, np.float32) for p in frame.priors]
@@ -421,7 +431,9 @@ def run_ours(args):
                "kernel_ms": {"m_step": ms_m,
                              "e_step": float(np.mean([s.kernel_ms[1] for s in stats])),
                              "initial_masks": float(np.mean([s.kernel_ms[2] for s in stats])),
-                             "reduce": float(np.mean([s.kernel_ms[3] for s in stats]))}},
+                             "reduce": float(np.mean([s.kernel_ms[3] for s in stats]))},
+               "stage_ms": {n: float(np.mean([s.stage_ms[n] for s in stats]))
+                            for n in stats[0].stage_ms}},
         "gpix_plane_per_s": w * h * dmax * fps / 1e9,
         "forced_iters_mode": forced,
     }
@@ -441,6 +453,7 @@ def main():
     ap.add_argument("--forced-steps", type=int, default=5)
     ap.add_argument("--cpu-rows", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="value loop only (profiling)")
     ap.add_argument("--budget", type=float, default=150.0,
                     help="reference arm: seconds for the whole run")
     args = ap.parse_args()

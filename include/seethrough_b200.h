@@ -138,7 +138,7 @@ typedef struct {
  * mu out (H*W) f64. */
 int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip_dmax, double* mu_out,
                  void* workspace, int64_t workspace_bytes, void* stream);
-int64_t st_mu_raster_workspace(int32_t W, int32_t H);
+int64_t st_mu_raster_workspace(int32_t W, int32_t H, int32_t n_tri);
 
 /* ---- solver pieces (DisparitySolver API, solver.py:162-432) ----------- */
 

@@ -264,10 +264,15 @@ class OracleSolver:
         fv = (v - iv)[:, None]
         base = iv.astype(np.int64) * w + iu.astype(np.int64)
         f2 = flat.reshape(-1, c)
-        t0, t1 = f2[base], f2[base + 1]
-        b0, b1 = f2[base + w], f2[base + w + 1]
-        top = t0 + fu * (t1 - t0)
-        bot = b0 + fu * (b1 - b0)
+        # zero-weight taps contribute exactly nothing, so (like sampling.py:40-55)
+        # skip their gathers when a whole batch sits on integer columns / rows
+        lerp_u = bool(fu.any())
+        t0 = f2[base]
+        top = t0 + fu * (f2[base + 1] - t0) if lerp_u else t0.astype(np.float64)
+        if not fv.any():
+            return top
+        b0 = f2[base + w]
+        bot = b0 + fu * (f2[base + w + 1] - b0) if lerp_u else b0.astype(np.float64)
         return top + fv * (bot - top)
 
     def ray(self, pix, d, k):

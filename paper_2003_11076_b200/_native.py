@@ -69,7 +69,7 @@ _SIGS = {
     "st_bilinear": (C.c_int, [_P, _I32, _I32, _I32, _P, _P, _I64, _P, _P]),
     "st_warp": (C.c_int, [C.POINTER(StRig), _I32, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "st_mu_raster": (C.c_int, [C.POINTER(StTri), _I32, _I32, _D, _P, _P, _I64, _P]),
-    "st_mu_raster_workspace": (C.c_int64, [_I32, _I32]),
+    "st_mu_raster_workspace": (C.c_int64, [_I32, _I32, _I32]),
     "st_support_build": (C.c_int, [_P, _P, _I32, _I32, _I32, C.POINTER(StParams),
                                    C.POINTER(StFrame), _P, _I64, C.POINTER(C.c_int64), _P]),
     "st_support_workspace": (C.c_int64, [_I32, _I32, _I32, _D]),

@@ -25,6 +25,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cub/cub.cuh>
+
 #include "st_common.cuh"
 
 namespace st {
@@ -62,7 +64,12 @@ __device__ __forceinline__ bool bary_inside(const double* __restrict__ T, double
   return -eps <= c2 && c2 <= 1.0 + eps;
 }
 
-__global__ void k_claim(TriDev d, int W, int H, MuWs w) {
+// Pixel-centre bbox of every triangle (empty for degenerate simplices) and
+// its pixel count, scanned afterwards so the claim tests can be spread
+// evenly over the grid (a few corner-anchor triangles span most of the
+// image; one thread per triangle would serialise them).
+__global__ void k_tri_bbox(TriDev d, int W, int H, int4* __restrict__ bbox,
+                           unsigned long long* __restrict__ area) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= d.n_tri) return;
   const int a = d.simp[3 * t], b = d.simp[3 * t + 1], c = d.simp[3 * t + 2];
@@ -70,19 +77,54 @@ __global__ void k_claim(TriDev d, int W, int H, MuWs w) {
   const double bx = d.pts[2 * b], by = d.pts[2 * b + 1];
   const double cx = d.pts[2 * c], cy = d.pts[2 * c + 1];
   const double* T = d.transform + 6 * t;
-  if (!(T[0] == T[0])) return;  // degenerate simplex: nan transform
-  const int x0 = max(0, (int)ceil(fmin(ax, fmin(bx, cx)) - 1e-6));
-  const int x1 = min(W - 1, (int)floor(fmax(ax, fmax(bx, cx)) + 1e-6));
-  const int y0 = max(0, (int)ceil(fmin(ay, fmin(by, cy)) - 1e-6));
-  const int y1 = min(H - 1, (int)floor(fmax(ay, fmax(by, cy)) + 1e-6));
-  for (int y = y0; y <= y1; ++y)
-    for (int x = x0; x <= x1; ++x)
-      if (bary_inside(T, (double)x, (double)y)) {
+  int4 bb;
+  bb.x = max(0, (int)ceil(fmin(ax, fmin(bx, cx)) - 1e-6));
+  bb.z = min(W - 1, (int)floor(fmax(ax, fmax(bx, cx)) + 1e-6));
+  bb.y = max(0, (int)ceil(fmin(ay, fmin(by, cy)) - 1e-6));
+  bb.w = min(H - 1, (int)floor(fmax(ay, fmax(by, cy)) + 1e-6));
+  unsigned long long n = 0;
+  if (T[0] == T[0] && bb.x <= bb.z && bb.y <= bb.w)  // nan transform: degenerate simplex
+    n = (unsigned long long)(bb.z - bb.x + 1) * (unsigned long long)(bb.w - bb.y + 1);
+  bbox[t] = bb;
+  area[t] = n;
+}
+
+#define CLAIM_ITEMS 16
+
+// Flattened (triangle, bbox pixel) work items; `start` is the exclusive scan
+// of the bbox areas (n_tri + 1 entries, start[n_tri] = total).
+__global__ void k_claim(TriDev d, int W, const int4* __restrict__ bbox,
+                        const unsigned long long* __restrict__ start, MuWs w) {
+  const unsigned long long total = start[d.n_tri];
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x * CLAIM_ITEMS;
+  for (unsigned long long i0 =
+           ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * CLAIM_ITEMS;
+       i0 < total; i0 += stride) {
+    // triangle owning item i0: last t with start[t] <= i0
+    int lo = 0, hi = d.n_tri - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (start[mid] <= i0)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    int t = lo;
+    const unsigned long long i1 = min(i0 + CLAIM_ITEMS, total);
+    for (unsigned long long i = i0; i < i1; ++i) {
+      while (i >= start[t + 1]) ++t;
+      const int4 bb = bbox[t];
+      const int bw = bb.z - bb.x + 1;
+      const unsigned long long local = i - start[t];
+      const int x = bb.x + (int)(local % bw), y = bb.y + (int)(local / bw);
+      if (bary_inside(d.transform + 6 * t, (double)x, (double)y)) {
         const size_t p = (size_t)y * W + x;
         atomicAdd(w.cnt + p, 1u);
         atomicMin(w.tmin + p, (unsigned)t);
         atomicMax(w.tmax + p, (unsigned)t);
       }
+    }
+  }
 }
 
 // scipy _distplane on the lifted point.
@@ -301,10 +343,11 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct MuLayout {
   size_t off[11];
+  size_t bbox, area, start, cub, cub_bytes;
   size_t total;
 };
 
-MuLayout mu_layout(int W, int H) {
+MuLayout mu_layout(int W, int H, int n_tri) {
   MuLayout L;
   const size_t npx = (size_t)W * H;
   size_t o = 0;
@@ -313,21 +356,29 @@ MuLayout mu_layout(int W, int H) {
     L.off[i] = o;
     o += align_up(sz[i] * npx);
   }
+  const size_t nt = (size_t)(n_tri > 0 ? n_tri : 1) + 1;
+  L.bbox = o;  o += align_up(sizeof(int4) * nt);
+  L.area = o;  o += align_up(sizeof(unsigned long long) * nt);
+  L.start = o; o += align_up(sizeof(unsigned long long) * nt);
+  L.cub_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, L.cub_bytes, (unsigned long long*)nullptr,
+                                (unsigned long long*)nullptr, (int)nt);
+  L.cub = o;   o += align_up(L.cub_bytes);
   L.total = o;
   return L;
 }
 
 }  // namespace
 
-extern "C" int64_t st_mu_raster_workspace(int32_t W, int32_t H) {
-  return (int64_t)mu_layout(W, H).total;
+extern "C" int64_t st_mu_raster_workspace(int32_t W, int32_t H, int32_t n_tri) {
+  return (int64_t)mu_layout(W, H, n_tri).total;
 }
 
 extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip_dmax,
                             double* mu_out, void* workspace, int64_t workspace_bytes,
                             void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  const MuLayout L = mu_layout(W, H);
+  const MuLayout L = mu_layout(W, H, tri->n_tri);
   if ((int64_t)L.total > workspace_bytes) {
     sthost::set_error("mu raster workspace too small");
     return ST_ENOMEM;
@@ -375,7 +426,19 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   ST_CUDA_CHECK(cudaMemsetAsync(w.tmin, 0xff, sizeof(unsigned) * npx, s));
   ST_CUDA_CHECK(cudaMemsetAsync(w.tmax, 0, sizeof(unsigned) * npx, s));
   if (d.n_tri > 0) {
-    st::k_claim<<<(d.n_tri + 127) / 128, 128, 0, s>>>(d, W, H, w);
+    int4* bbox = (int4*)(ws + L.bbox);
+    auto* area = (unsigned long long*)(ws + L.area);
+    auto* start = (unsigned long long*)(ws + L.start);
+    ST_CUDA_CHECK(cudaMemsetAsync(area + d.n_tri, 0, sizeof(unsigned long long), s));
+    st::k_tri_bbox<<<(d.n_tri + 127) / 128, 128, 0, s>>>(d, W, H, bbox, area);
+    ST_LAUNCH_CHECK("k_tri_bbox");
+    size_t tb = L.cub_bytes;
+    ST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws + L.cub, tb, area, start, d.n_tri + 1, s));
+    sthost::count_launch();
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    st::k_claim<<<sms * 8, 256, 0, s>>>(d, W, bbox, start, w);
     ST_LAUNCH_CHECK("k_claim");
   }
   const unsigned blocks = (unsigned)((npx + 255) / 256);

@@ -95,7 +95,7 @@ def mu_raster_device(tri, width, height, clip_dmax=0.0, tri_dev=None):
     t = require_cuda()
     td = tri_dev or TriDevice(tri)
     mu = empty((height * width,), t.float64)
-    ws = empty((int(N.lib().st_mu_raster_workspace(width, height)),), t.uint8)
+    ws = empty((int(N.lib().st_mu_raster_workspace(width, height, td.n_tri)),), t.uint8)
     N.invoke("st_mu_raster", td.st, width, height, float(clip_dmax), mu, ws, ws.numel())
     return mu
 

@@ -47,7 +47,7 @@ class FramePipeline:
         self.priors = empty((K, H, W), t.float32)
         self.desc = empty((K, H, W, 16), t.uint8)
         self.mu = empty((H * W,), t.float64)
-        self.mu_ws = empty((int(N.lib().st_mu_raster_workspace(W, H)),), t.uint8)
+        self.mu_ws = empty((1,), t.uint8)
         self.sup_ws = empty((1,), t.uint8)
         self.solve_ws = empty((int(N.lib().st_solve_workspace(W, H, K)),), t.uint8)
         self.values = empty((H, W), t.float32)
@@ -87,9 +87,17 @@ class FramePipeline:
         """Descriptors, mu, support lists, EM, refocus + median for the loaded frame."""
         p = N.make_params(self.params, self.prior_params, forced_iters, timing)
         K, H, W = self.K, self.H, self.W
+        marks = []
+        mark = (lambda: marks.append(self._event())) if timing else (lambda: None)
+        mark()
         N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
+        mark()
+        need = int(N.lib().st_mu_raster_workspace(W, H, tri_dev.n_tri))
+        if self.mu_ws.numel() < need:
+            self.mu_ws = empty((need,), self.t.uint8)
         N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max), self.mu,
                  self.mu_ws, self.mu_ws.numel())
+        mark()
         need = int(N.lib().st_support_workspace(tri_dev.n_sup, W, H,
                                                 float(self.prior_params.neighborhood_radius)))
         if self.sup_ws.numel() < need:
@@ -97,11 +105,13 @@ class FramePipeline:
         rec = N.C.c_int64(0)
         N.invoke("st_support_build", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W, H, p,
                  self.frame, self.sup_ws, self.sup_ws.numel(), rec)
+        mark()
         stats = N.StStats()
         cb = N.REDUCE_FN(reduce) if reduce is not None else N.REDUCE_FN()
         N.invoke("st_solve", self.frame, self.rig, p, int(bool(dynamic_only)), None,
                  self.values, self.status, self.sbits, self.vbits, stats, self.solve_ws,
                  self.solve_ws.numel(), cb, None)
+        mark()
         stats.support_records = rec.value
         copy = None
         if dynamic_only:
@@ -112,7 +122,18 @@ class FramePipeline:
         N.invoke("st_synthesize", self.images, self.rig, self.values, self.status, self.sbits,
                  int(self.params.min_static_rays), int(median_radius), copy, self.image,
                  self.prov, self.n_rays, self.scratch)
-        return _stats_of(stats)
+        mark()
+        out = _stats_of(stats)
+        if timing:
+            marks[-1].synchronize()
+            names = ("descriptors", "mu_raster", "support_build", "solve", "synthesize")
+            out.stage_ms = {n: marks[i].elapsed_time(marks[i + 1]) for i, n in enumerate(names)}
+        return out
+
+    def _event(self):
+        e = self.t.cuda.Event(enable_timing=True)
+        e.record(self.t.cuda.current_stream())
+        return e
 
     # -- outputs ------------------------------------------------------------------------
 
