@@ -98,6 +98,10 @@ int st_device_count(void);
  * threads; CUB's internal launches inside st_support_build / st_solve count
  * as one per CUB call). */
 int64_t st_launch_count(void);
+/* Diagnostics: which = 1 checks the kernels' exact small-integer division
+ * (div_small) against __ddiv_rn on n random doubles x 12 divisors and
+ * returns the number of bit mismatches (expected 0). */
+int st_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* mismatches, void* stream);
 
 /* ---- L1 primitives ---------------------------------------------------- */
 

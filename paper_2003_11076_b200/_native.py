@@ -65,6 +65,7 @@ _SIGS = {
     "st_version": (C.c_int, []),
     "st_device_count": (C.c_int, []),
     "st_launch_count": (C.c_int64, []),
+    "st_selftest": (C.c_int, [_I32, _I64, C.c_uint64, C.POINTER(C.c_int64), _P]),
     "st_descriptors": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
     "st_bilinear": (C.c_int, [_P, _I32, _I32, _I32, _P, _P, _I64, _P, _P]),
     "st_warp": (C.c_int, [C.POINTER(StRig), _I32, _P, _P, _P, _I64, _P, _P, _P, _P]),

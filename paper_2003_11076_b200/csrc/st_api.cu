@@ -88,6 +88,12 @@ int make_ctx(const st_frame* f, const st_rig* rig, const st_params* p, st::EmCtx
   c.tiles_x = (c.W + ST_TW - 1) / ST_TW;
   c.sup_ir = (int)floor(p->neighborhood_radius);
   c.sup_r2 = p->neighborhood_radius * p->neighborhood_radius;
+  int ex = 0;
+  const double mant = frexp(p->sigma, &ex);
+  c.inv_sigma = (p->sigma > 0 && mant == 0.5) ? 1.0 / p->sigma : 0.0;  // exact scaling
+  c.inv_sigma_f = (float)(1.0 / p->sigma);
+  c.gamma_f = (float)p->gamma;
+  for (int n = 0; n <= ST_MAX_VIEWS; ++n) c.recip[n] = n ? 1.0 / (double)n : 0.0;
   return ST_OK;
 }
 
@@ -168,9 +174,64 @@ __global__ void k_warp(st_rig rig, int k, const double* __restrict__ u,
   ok[i] = hz > 0.0 ? 1 : 0;
 }
 
+// Self-test of div_small against __ddiv_rn: x spans many binades and
+// integer-valued / half-integer patterns, n = 1..12.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_selftest_div(int64_t n, unsigned long long seed,
+                               unsigned long long* __restrict__ bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long h = mix64(seed ^ (unsigned long long)i);
+  double x;
+  const int kind = (int)(h & 3);
+  if (kind == 0) {
+    // random mantissa, exponent in [-60, 60]
+    const unsigned long long m = (h >> 12) | 0x3ff0000000000000ull;
+    x = ldexp(__longlong_as_double((long long)m) - 1.0 + 1.0, (int)((h >> 2) & 127) - 63);
+  } else if (kind == 1) {
+    x = (double)(long long)(h >> 20);  // large integers
+  } else if (kind == 2) {
+    x = (double)((h >> 40) & 0xffffff) * 0.5;  // half integers
+  } else {
+    x = __longlong_as_double((long long)((h >> 2) & 0x7fefffffffffffffull));  // any finite
+    if (fabs(x) < 1e-300 || fabs(x) > 1e300) x = 1.0 + (double)(h & 0xffff);
+  }
+  for (int k = 1; k <= 12; ++k) {
+    const double want = __ddiv_rn(x, (double)k);
+    const double got = div_small(x, (double)k, 1.0 / (double)k);
+    if (__double_as_longlong(want) != __double_as_longlong(got) && !(want == 0.0 && got == 0.0))
+      atomicAdd(bad, 1ull);
+  }
+}
+
 }  // namespace st
 
 extern "C" {
+
+int st_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* mismatches, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (which != 1) {
+    sthost::set_error("unknown self-test %d", which);
+    return ST_EINVAL;
+  }
+  unsigned long long* bad = nullptr;
+  ST_CUDA_CHECK(cudaMallocAsync(&bad, sizeof(*bad), s));
+  ST_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(*bad), s));
+  st::k_selftest_div<<<blocks_for(n, 256), 256, 0, s>>>(n, seed, bad);
+  ST_LAUNCH_CHECK("k_selftest_div");
+  unsigned long long h = 0;
+  ST_CUDA_CHECK(cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, s));
+  ST_CUDA_CHECK(cudaFreeAsync(bad, s));
+  ST_CUDA_CHECK(cudaStreamSynchronize(s));
+  *mismatches = (int64_t)h;
+  return ST_OK;
+}
 
 const char* st_last_error(void) { return sthost::g_err; }
 int st_version(void) { return ST_VERSION; }
@@ -336,7 +397,7 @@ static SolveLayout solve_layout(int W, int H) {
   L.active = o;   o += align_up(sizeof(int64_t) * npx);
   L.flags = o;    o += align_up(sizeof(uint32_t) * (npx + 1));
   L.offs = o;     o += align_up(sizeof(uint32_t) * (npx + 1));
-  L.partials = o; o += align_up(sizeof(st::Partial) * L.max_blocks);
+  L.partials = o; o += align_up(sizeof(st::Partial) * L.max_blocks * (EM_BLOCK / 32));
   L.reduced = o;  o += align_up(sizeof(st::Partial) * 66);
   L.cub = o;      o += align_up(L.cub_bytes);
   L.total = o;
@@ -445,7 +506,7 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       st::k_m_step<<<nblk, EM_BLOCK, 0, s>>>(c, a);
       ST_LAUNCH_CHECK("k_m_step");
       ev.record(1, s);
-      st::k_reduce_partials<<<1, 256, 0, s>>>(partials, nblk, reduced + it);
+      st::k_reduce_partials<<<1, 256, 0, s>>>(partials, nblk * (EM_BLOCK / 32), reduced + it);
       ST_LAUNCH_CHECK("k_reduce_partials");
       ev.record(2, s);
       stats->kernel_launches[0] += 1;

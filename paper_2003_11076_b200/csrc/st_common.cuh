@@ -99,10 +99,36 @@ __device__ __forceinline__ double lerp_u8(int g0, int g1, double f) {
   return dadd(i2d_exact(g0), dmul(f, i2d_exact(g1 - g0)));
 }
 
+// Correctly rounded x / n for a small positive integer n with r = RN(1/n):
+// q = RN(x r) is faithful, the residual x - q n is exact in one FMA, and
+// RN(q + (x - q n) r) is the correctly rounded quotient (Markstein's final
+// correction step).  Three DP ops instead of the generic __ddiv_rn sequence;
+// st_selftest(1, ...) checks it against __ddiv_rn bit for bit.
+__device__ __forceinline__ double div_small(double x, double n, double r) {
+  const double q = __dmul_rn(x, r);
+  const double e = __fma_rn(-q, n, x);
+  return __fma_rn(e, r, q);
+}
+
 // prior.py:365-370 -- log(gamma + exp(-z^2/2)), z = (d - mu)/sigma.
-__device__ __forceinline__ double log_prior(double d, double mu, double sigma, double gamma) {
-  double z = ddiv(dsub(d, mu), sigma);
+// inv_sigma != 0 means sigma is a power of two and the division is an exact
+// scaling.
+__device__ __forceinline__ double log_prior(double d, double mu, double sigma, double gamma,
+                                            double inv_sigma = 0.0) {
+  const double dm = dsub(d, mu);
+  const double z = inv_sigma != 0.0 ? dmul(dm, inv_sigma) : ddiv(dm, sigma);
   return log(dadd(gamma, exp(dmul(dmul(-0.5, z), z))));
+}
+
+// A cheap fp32 lower-bound test for the M-step's pruning: true only when the
+// exact -log prior certainly exceeds `best` (the fp32 estimate is within
+// ~1e-6 relative; the margin is 100x that).
+__device__ __forceinline__ bool surely_pruned(double d, double mu, float inv_sigma_f,
+                                              float gamma_f, double best) {
+  if (!(best < 1e30)) return false;
+  const float z = (float)(d - mu) * inv_sigma_f;
+  const float b = -__logf(gamma_f + __expf(-0.5f * z * z));
+  return (double)b > best + 1e-4 * (1.0 + fabs(best));
 }
 
 __device__ __forceinline__ double variance_ceiling() { return 16.0 * 127.5 * 127.5; }

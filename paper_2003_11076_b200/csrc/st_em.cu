@@ -70,7 +70,7 @@ struct Energy {
 };
 
 __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, double d,
-                                            uint32_t bits, double mu) {
+                                            uint32_t bits, double lp) {
   double s1[16], s2[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -94,9 +94,10 @@ __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, 
   double var;
   if (out.real) {
     const double nn = (double)(cnt > 1 ? cnt : 1);
+    const double rn = c.recip[cnt > 1 ? cnt : 1];
     double t[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) t[i] = dsub(s2[i], ddiv(dmul(s1[i], s1[i]), nn));
+    for (int i = 0; i < 16; ++i) t[i] = dsub(s2[i], div_small(dmul(s1[i], s1[i]), nn, rn));
     // numpy's contiguous 16-wide reduction: r_j = t_j + t_{j+8}, then the
     // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) tree.
     double r[8];
@@ -104,11 +105,11 @@ __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, 
     for (int j = 0; j < 8; ++j) r[j] = dadd(t[j], t[j + 8]);
     const double sum = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])),
                             dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
-    var = fmax(ddiv(sum, nn), 0.0);
+    var = fmax(div_small(sum, nn, rn), 0.0);
   } else {
     var = variance_ceiling();
   }
-  out.e = dsub(dmul(c.p.beta, var), log_prior(d, mu, c.p.sigma, c.p.gamma));
+  out.e = dsub(dmul(c.p.beta, var), lp);
   return out;
 }
 
@@ -122,30 +123,14 @@ __device__ __forceinline__ T warp_sum(T x) {
   return x;
 }
 
-// Sum over the block in a fixed order; result valid in thread 0.
-template <typename T>
-__device__ T block_sum(T x, T* smem) {
-  x = warp_sum(x);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) smem[wid] = x;
-  __syncthreads();
-  T s = T(0);
-  if (threadIdx.x == 0) {
-    const int nw = (blockDim.x + 31) >> 5;
-    for (int i = 0; i < nw; ++i) s += smem[i];
-  }
-  __syncthreads();
-  return s;
-}
-
 // ---------------------------------------------------------------------------
 // M-step (solver.py:325-407), with the iteration bookkeeping of solve()
 // (solver.py:463-475) fused in: energy of the previous disparity under the
-// current masks and the changed count.
+// current masks and the changed count.  Statistics leave as one partial per
+// warp (fixed shuffle order, no block barrier), summed in fixed order by
+// k_reduce_partials, so they are deterministic run to run.
 
 __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
-  __shared__ double sh_d[EM_BLOCK / 32];
-  __shared__ long long sh_i[EM_BLOCK / 32];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = i < a.n;
 
@@ -165,10 +150,13 @@ __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
     auto offer = [&](double d) {
       ++n_cand;
       // -log prior bounds the energy from below (var >= 0): exact pruning
-      const double bound = -log_prior(d, mu, c.p.sigma, c.p.gamma);
-      if (!(bound <= be)) return;
+      // (solver.py:341-347).  Far candidates are rejected by a cheap fp32
+      // test; anything close gets the exact fp64 comparison.
+      if (surely_pruned(d, mu, c.inv_sigma_f, c.gamma_f, be)) return;
+      const double lp = log_prior(d, mu, c.p.sigma, c.p.gamma, c.inv_sigma);
+      if (!(-lp <= be)) return;
       ++n_eval;
-      const Energy E = energy_at(c, u, v, d, bits, mu);
+      const Energy E = energy_at(c, u, v, d, bits, lp);
       if (E.e < be || (E.e == be && d < bd)) {
         be = E.e;
         bd = d;
@@ -222,7 +210,8 @@ __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
     if (a.d_prev) {
       const double dp = a.d_prev[i];
       if (!isnan(dp)) {
-        const Energy P = energy_at(c, u, v, dp, bits, mu);
+        const Energy P =
+            energy_at(c, u, v, dp, bits, log_prior(dp, mu, c.p.sigma, c.p.gamma, c.inv_sigma));
         if (isfinite(P.e)) {
           pe_fin = P.e;
           n_pfin = 1;
@@ -233,15 +222,15 @@ __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
     }
   }
   if (a.partials) {
-    const double s_e = block_sum(e_fin, sh_d);
-    const double s_pe = block_sum(pe_fin, sh_d);
-    const long long c_fin = block_sum(n_fin, sh_i);
-    const long long c_pfin = block_sum(n_pfin, sh_i);
-    const long long c_ch = block_sum(n_changed, sh_i);
-    const long long c_cand = block_sum(n_cand, sh_i);
-    const long long c_eval = block_sum(n_eval, sh_i);
-    if (threadIdx.x == 0) {
-      Partial& P = a.partials[blockIdx.x];
+    const double s_e = warp_sum(e_fin);
+    const double s_pe = warp_sum(pe_fin);
+    const long long c_fin = warp_sum(n_fin);
+    const long long c_pfin = warp_sum(n_pfin);
+    const long long c_ch = warp_sum(n_changed);
+    const long long c_cand = warp_sum(n_cand);
+    const long long c_eval = warp_sum(n_eval);
+    if ((threadIdx.x & 31) == 0) {
+      Partial& P = a.partials[(blockIdx.x * blockDim.x + threadIdx.x) >> 5];
       P.sum_e = s_e;
       P.sum_pe = s_pe;
       P.n_fin = c_fin;
@@ -279,14 +268,18 @@ __device__ __forceinline__ bool prefer(double s, int pop, uint32_t m, double bs,
   return m < bm;
 }
 
+__constant__ double c_recip[13] = {0.0,       1.0 / 1,  1.0 / 2,  1.0 / 3, 1.0 / 4,
+                                   1.0 / 5,   1.0 / 6,  1.0 / 7,  1.0 / 8, 1.0 / 9,
+                                   1.0 / 10,  1.0 / 11, 1.0 / 12};
+
 __device__ __forceinline__ double div_n(double x, int n) {
-  // powers of two scale exactly; other counts need the IEEE division
+  // powers of two scale exactly; other counts use the exact small divisor
   switch (n) {
     case 1: return x;
     case 2: return dmul(x, 0.5);
     case 4: return dmul(x, 0.25);
     case 8: return dmul(x, 0.125);
-    default: return ddiv(x, (double)n);
+    default: return div_small(x, (double)n, c_recip[n]);
   }
 }
 
@@ -505,7 +498,8 @@ __global__ void k_energy(EmCtx c, const int64_t* __restrict__ pix, const double*
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t p = pix[i];
-  const Energy E = energy_at(c, (double)(p % c.W), (double)(p / c.W), d[i], bits[i], c.mu[p]);
+  const double lp = log_prior(d[i], c.mu[p], c.p.sigma, c.p.gamma, c.inv_sigma);
+  const Energy E = energy_at(c, (double)(p % c.W), (double)(p / c.W), d[i], bits[i], lp);
   e[i] = E.e;
   real[i] = E.real ? 1 : 0;
 }

@@ -29,6 +29,10 @@ struct EmCtx {
   int tiles_x;
   int sup_ir;
   double sup_r2;
+  double inv_sigma;     // 1/sigma when sigma is a power of two (exact), else 0
+  float inv_sigma_f;    // fp32 1/sigma for the pruning pre-test
+  float gamma_f;
+  double recip[ST_MAX_VIEWS + 1];  // RN(1/n), n = 1..12, for div_small
 };
 
 struct Partial {

@@ -84,6 +84,16 @@ def _solver(st, g):
 
 # -- L1 primitives -------------------------------------------------------------------
 
+def test_exact_small_division_selftest(st):
+    """The kernels divide by ray counts with a 3-FMA Markstein step; it must
+    equal IEEE division bit for bit."""
+    import ctypes
+    from paper_2003_11076_b200 import _native as N
+    for seed in (1, 2, 3):
+        bad = ctypes.c_int64(-1)
+        N.check(N.lib().st_selftest(1, 1 << 24, seed, bad, N.stream_handle()))
+        assert bad.value == 0
+
 def test_descriptors_gray_sobel_exact(st):
     z = cases("sampling_cases")
     for im, g, d in zip(z["desc_images"], z["desc_gray"], z["desc_out"]):
