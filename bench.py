@@ -385,8 +385,11 @@ def run_ours(args):
         peak, peak_src = 6650.0, "fallback"
     achieved = bytes_m / (ms_m / 1e3) / 1e9
     npx = w * h
-    c_bar = s0.candidates_total / max(1, npx * s0.iterations_run)
-    frame_bytes = npx * (s0.iterations_run * (c_bar * k * 16 + k * 20) + 7 * k)
+    c_bar = s0.candidates_total / max(1, s0.msteps)
+    # SURVEY 8d model, charged for the pixel M/E-steps the incremental EM runs
+    frame_bytes = s0.msteps * c_bar * k * 16 + s0.esteps * k * 20 + npx * 7 * k
+    # the same model charging every pixel every iteration (full recompute)
+    model_full = npx * (s0.iterations_run * (c_bar * k * 16 + k * 20) + 7 * k)
     step_ms_mean = total_ms / args.steps
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
@@ -419,15 +422,19 @@ def run_ours(args):
                      "share_of_step": ms_m / step_ms_mean},
         "frame_roofline": {"model_bytes": frame_bytes, "achieved_gbs":
                            frame_bytes / (step_ms_mean / 1e3) / 1e9,
-                           "frac": frame_bytes / (step_ms_mean / 1e3) / 1e9 / peak},
+                           "frac": frame_bytes / (step_ms_mean / 1e3) / 1e9 / peak,
+                           "model_bytes_full_recompute": model_full,
+                           "frac_full_recompute_model":
+                               model_full / (step_ms_mean / 1e3) / 1e9 / peak},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / e2e_steps},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "em": {"iterations_run": s0.iterations_run, "converged_after": s0.converged_after,
-               "candidates_per_px_iter": c_bar,
-               "energy_evals_per_px_iter": s0.energy_evals / max(1, npx * s0.iterations_run),
+               "candidates_per_mstep": c_bar,
+               "energy_evals_per_mstep": s0.energy_evals / max(1, s0.msteps),
+               "pixel_msteps": s0.msteps, "pixel_esteps": s0.esteps,
                "kernel_ms": {"m_step": ms_m,
                              "e_step": float(np.mean([s.kernel_ms[1] for s in stats])),
                              "initial_masks": float(np.mean([s.kernel_ms[2] for s in stats])),

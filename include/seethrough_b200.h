@@ -84,7 +84,9 @@ typedef struct {
   int64_t support_records;           /* diagnostic: (tile, value) records built */
   int64_t candidates_total;          /* sum over iterations/pixels of candidates in range */
   int64_t energy_evals;              /* sum of candidate energies actually evaluated */
-  int64_t prev_evals;                /* previous-disparity energies (iterations >= 2) */
+  int64_t prev_evals;                /* previous-disparity energies computed (iterations >= 2) */
+  int64_t msteps;                    /* pixel M-steps computed (incremental EM skips the rest) */
+  int64_t esteps;                    /* pixel E-steps computed */
   /* with st_params.timing: summed CUDA-event durations per kernel family
    * [0] k_m_step, [1] k_e_step_at, [2] k_initial_masks, [3] the rest */
   double kernel_ms[4];

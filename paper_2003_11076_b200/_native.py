@@ -37,6 +37,7 @@ class StStats(C.Structure):
                 ("changed_fraction", C.c_double * 64), ("active_pixels", C.c_int64),
                 ("support_records", C.c_int64), ("candidates_total", C.c_int64),
                 ("energy_evals", C.c_int64), ("prev_evals", C.c_int64),
+                ("msteps", C.c_int64), ("esteps", C.c_int64),
                 ("kernel_ms", C.c_double * 4), ("kernel_launches", C.c_int32 * 4)]
 
 

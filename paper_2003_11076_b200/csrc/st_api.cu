@@ -321,9 +321,10 @@ int st_m_step(const st_frame* f, const st_rig* rig, const st_params* p, const in
   a.active = active;
   a.n = n;
   a.static_all = static_all;
-  a.d_out = d_out;
-  a.e_out = e_out;
-  a.status_out = status_out;
+  a.first = 1;
+  a.d = d_out;
+  a.e = e_out;
+  a.status = status_out;
   st::k_m_step<<<blocks_for(n, EM_BLOCK), EM_BLOCK, 0, (cudaStream_t)stream>>>(c, a);
   ST_LAUNCH_CHECK("k_m_step");
   return ST_OK;
@@ -376,28 +377,35 @@ int st_masked_variance(const double* desc, const uint8_t* mask, int64_t n, int32
 // fused solve
 
 struct SolveLayout {
-  size_t d0, d1, e, st_act, active, flags, offs, partials, reduced, cub, total;
+  size_t d, e, pe, st_act, chg, mask_in, mlist, elist, counts, active, flags, offs, work,
+      parts, reduced, cub, total;
   size_t cub_bytes;
-  int max_blocks;
+  int max_warps;
 };
 
 static SolveLayout solve_layout(int W, int H) {
   SolveLayout L;
   const int64_t npx = (int64_t)W * H;
-  L.max_blocks = (int)blocks_for(npx, EM_BLOCK);
+  L.max_warps = (int)blocks_for(npx, EM_BLOCK) * (EM_BLOCK / 32);
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                 (int)(npx + 1));
   L.cub_bytes = scan_bytes;
   size_t o = 0;
-  L.d0 = o;       o += align_up(sizeof(double) * npx);
-  L.d1 = o;       o += align_up(sizeof(double) * npx);
+  L.d = o;        o += align_up(sizeof(double) * npx);
   L.e = o;        o += align_up(sizeof(double) * npx);
+  L.pe = o;       o += align_up(sizeof(double) * npx);
   L.st_act = o;   o += align_up(npx);
+  L.chg = o;      o += align_up(npx);
+  L.mask_in = o;  o += align_up(sizeof(uint32_t) * npx);
+  L.mlist = o;    o += align_up(sizeof(int32_t) * npx);
+  L.elist = o;    o += align_up(sizeof(int32_t) * npx);
+  L.counts = o;   o += align_up(sizeof(uint32_t) * 2);
   L.active = o;   o += align_up(sizeof(int64_t) * npx);
   L.flags = o;    o += align_up(sizeof(uint32_t) * (npx + 1));
   L.offs = o;     o += align_up(sizeof(uint32_t) * (npx + 1));
-  L.partials = o; o += align_up(sizeof(st::Partial) * L.max_blocks * (EM_BLOCK / 32));
+  L.work = o;     o += align_up(sizeof(st::Partial) * L.max_warps);
+  L.parts = o;    o += align_up(sizeof(st::Partial) * L.max_warps);
   L.reduced = o;  o += align_up(sizeof(st::Partial) * 66);
   L.cub = o;      o += align_up(L.cub_bytes);
   L.total = o;
@@ -427,13 +435,20 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
     return ST_ENOMEM;
   }
   char* ws = (char*)workspace;
-  double* dbuf[2] = {(double*)(ws + L.d0), (double*)(ws + L.d1)};
+  double* d_act = (double*)(ws + L.d);
   double* e_act = (double*)(ws + L.e);
+  double* pe_act = (double*)(ws + L.pe);
   uint8_t* st_act = (uint8_t*)(ws + L.st_act);
+  uint8_t* chg = (uint8_t*)(ws + L.chg);
+  uint32_t* mask_in = (uint32_t*)(ws + L.mask_in);
+  int32_t* mlist = (int32_t*)(ws + L.mlist);
+  int32_t* elist = (int32_t*)(ws + L.elist);
+  uint32_t* counts = (uint32_t*)(ws + L.counts);
   int64_t* active = (int64_t*)(ws + L.active);
   uint32_t* flags = (uint32_t*)(ws + L.flags);
   uint32_t* offs = (uint32_t*)(ws + L.offs);
-  st::Partial* partials = (st::Partial*)(ws + L.partials);
+  st::Partial* work = (st::Partial*)(ws + L.work);
+  st::Partial* parts = (st::Partial*)(ws + L.parts);
   st::Partial* reduced = (st::Partial*)(ws + L.reduced);
 
   memset(stats, 0, sizeof(*stats));
@@ -483,40 +498,52 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
 
   const int iters = p->forced_iters > 0 ? p->forced_iters : p->max_iters;
   const int nblk = (int)blocks_for(n_act, EM_BLOCK);
-  int last = -1;  // buffer holding the final d
+  const int nwarps = nblk * (EM_BLOCK / 32);
+  bool solved = false;
   for (int it = 1; it <= iters && it <= 64; ++it) {
     if (n_act_global == 0) {
       stats->converged_after = 0;
       break;
     }
     stats->iterations_run = it;
-    double* d_cur = dbuf[it & 1];
-    const double* d_prev = it > 1 ? dbuf[(it - 1) & 1] : nullptr;
     if (n_act > 0) {
+      // Incremental EM (see k_m_step): iteration 1 solves every slot; later
+      // iterations re-solve only slots whose mask changed, and re-run the
+      // E-step only where d changed.  Both steps are pure per-pixel
+      // functions of those inputs, so the result is bit-identical to a
+      // full recomputation.
+      ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), s));
+      ev.record(0, s);
+      if (it > 1) {
+        st::k_flag_mstep<<<nblk, EM_BLOCK, 0, s>>>(act_ptr, n_act, static_bits, mask_in, e_act,
+                                                   pe_act, chg, mlist, counts);
+        ST_LAUNCH_CHECK("k_flag_mstep");
+      }
       st::MStepArgs a = {};
       a.active = act_ptr;
       a.n = n_act;
+      a.list = it > 1 ? mlist : nullptr;
+      a.list_count = counts;
       a.static_all = static_bits;
-      a.d_prev = d_prev;
-      a.d_out = d_cur;
-      a.e_out = e_act;
-      a.status_out = st_act;
-      a.partials = partials;
-      ev.record(0, s);
+      a.first = it == 1;
+      a.d = d_act;
+      a.e = e_act;
+      a.status = st_act;
+      a.mask_in = mask_in;
+      a.pe = pe_act;
+      a.chg = chg;
+      a.elist = elist;
+      a.elist_count = counts + 1;
+      a.partials = work;
       st::k_m_step<<<nblk, EM_BLOCK, 0, s>>>(c, a);
       ST_LAUNCH_CHECK("k_m_step");
       ev.record(1, s);
-      st::k_reduce_partials<<<1, 256, 0, s>>>(partials, nblk * (EM_BLOCK / 32), reduced + it);
-      ST_LAUNCH_CHECK("k_reduce_partials");
-      ev.record(2, s);
-      stats->kernel_launches[0] += 1;
-      stats->kernel_launches[1] += 1;
-      stats->kernel_launches[3] += 1;
-      // E-step on solved pixels, in place (each pixel owns its slot)
       st::EStepArgs e = {};
       e.pix = act_ptr;
       e.n = n_act;
-      e.d = d_cur;
+      e.list = elist;
+      e.list_count = counts + 1;
+      e.d = d_act;
       e.status = st_act;
       e.static_out = static_bits;
       e.valid_out = valid_bits;
@@ -524,18 +551,33 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       st::k_e_step_at<<<blocks_for(n_act, ESTEP_BLOCK), ESTEP_BLOCK, estep_smem(rig->num_views),
                         s>>>(c, e);
       ST_LAUNCH_CHECK("k_e_step_at");
+      ev.record(2, s);
+      st::k_em_stats<<<nblk, EM_BLOCK, 0, s>>>(n_act, it > 1, e_act, pe_act, chg, work, nwarps,
+                                               parts);
+      ST_LAUNCH_CHECK("k_em_stats");
+      st::k_reduce_partials<<<1, 256, 0, s>>>(parts, nwarps, reduced + it);
+      ST_LAUNCH_CHECK("k_reduce_partials");
       ev.record(3, s);
+      stats->kernel_launches[0] += 1;
+      stats->kernel_launches[1] += 1;
+      stats->kernel_launches[3] += it > 1 ? 3 : 2;
+      solved = true;
     } else {
       ST_CUDA_CHECK(cudaMemsetAsync(reduced + it, 0, sizeof(st::Partial), s));
     }
-    last = it & 1;
     st::Partial r;
+    uint32_t work_counts[2] = {0, 0};
     ST_CUDA_CHECK(cudaMemcpyAsync(&r, reduced + it, sizeof(r), cudaMemcpyDeviceToHost, s));
+    ST_CUDA_CHECK(cudaMemcpyAsync(work_counts, counts, sizeof(work_counts),
+                                  cudaMemcpyDeviceToHost, s));
     ST_CUDA_CHECK(cudaStreamSynchronize(s));
+    stats->msteps += it > 1 ? work_counts[0] : n_act;
+    stats->esteps += work_counts[1];
+    if (it > 1) stats->prev_evals += work_counts[0];
     if (n_act > 0) {
       stats->kernel_ms[0] += ev.ms(0, 1);
-      stats->kernel_ms[3] += ev.ms(1, 2);
-      stats->kernel_ms[1] += ev.ms(2, 3);
+      stats->kernel_ms[1] += ev.ms(1, 2);
+      stats->kernel_ms[3] += ev.ms(2, 3);
     }
     if (it == 1) stats->kernel_ms[2] += ev.ms(4, 5);
     double v[7] = {r.sum_e, (double)r.n_fin, r.sum_pe, (double)r.n_pfin, (double)r.n_changed,
@@ -547,7 +589,6 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
     stats->mean_energy[it - 1] = v[1] > 0 ? v[0] / v[1] : NAN;
     stats->candidates_total += (int64_t)v[5];
     stats->energy_evals += (int64_t)v[6];
-    stats->prev_evals += (int64_t)v[3];
     if (it > 1) {
       stats->prev_energy[it - 2] = v[3] > 0 ? v[2] / v[3] : NAN;
       const double changed = v[4] / n_act_global;
@@ -562,15 +603,14 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
   // outputs (solver.py:491-500)
   if (dense) {
     st::k_pack_outputs<<<blocks_for(npx, 256), 256, 0, s>>>(
-        f->mu, npx, nullptr, npx, last >= 0 ? dbuf[last] : nullptr, st_act, values, status, 1);
+        f->mu, npx, nullptr, npx, solved ? d_act : nullptr, st_act, values, status, 1);
     ST_LAUNCH_CHECK("k_pack_outputs");
   } else {
     st::k_fill_mu<<<blocks_for(npx, 256), 256, 0, s>>>(f->mu, npx, values, status);
     ST_LAUNCH_CHECK("k_fill_mu");
-    if (last >= 0 && n_act > 0) {
-      st::k_pack_outputs<<<blocks_for(n_act, 256), 256, 0, s>>>(f->mu, npx, active, n_act,
-                                                                dbuf[last], st_act, values,
-                                                                status, 0);
+    if (solved && n_act > 0) {
+      st::k_pack_outputs<<<blocks_for(n_act, 256), 256, 0, s>>>(f->mu, npx, active, n_act, d_act,
+                                                                st_act, values, status, 0);
       ST_LAUNCH_CHECK("k_pack_outputs");
     }
   }

@@ -93,8 +93,8 @@ __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, 
   out.real = cnt >= c.p.min_static_rays;
   double var;
   if (out.real) {
-    const double nn = (double)(cnt > 1 ? cnt : 1);
-    const double rn = c.recip[cnt > 1 ? cnt : 1];
+    const double nn = (double)cnt;
+    const double rn = c.recip[cnt];
     double t[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) t[i] = dsub(s2[i], div_small(dmul(s1[i], s1[i]), nn, rn));
@@ -123,19 +123,40 @@ __device__ __forceinline__ T warp_sum(T x) {
   return x;
 }
 
+// Warp-aggregated append of `slot` to a worklist (one atomic per warp).  The
+// list order depends on scheduling; every consumer's per-slot result does
+// not, and statistics are summed per slot elsewhere, so results stay
+// deterministic.
+__device__ __forceinline__ void list_append(bool want, int32_t slot, int32_t* list,
+                                            uint32_t* count) {
+  const unsigned ballot = __ballot_sync(0xffffffffu, want);
+  if (!ballot) return;
+  const int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == __ffs(ballot) - 1) base = atomicAdd(count, (unsigned)__popc(ballot));
+  base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
+  if (want) list[base + __popc(ballot & ((1u << lane) - 1))] = slot;
+}
+
 // ---------------------------------------------------------------------------
-// M-step (solver.py:325-407), with the iteration bookkeeping of solve()
-// (solver.py:463-475) fused in: energy of the previous disparity under the
-// current masks and the changed count.  Statistics leave as one partial per
-// warp (fixed shuffle order, no block barrier), summed in fixed order by
-// k_reduce_partials, so they are deterministic run to run.
+// M-step (solver.py:325-407).  Incremental EM: m_step is a pure function of
+// (pixel, static mask) -- the candidate set is fixed per solve -- so from the
+// second iteration on only slots whose mask changed since their last M-step
+// are recomputed (k_flag_mstep builds that worklist); the others keep d, E and
+// status bit for bit, and the previous-disparity energy of solve()
+// (solver.py:468-471) equals their stored E.  Worked slots also get the
+// previous-disparity energy and the |d - d_prev| > 0.5 flag here, and append
+// themselves to the E-step worklist when their d changed (e_step_at is a pure
+// function of (pixel, d)).
 
 __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i < a.n;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
+  const bool live = t < n_work;
+  const int64_t i = live ? (a.list ? (int64_t)a.list[t] : t) : 0;
 
-  double e_fin = 0.0, pe_fin = 0.0;
-  long long n_fin = 0, n_pfin = 0, n_changed = 0, n_cand = 0, n_eval = 0;
+  long long n_cand = 0, n_eval = 0;
+  bool want_e = false;
 
   if (live) {
     const int64_t pix = a.active ? a.active[i] : i;
@@ -200,45 +221,101 @@ __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
     } else if (!br) {
       status = ST_STATUS_NO_STATIC_EVIDENCE;
     }
-    a.d_out[i] = bd;
-    a.e_out[i] = be;
-    a.status_out[i] = status;
-    if (isfinite(be)) {
-      e_fin = be;
-      n_fin = 1;
-    }
-    if (a.d_prev) {
-      const double dp = a.d_prev[i];
-      if (!isnan(dp)) {
-        const Energy P =
-            energy_at(c, u, v, dp, bits, log_prior(dp, mu, c.p.sigma, c.p.gamma, c.inv_sigma));
-        if (isfinite(P.e)) {
-          pe_fin = P.e;
-          n_pfin = 1;
-        }
-      }
+    if (!a.first) {
+      const double dp = a.d[i];  // previous disparity (in place)
+      double pe = NAN;
+      if (!isnan(dp))
+        pe = energy_at(c, u, v, dp, bits, log_prior(dp, mu, c.p.sigma, c.p.gamma, c.inv_sigma)).e;
+      a.pe[i] = pe;
       // |d - d_prev| > 0.5 with NaN -> False (solver.py:472-475)
-      if (fabs(bd - dp) > 0.5) n_changed = 1;
+      a.chg[i] = fabs(bd - dp) > 0.5 ? 1 : 0;
+      want_e = status != ST_STATUS_LOW_TEXTURE &&
+               __double_as_longlong(bd) != __double_as_longlong(dp);
+    } else {
+      want_e = status != ST_STATUS_LOW_TEXTURE;
     }
+    a.d[i] = bd;
+    a.e[i] = be;
+    a.status[i] = status;
+    if (a.mask_in) a.mask_in[i] = bits;
   }
+  if (a.elist) list_append(want_e, (int32_t)i, a.elist, a.elist_count);
   if (a.partials) {
-    const double s_e = warp_sum(e_fin);
-    const double s_pe = warp_sum(pe_fin);
-    const long long c_fin = warp_sum(n_fin);
-    const long long c_pfin = warp_sum(n_pfin);
-    const long long c_ch = warp_sum(n_changed);
     const long long c_cand = warp_sum(n_cand);
     const long long c_eval = warp_sum(n_eval);
     if ((threadIdx.x & 31) == 0) {
       Partial& P = a.partials[(blockIdx.x * blockDim.x + threadIdx.x) >> 5];
-      P.sum_e = s_e;
-      P.sum_pe = s_pe;
-      P.n_fin = c_fin;
-      P.n_pfin = c_pfin;
-      P.n_changed = c_ch;
       P.n_cand = c_cand;
       P.n_eval = c_eval;
     }
+  }
+}
+
+// Iteration >= 2: which slots need a new M-step (mask changed since their
+// last one).  The others carry their previous-disparity energy (= their E)
+// and changed = 0 into the statistics.
+__global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n,
+                             const uint32_t* __restrict__ static_all,
+                             const uint32_t* __restrict__ mask_in, const double* __restrict__ e,
+                             double* __restrict__ pe, uint8_t* __restrict__ chg,
+                             int32_t* __restrict__ list, uint32_t* __restrict__ count) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool want = false;
+  if (i < n) {
+    const int64_t pix = active ? active[i] : i;
+    want = static_all[pix] != mask_in[i];
+    if (!want) {
+      pe[i] = e[i];
+      chg[i] = 0;
+    }
+  }
+  list_append(want, (int32_t)i, list, count);
+}
+
+// Per-iteration statistics over every active slot, as fixed-order per-warp
+// partials (solver.py:463-475: mean of finite E, mean of finite previous
+// energies, changed count).
+__global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ e,
+                           const double* __restrict__ pe, const uint8_t* __restrict__ chg,
+                           const Partial* __restrict__ work, int n_work_parts,
+                           Partial* __restrict__ parts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double se = 0.0, spe = 0.0;
+  long long nf = 0, npf = 0, nch = 0;
+  if (i < n) {
+    const double x = e[i];
+    if (isfinite(x)) {
+      se = x;
+      nf = 1;
+    }
+    if (with_prev) {
+      const double y = pe[i];
+      if (isfinite(y)) {
+        spe = y;
+        npf = 1;
+      }
+      nch = chg[i];
+    }
+  }
+  se = warp_sum(se);
+  spe = warp_sum(spe);
+  nf = warp_sum(nf);
+  npf = warp_sum(npf);
+  nch = warp_sum(nch);
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t w = i >> 5;
+    Partial P = {};
+    P.sum_e = se;
+    P.sum_pe = spe;
+    P.n_fin = nf;
+    P.n_pfin = npf;
+    P.n_changed = nch;
+    // fold the M-step's work counters (warp w of that launch) in as well
+    if (w < n_work_parts) {
+      P.n_cand = work[w].n_cand;
+      P.n_eval = work[w].n_eval;
+    }
+    parts[w] = P;
   }
 }
 
@@ -429,8 +506,10 @@ __device__ __forceinline__ uint32_t gather_pixel(const EmCtx& c, double u, doubl
 
 __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a) {
   extern __shared__ double sh_f[];
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
+  if (t >= n_work) return;
+  const int64_t i = a.list ? (int64_t)a.list[t] : t;
   if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) return;  // solver.py:476-478
   const int64_t pix = a.pix ? a.pix[i] : i;
   const double u = (double)(pix % c.W), v = (double)(pix / c.W);

@@ -40,20 +40,31 @@ struct Partial {
   long long n_fin, n_pfin, n_changed, n_cand, n_eval;
 };
 
+// Slots are the rows of the active set (slot i -> pixel active[i], or i when
+// dense).  All per-slot arrays are indexed by slot.
 struct MStepArgs {
-  const int64_t* active;     // nullable: dense over all pixels
-  int64_t n;
-  const uint32_t* static_all;
-  const double* d_prev;      // nullable: first iteration
-  double* d_out;
-  double* e_out;
-  uint8_t* status_out;
-  Partial* partials;         // nullable: one per block
+  const int64_t* active;       // nullable: dense over all pixels
+  int64_t n;                   // number of slots
+  const int32_t* list;         // nullable: worklist of slots (count in *list_count)
+  const uint32_t* list_count;
+  const uint32_t* static_all;  // per pixel
+  int first;                   // 1: no previous disparity (iteration 1 / API)
+  double* d;                   // out; in = previous disparity when !first
+  double* e;
+  uint8_t* status;
+  uint32_t* mask_in;           // nullable: mask each slot was solved with
+  double* pe;                  // !first: energy of the previous d under the mask
+  uint8_t* chg;                // !first: |d - d_prev| > 0.5
+  int32_t* elist;              // nullable: E-step worklist (append)
+  uint32_t* elist_count;
+  Partial* partials;           // nullable: per-warp work counters
 };
 
 struct EStepArgs {
   const int64_t* pix;        // nullable: dense
   int64_t n;
+  const int32_t* list;       // nullable: worklist of rows (count in *list_count)
+  const uint32_t* list_count;
   const double* d;
   const uint8_t* status;     // nullable; LOW_TEXTURE rows are skipped
   uint32_t* static_out;
@@ -62,6 +73,12 @@ struct EStepArgs {
 };
 
 __global__ void k_m_step(EmCtx c, MStepArgs a);
+__global__ void k_flag_mstep(const int64_t* active, int64_t n, const uint32_t* static_all,
+                             const uint32_t* mask_in, const double* e, double* pe, uint8_t* chg,
+                             int32_t* list, uint32_t* count);
+__global__ void k_em_stats(int64_t n, int with_prev, const double* e, const double* pe,
+                           const uint8_t* chg, const Partial* work, int n_work_parts,
+                           Partial* parts);
 __global__ void k_e_step_at(EmCtx c, EStepArgs a);
 __global__ void k_initial_masks(EmCtx c, const int64_t* pix, int64_t n, uint32_t* static_out,
                                 uint32_t* valid_out);

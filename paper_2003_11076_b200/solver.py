@@ -283,6 +283,8 @@ def _stats_of(s):
     st.candidates_total = int(s.candidates_total)
     st.energy_evals = int(s.energy_evals)
     st.prev_evals = int(s.prev_evals)
+    st.msteps = int(s.msteps)
+    st.esteps = int(s.esteps)
     st.support_records = int(s.support_records)
     st.kernel_ms = [float(x) for x in s.kernel_ms]
     st.kernel_launches = [int(x) for x in s.kernel_launches]
