@@ -91,8 +91,18 @@ int make_ctx(const st_frame* f, const st_rig* rig, const st_params* p, st::EmCtx
   int ex = 0;
   const double mant = frexp(p->sigma, &ex);
   c.inv_sigma = (p->sigma > 0 && mant == 0.5) ? 1.0 / p->sigma : 0.0;  // exact scaling
-  c.inv_sigma_f = (float)(1.0 / p->sigma);
+  c.sigma_f = (float)p->sigma;
   c.gamma_f = (float)p->gamma;
+  // rectified rig: h = (u + d bx, v, 1) exactly (the general left-to-right
+  // formula reduces to these roundings when A = I and b_y = b_z = 0)
+  c.rectified = 1;
+  for (int k = 0; k < rig->num_views; ++k) {
+    const double* a = rig->warp_a[k];
+    const double* b = rig->warp_b[k];
+    const bool eye = a[0] == 1.0 && a[1] == 0.0 && a[2] == 0.0 && a[3] == 0.0 && a[4] == 1.0 &&
+                     a[5] == 0.0 && a[6] == 0.0 && a[7] == 0.0 && a[8] == 1.0;
+    if (!eye || b[1] != 0.0 || b[2] != 0.0 || !(fabs(b[0]) < 1e300)) c.rectified = 0;
+  }
   for (int n = 0; n <= ST_MAX_VIEWS; ++n) c.recip[n] = n ? 1.0 / (double)n : 0.0;
   return ST_OK;
 }
@@ -552,10 +562,11 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
                         s>>>(c, e);
       ST_LAUNCH_CHECK("k_e_step_at");
       ev.record(2, s);
-      st::k_em_stats<<<nblk, EM_BLOCK, 0, s>>>(n_act, it > 1, e_act, pe_act, chg, work, nwarps,
-                                               parts);
+      const int sblk = (int)blocks_for(n_act, STATS_BLOCK);
+      st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(n_act, it > 1, e_act, pe_act, chg, work, nwarps,
+                                                  parts);
       ST_LAUNCH_CHECK("k_em_stats");
-      st::k_reduce_partials<<<1, 256, 0, s>>>(parts, nwarps, reduced + it);
+      st::k_reduce_partials<<<1, 256, 0, s>>>(parts, sblk, reduced + it);
       ST_LAUNCH_CHECK("k_reduce_partials");
       ev.record(3, s);
       stats->kernel_launches[0] += 1;

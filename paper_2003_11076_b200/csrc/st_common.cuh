@@ -120,15 +120,20 @@ __device__ __forceinline__ double log_prior(double d, double mu, double sigma, d
   return log(dadd(gamma, exp(dmul(dmul(-0.5, z), z))));
 }
 
-// A cheap fp32 lower-bound test for the M-step's pruning: true only when the
-// exact -log prior certainly exceeds `best` (the fp32 estimate is within
-// ~1e-6 relative; the margin is 100x that).
-__device__ __forceinline__ bool surely_pruned(double d, double mu, float inv_sigma_f,
-                                              float gamma_f, double best) {
-  if (!(best < 1e30)) return false;
-  const float z = (float)(d - mu) * inv_sigma_f;
-  const float b = -__logf(gamma_f + __expf(-0.5f * z * z));
-  return (double)b > best + 1e-4 * (1.0 + fabs(best));
+// Pruning radius for the M-step: -log prior(d) = -log(gamma + exp(-z^2/2))
+// grows with |d - mu|, so it exceeds the incumbent energy `best` exactly when
+// |d - mu| > sigma sqrt(-2 ln(exp(-best) - gamma)).  Computed in fp32 once
+// per incumbent change; callers prune only beyond the radius plus a margin
+// (1e-4 relative + 0.01 absolute) far larger than the fp32 error (the
+// argument is kept >= 1e-3, so |d ln x| < 1e-4), and run the exact fp64
+// comparison for everything inside it.
+__device__ __forceinline__ double prune_radius(double best, float sigma_f, float gamma_f) {
+  if (!(best < 1e30)) return INFINITY;
+  const float x = expf(-(float)best) - gamma_f;
+  if (!(x >= 1e-3f)) return INFINITY;  // nothing prunable (best near -log gamma)
+  if (x >= 1.0f) return 0.0;           // best below every bound
+  const float r = sigma_f * sqrtf(-2.0f * logf(x));
+  return (double)r * (1.0 + 1e-4) + 0.01;
 }
 
 __device__ __forceinline__ double variance_ceiling() { return 16.0 * 127.5 * 127.5; }

@@ -20,6 +20,26 @@ namespace st {
 // 16-channel bilinear descriptor sample, fp64 recipe (sampling.py:49-55 on
 // the float32 copy of the uint8 map: tap differences are exact integers).
 // Calls `sink(c, f)` for each channel in order.
+// Four channels of one 32-bit descriptor word pair: exact g0 and g1 - g0 as
+// doubles via the 2^52 trick (one PRMT / paired 16-bit SIMD difference + one
+// DADD each), then the fp64 lerp g0 + fu * (g1 - g0).
+__device__ __forceinline__ void lerp_word(uint32_t wa, uint32_t wb, double fu, double (&f)[4]) {
+  const uint32_t ea = wa & 0x00ff00ffu, eb = wb & 0x00ff00ffu;
+  const uint32_t oa = (wa >> 8) & 0x00ff00ffu, ob = (wb >> 8) & 0x00ff00ffu;
+  const uint32_t de = eb + 0x01000100u - ea;  // bytes 0 and 2: (g1 - g0 + 256) per 16-bit lane
+  const uint32_t dodd = ob + 0x01000100u - oa;  // bytes 1 and 3
+  const uint32_t lanes[4] = {__byte_perm(de, 0u, 0x4410), __byte_perm(dodd, 0u, 0x4410),
+                             __byte_perm(de, 0u, 0x4432), __byte_perm(dodd, 0u, 0x4432)};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double g0 = __dsub_rn(__hiloint2double(0x43300000, __byte_perm(wa, 0u, 0x4440 | j)),
+                                4503599627370496.0);          // 2^52
+    const double df = __dsub_rn(__hiloint2double(0x43300000, lanes[j]),
+                                4503599627370752.0);          // 2^52 + 256
+    f[j] = dadd(g0, dmul(fu, df));
+  }
+}
+
 template <typename Sink>
 __device__ __forceinline__ void sample_desc(const uint4* __restrict__ plane, int W, const Taps& t,
                                             Sink&& sink) {
@@ -30,10 +50,11 @@ __device__ __forceinline__ void sample_desc(const uint4* __restrict__ plane, int
   const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
   if (t.fv == 0.0) {
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const int g0 = (aw[c >> 2] >> (8 * (c & 3))) & 0xff;
-      const int g1 = (bw[c >> 2] >> (8 * (c & 3))) & 0xff;
-      sink(c, lerp_u8(g0, g1, t.fu));
+    for (int w = 0; w < 4; ++w) {
+      double f[4];
+      lerp_word(aw[w], bw[w], t.fu, f);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sink(4 * w + j, f[j]);
     }
   } else {
     const uint4 e = __ldg(plane + base + t.sv);
@@ -61,6 +82,19 @@ __device__ __forceinline__ double sample_prior(const float* __restrict__ plane, 
   return dadd(top, dmul(t.fv, dsub(bot, top)));
 }
 
+// Warp with the rectified-rig shortcut (identical roundings, see make_ctx).
+__device__ __forceinline__ WarpOut warp_ctx(const EmCtx& c, int k, double u, double v,
+                                            double d) {
+  if (c.rectified) {
+    WarpOut o;
+    o.pu = dadd(u, dmul(d, c.rig.warp_b[k][0]));
+    o.pv = v;
+    o.front = true;
+    return o;
+  }
+  return warp_to(c.rig, k, u, v, d);
+}
+
 // ---------------------------------------------------------------------------
 // energy (solver.py:229-260)
 
@@ -80,7 +114,7 @@ __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, 
   int cnt = 0;
   for (int k = 0; k < c.rig.num_views; ++k) {
     if (!((bits >> k) & 1u)) continue;
-    const WarpOut w = warp_to(c.rig, k, u, v, d);
+    const WarpOut w = warp_ctx(c, k, u, v, d);
     if (!in_margin(c.rig, k, w)) continue;
     const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
     sample_desc(c.desc + (size_t)k * c.HW, c.W, t, [&](int ch, double f) {
@@ -168,12 +202,13 @@ __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
 
     double be = INFINITY, bd = INFINITY;
     bool br = false;
+    double lim = INFINITY;  // pruning radius of the current incumbent
     auto offer = [&](double d) {
       ++n_cand;
       // -log prior bounds the energy from below (var >= 0): exact pruning
-      // (solver.py:341-347).  Far candidates are rejected by a cheap fp32
-      // test; anything close gets the exact fp64 comparison.
-      if (surely_pruned(d, mu, c.inv_sigma_f, c.gamma_f, be)) return;
+      // (solver.py:341-347).  Candidates beyond the incumbent's radius are
+      // certainly pruned; the rest get the exact fp64 comparison.
+      if (fabs(d - mu) > lim) return;
       const double lp = log_prior(d, mu, c.p.sigma, c.p.gamma, c.inv_sigma);
       if (!(-lp <= be)) return;
       ++n_eval;
@@ -182,6 +217,7 @@ __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
         be = E.e;
         bd = d;
         br = E.real;
+        lim = prune_radius(be, c.sigma_f, c.gamma_f);
       }
     };
 
@@ -302,7 +338,10 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ 
   nf = warp_sum(nf);
   npf = warp_sum(npf);
   nch = warp_sum(nch);
-  if ((threadIdx.x & 31) == 0) {
+  // one partial per block, warps combined in fixed order
+  __shared__ Partial sp[STATS_BLOCK / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
     const int64_t w = i >> 5;
     Partial P = {};
     P.sum_e = se;
@@ -315,7 +354,21 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ 
       P.n_cand = work[w].n_cand;
       P.n_eval = work[w].n_eval;
     }
-    parts[w] = P;
+    sp[wid] = P;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Partial B = sp[0];
+    for (int j = 1; j < (int)(blockDim.x >> 5); ++j) {
+      B.sum_e += sp[j].sum_e;
+      B.sum_pe += sp[j].sum_pe;
+      B.n_fin += sp[j].n_fin;
+      B.n_pfin += sp[j].n_pfin;
+      B.n_changed += sp[j].n_changed;
+      B.n_cand += sp[j].n_cand;
+      B.n_eval += sp[j].n_eval;
+    }
+    parts[blockIdx.x] = B;
   }
 }
 
@@ -488,7 +541,7 @@ __device__ __forceinline__ uint32_t gather_pixel(const EmCtx& c, double u, doubl
                                                  double* f, int stride, double* q) {
   uint32_t vb = 0;
   for (int k = 0; k < c.rig.num_views; ++k) {
-    const WarpOut w = warp_to(c.rig, k, u, v, d);
+    const WarpOut w = warp_ctx(c, k, u, v, d);
     if (in_margin(c.rig, k, w)) {
       const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
       sample_desc(c.desc + (size_t)k * c.HW, c.W, t,
@@ -534,7 +587,7 @@ __global__ void k_initial_masks(EmCtx c, const int64_t* __restrict__ pix_list, i
   const double d = c.mu[pix];
   uint32_t sb = 0, vb = 0;
   for (int k = 0; k < c.rig.num_views; ++k) {
-    const WarpOut w = warp_to(c.rig, k, u, v, d);
+    const WarpOut w = warp_ctx(c, k, u, v, d);
     if (!in_margin(c.rig, k, w)) continue;
     const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
     const double q = sample_prior(c.priors + (size_t)k * c.HW, c.W, t);

@@ -6,6 +6,7 @@
 #include "st_common.cuh"
 
 #define EM_BLOCK 128
+#define STATS_BLOCK 256
 #define ESTEP_BLOCK 64
 #define ST_MAX_BAND 64
 
@@ -30,8 +31,9 @@ struct EmCtx {
   int sup_ir;
   double sup_r2;
   double inv_sigma;     // 1/sigma when sigma is a power of two (exact), else 0
-  float inv_sigma_f;    // fp32 1/sigma for the pruning pre-test
+  float sigma_f;        // fp32 sigma / gamma for the pruning radius
   float gamma_f;
+  int rectified;        // every view: A = I, b = (bx, 0, 0) -> 1-D horizontal warp
   double recip[ST_MAX_VIEWS + 1];  // RN(1/n), n = 1..12, for div_small
 };
 
