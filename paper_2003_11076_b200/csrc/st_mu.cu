@@ -24,6 +24,7 @@
 #include <float.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <cub/cub.cuh>
 
@@ -45,6 +46,9 @@ struct MuWs {
   unsigned *cnt, *tmin, *tmax;
   int32_t *res0, *res1, *final_s, *chunk_of, *len, *end0, *end1;
   uint8_t* chosen;
+  int32_t *chunks, *runs;  // worklists of chunk starts / run starts
+  unsigned* counts;        // [0] chunks, [1] runs
+  int chunk;  // chunk length for the speculative walks (MU_CHUNK, env ST_MU_CHUNK)
 };
 
 // scipy _barycentric_inside (ndim = 2), same operation order.
@@ -138,11 +142,42 @@ __device__ __forceinline__ double distplane(const TriDev& d, int s, double z0, d
   return dist;
 }
 
+// The current simplex's walk tables, kept in registers across consecutive
+// queries: along a run of edge pixels the walk almost always stays in (or
+// returns to) the same simplex, so most steps need no memory access.
+struct TriCache {
+  int s = -1;
+  double e0, e1, e2, e3;      // lifted facet equation
+  double t0, t1, t2, t3, t4, t5;  // barycentric transform
+  int n0, n1, n2;             // neighbours
+  __device__ __forceinline__ void ensure(const TriDev& d, int t) {
+    if (t == s) return;
+    s = t;
+    const double2* ep = reinterpret_cast<const double2*>(d.equations + 4 * t);
+    const double2 a = __ldg(ep), b = __ldg(ep + 1);
+    e0 = a.x; e1 = a.y; e2 = b.x; e3 = b.y;
+    const double2* tp = reinterpret_cast<const double2*>(d.transform + 6 * t);
+    const double2 x = __ldg(tp), y = __ldg(tp + 1), z = __ldg(tp + 2);
+    t0 = x.x; t1 = x.y; t2 = y.x; t3 = y.y; t4 = z.x; t5 = z.y;
+    n0 = __ldg(d.nb + 3 * t);
+    n1 = __ldg(d.nb + 3 * t + 1);
+    n2 = __ldg(d.nb + 3 * t + 2);
+  }
+  __device__ __forceinline__ int nb(int k) const { return k == 0 ? n0 : (k == 1 ? n1 : n2); }
+  __device__ __forceinline__ double dist(double z0, double z1, double z2) const {
+    double v = e3;
+    v = dadd(v, dmul(e0, z0));
+    v = dadd(v, dmul(e1, z1));
+    v = dadd(v, dmul(e2, z2));
+    return v;
+  }
+};
+
 // _find_simplex + _find_simplex_directed for one query; `start` in/out.
 // The brute-force fallback (lowest-index including simplex) is the claim
 // pass's tmin.
 __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0, double x1,
-                            int& start) {
+                            int& start, TriCache& tc) {
   const double eps = QH_EPS;
   if (x0 < d.lo0 - eps || x0 > d.hi0 + eps || x1 < d.lo1 - eps || x1 > d.hi1 + eps) return -1;
   if (d.n_tri <= 0) return -1;
@@ -153,15 +188,29 @@ __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0
   z2 = dadd(z2, d.psh);
   int s = start;
   if (s < 0 || s >= d.n_tri) s = 0;
-  double best = distplane(d, s, x0, x1, z2);
+  tc.ensure(d, s);
+  double best = tc.dist(x0, x1, z2);
   bool changed = true;
   while (changed) {
     if (best > 0.0) break;
     changed = false;
+    // the three neighbours' distances, fetched in parallel; used as long as
+    // s has not moved inside this sweep (scipy reads the neighbours of the
+    // CURRENT s at every k)
+    tc.ensure(d, s);
+    const int s0 = s;
+    double pre[3];
+#pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const int m = d.nb[3 * s + k];  // s may have moved within this loop (as in scipy)
+      const int m = tc.nb(k);
+      pre[k] = m >= 0 ? distplane(d, m, x0, x1, z2) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      tc.ensure(d, s);
+      const int m = tc.nb(k);
       if (m == -1) continue;
-      const double dd = distplane(d, m, x0, x1, z2);
+      const double dd = s == s0 ? pre[k] : distplane(d, m, x0, x1, z2);
       if (dd > dadd(best, dmul(eps, dadd(1.0, fabs(best))))) {
         s = m;
         best = dd;
@@ -176,18 +225,18 @@ __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0
       start = s;
       return s;
     }
-    const double* T = d.transform + 6 * s;
+    tc.ensure(d, s);
     int inside = 1;
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
     for (int k = 0; k < 3; ++k) {
       double ck;
       if (k == 0) {
-        c0 = dadd(c0, dmul(T[0], dsub(x0, T[4])));
-        c0 = dadd(c0, dmul(T[1], dsub(x1, T[5])));
+        c0 = dadd(c0, dmul(tc.t0, dsub(x0, tc.t4)));
+        c0 = dadd(c0, dmul(tc.t1, dsub(x1, tc.t5)));
         ck = c0;
       } else if (k == 1) {
-        c1 = dadd(c1, dmul(T[2], dsub(x0, T[4])));
-        c1 = dadd(c1, dmul(T[3], dsub(x1, T[5])));
+        c1 = dadd(c1, dmul(tc.t2, dsub(x0, tc.t4)));
+        c1 = dadd(c1, dmul(tc.t3, dsub(x1, tc.t5)));
         ck = c1;
       } else {
         c2 = 1.0;
@@ -196,7 +245,7 @@ __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0
         ck = c2;
       }
       if (ck < -eps) {
-        const int m = d.nb[3 * s + k];
+        const int m = tc.nb(k);
         if (m == -1) {
           start = s;  // outside the triangulation: bail out
           return -1;
@@ -233,12 +282,35 @@ __device__ __forceinline__ bool chunk_start(const MuWs& w, int64_t p) {
   if (!ambiguous(w, p)) return false;
   if (p == 0) return true;
   if (!ambiguous(w, p - 1)) return true;
-  return (p % MU_CHUNK) == 0 && w.cnt[p - 1] == 2u;
+  return (p % w.chunk) == 0 && w.cnt[p - 1] == 2u;
+}
+
+// Dense worklists of chunk starts and run starts (warp-aggregated appends;
+// list order is irrelevant: every entry owns disjoint pixels).
+__device__ __forceinline__ void append_lane(bool want, int32_t v, int32_t* list,
+                                            unsigned* count) {
+  const unsigned ballot = __ballot_sync(0xffffffffu, want);
+  if (!ballot) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+  unsigned base = 0;
+  if (lane == leader) base = atomicAdd(count, (unsigned)__popc(ballot));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (want) list[base + __popc(ballot & ((1u << lane) - 1))] = v;
+}
+
+__global__ void k_mu_lists(int64_t npx, MuWs w) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = p < npx;
+  const bool cs = in && chunk_start(w, p);
+  const bool rs = in && ambiguous(w, p) && (p == 0 || !ambiguous(w, p - 1));
+  append_lane(cs, (int32_t)p, w.chunks, w.counts);
+  append_lane(rs, (int32_t)p, w.runs, w.counts + 1);
 }
 
 __global__ void k_walk_chunks(TriDev d, int W, int64_t npx, MuWs w) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npx || !chunk_start(w, p)) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)w.counts[0]) return;
+  const int64_t p = w.chunks[t];
   int opts[2];
   int nopt;
   if (p == 0) {
@@ -254,10 +326,11 @@ __global__ void k_walk_chunks(TriDev d, int W, int64_t npx, MuWs w) {
   }
   int64_t q = p;
   int st0 = opts[0], st1 = nopt > 1 ? opts[1] : 0;
+  TriCache tc0, tc1;
   do {
     const double x0 = (double)(q % W), x1 = (double)(q / W);
-    w.res0[q] = find_simplex(d, w, q, x0, x1, st0);
-    if (nopt > 1) w.res1[q] = find_simplex(d, w, q, x0, x1, st1);
+    w.res0[q] = find_simplex(d, w, q, x0, x1, st0, tc0);
+    if (nopt > 1) w.res1[q] = find_simplex(d, w, q, x0, x1, st1, tc1);
     w.chunk_of[q] = (int32_t)p;
     ++q;
   } while (q < npx && ambiguous(w, q) && !chunk_start(w, q));
@@ -267,8 +340,9 @@ __global__ void k_walk_chunks(TriDev d, int W, int64_t npx, MuWs w) {
 }
 
 __global__ void k_resolve_runs(TriDev d, int W, int64_t npx, MuWs w) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npx || !ambiguous(w, p) || (p > 0 && ambiguous(w, p - 1))) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)w.counts[1]) return;
+  const int64_t p = w.runs[t];
   int64_t c = p;
   w.chosen[c] = 0;
   int carry = w.end0[c];
@@ -287,7 +361,9 @@ __global__ void k_resolve_runs(TriDev d, int W, int64_t npx, MuWs w) {
       int st = carry;
       int64_t q = nxt;
       const int64_t e = nxt + w.len[nxt];
-      for (; q < e; ++q) w.final_s[q] = find_simplex(d, w, q, (double)(q % W), (double)(q / W), st);
+      TriCache tc;
+      for (; q < e; ++q)
+        w.final_s[q] = find_simplex(d, w, q, (double)(q % W), (double)(q / W), st, tc);
       w.chosen[nxt] = 2;
       carry = st;
       c = nxt;
@@ -342,7 +418,7 @@ namespace {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct MuLayout {
-  size_t off[11];
+  size_t off[14];
   size_t bbox, area, start, cub, cub_bytes;
   size_t total;
 };
@@ -351,10 +427,10 @@ MuLayout mu_layout(int W, int H, int n_tri) {
   MuLayout L;
   const size_t npx = (size_t)W * H;
   size_t o = 0;
-  const size_t sz[11] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 1};
-  for (int i = 0; i < 11; ++i) {
+  const size_t sz[14] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 1, 4, 4, 0};
+  for (int i = 0; i < 14; ++i) {
     L.off[i] = o;
-    o += align_up(sz[i] * npx);
+    o += align_up(sz[i] ? sz[i] * npx : 256);  // the counts slot is fixed-size
   }
   const size_t nt = (size_t)(n_tri > 0 ? n_tri : 1) + 1;
   L.bbox = o;  o += align_up(sizeof(int4) * nt);
@@ -405,6 +481,15 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   w.end0 = (int32_t*)(ws + L.off[8]);
   w.end1 = (int32_t*)(ws + L.off[9]);
   w.chosen = (uint8_t*)(ws + L.off[10]);
+  w.chunks = (int32_t*)(ws + L.off[11]);
+  w.runs = (int32_t*)(ws + L.off[12]);
+  w.counts = (unsigned*)(ws + L.off[13]);
+  static const int chunk_env = [] {
+    const char* e = getenv("ST_MU_CHUNK");
+    const int v = e ? atoi(e) : 0;
+    return v >= 2 ? v : MU_CHUNK;
+  }();
+  w.chunk = chunk_env;
   st::TriDev d;
   d.pts = tri->points;
   d.disp = tri->disparities;
@@ -425,6 +510,7 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   ST_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned) * npx, s));
   ST_CUDA_CHECK(cudaMemsetAsync(w.tmin, 0xff, sizeof(unsigned) * npx, s));
   ST_CUDA_CHECK(cudaMemsetAsync(w.tmax, 0, sizeof(unsigned) * npx, s));
+  ST_CUDA_CHECK(cudaMemsetAsync(w.counts, 0, 2 * sizeof(unsigned), s));
   if (d.n_tri > 0) {
     int4* bbox = (int4*)(ws + L.bbox);
     auto* area = (unsigned long long*)(ws + L.area);
@@ -442,7 +528,10 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
     ST_LAUNCH_CHECK("k_claim");
   }
   const unsigned blocks = (unsigned)((npx + 255) / 256);
-  st::k_walk_chunks<<<blocks, 256, 0, s>>>(d, W, npx, w);
+  st::k_mu_lists<<<blocks, 256, 0, s>>>(npx, w);
+  ST_LAUNCH_CHECK("k_mu_lists");
+  // worklist grids are sized for the worst case; surplus threads exit at once
+  st::k_walk_chunks<<<(unsigned)((npx + 127) / 128), 128, 0, s>>>(d, W, npx, w);
   ST_LAUNCH_CHECK("k_walk_chunks");
   st::k_resolve_runs<<<blocks, 256, 0, s>>>(d, W, npx, w);
   ST_LAUNCH_CHECK("k_resolve_runs");

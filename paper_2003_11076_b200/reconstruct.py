@@ -64,6 +64,7 @@ class FramePipeline:
         self.frame.priors = self.priors.data_ptr()
         self.frame.desc = self.desc.data_ptr()
         self.frame.mu = self.mu.data_ptr()
+        self.side = t.cuda.Stream()
 
     # -- inputs ---------------------------------------------------------------------
 
@@ -87,24 +88,36 @@ class FramePipeline:
         """Descriptors, mu, support lists, EM, refocus + median for the loaded frame."""
         p = N.make_params(self.params, self.prior_params, forced_iters, timing)
         K, H, W = self.K, self.H, self.W
+        t = self.t
+        main = t.cuda.current_stream()
         marks = []
         mark = (lambda: marks.append(self._event())) if timing else (lambda: None)
         mark()
-        N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
-        mark()
+        # the surface raster runs on a side stream, overlapped with the
+        # descriptors and the support lists (its Qhull-walk emulation has a
+        # long single-thread chain at the image corner)
         need = int(N.lib().st_mu_raster_workspace(W, H, tri_dev.n_tri))
         if self.mu_ws.numel() < need:
-            self.mu_ws = empty((need,), self.t.uint8)
-        N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max), self.mu,
-                 self.mu_ws, self.mu_ws.numel())
+            self.mu_ws = empty((need,), t.uint8)
+        ready = t.cuda.Event()
+        ready.record(main)
+        with t.cuda.stream(self.side):
+            self.side.wait_event(ready)
+            mu_start = self._event() if timing else None
+            N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max), self.mu,
+                     self.mu_ws, self.mu_ws.numel())
+            mu_done = self._event(timing=timing)
+        N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
         mark()
         need = int(N.lib().st_support_workspace(tri_dev.n_sup, W, H,
                                                 float(self.prior_params.neighborhood_radius)))
         if self.sup_ws.numel() < need:
-            self.sup_ws = empty((need,), self.t.uint8)
+            self.sup_ws = empty((need,), t.uint8)
         rec = N.C.c_int64(0)
         N.invoke("st_support_build", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W, H, p,
                  self.frame, self.sup_ws, self.sup_ws.numel(), rec)
+        mark()
+        main.wait_event(mu_done)
         mark()
         stats = N.StStats()
         cb = N.REDUCE_FN(reduce) if reduce is not None else N.REDUCE_FN()
@@ -126,12 +139,13 @@ class FramePipeline:
         out = _stats_of(stats)
         if timing:
             marks[-1].synchronize()
-            names = ("descriptors", "mu_raster", "support_build", "solve", "synthesize")
+            names = ("descriptors", "support_build", "mu_wait", "solve", "synthesize")
             out.stage_ms = {n: marks[i].elapsed_time(marks[i + 1]) for i, n in enumerate(names)}
+            out.stage_ms["mu_raster_side_stream"] = mu_start.elapsed_time(mu_done)
         return out
 
-    def _event(self):
-        e = self.t.cuda.Event(enable_timing=True)
+    def _event(self, timing=True):
+        e = self.t.cuda.Event(enable_timing=timing)
         e.record(self.t.cuda.current_stream())
         return e
 
