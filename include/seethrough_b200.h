@@ -154,10 +154,12 @@ typedef struct {
   const float* priors;     /* (K,H,W)   */
   const uint8_t* desc;     /* (K,H,W,16) */
   const double* mu;        /* (H*W) clipped surface */
-  /* support tile lists built by st_support_build (SoA, sorted by tile then value) */
-  const uint32_t* sup_tile_start;  /* (n_tiles+1) */
-  const float* sup_value;          /* (n_records) fp32-rounded support disparity */
-  const uint32_t* sup_uv;          /* (n_records) u | v << 16 */
+  /* support candidate groups built by st_support_build: for every 32x8
+   * pixel tile, its distinct fp32 support disparities (ascending) with a
+   * 32x8 bit mask of the tile pixels whose radius holds such a point */
+  const uint32_t* sup_tile_start;  /* (n_tiles+1) first group of each tile */
+  const float* sup_value;          /* (n_groups) fp32-rounded support disparity */
+  const uint32_t* sup_mask;        /* (n_groups, 8) row bit masks */
 } st_frame;
 
 /* Build per-tile support candidate lists (solver.py:286-321 semantics).

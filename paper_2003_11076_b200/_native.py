@@ -44,7 +44,7 @@ class StStats(C.Structure):
 class StFrame(C.Structure):
     _fields_ = [("images", C.c_void_p), ("priors", C.c_void_p), ("desc", C.c_void_p),
                 ("mu", C.c_void_p), ("sup_tile_start", C.c_void_p),
-                ("sup_value", C.c_void_p), ("sup_uv", C.c_void_p)]
+                ("sup_value", C.c_void_p), ("sup_mask", C.c_void_p)]
 
 
 class StTri(C.Structure):

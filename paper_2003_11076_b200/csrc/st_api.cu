@@ -84,7 +84,7 @@ int make_ctx(const st_frame* f, const st_rig* rig, const st_params* p, st::EmCtx
   c.n_coarse = span > 0 ? (int)span : 0;
   c.sup_tile_start = f->sup_tile_start;
   c.sup_value = f->sup_value;
-  c.sup_uv = f->sup_uv;
+  c.sup_mask = f->sup_mask;
   c.tiles_x = (c.W + ST_TW - 1) / ST_TW;
   c.sup_ir = (int)floor(p->neighborhood_radius);
   c.sup_r2 = p->neighborhood_radius * p->neighborhood_radius;

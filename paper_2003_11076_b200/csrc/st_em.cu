@@ -95,6 +95,24 @@ __device__ __forceinline__ WarpOut warp_ctx(const EmCtx& c, int k, double u, dou
   return warp_to(c.rig, k, u, v, d);
 }
 
+// Tap selection for an in-margin ray.  On rectified rigs the clip and the
+// min(., n - 2) of sampling.py are no-ops inside the margin and v is an
+// integer row, so the taps reduce to floor(pu) and a zero vertical weight.
+__device__ __forceinline__ Taps taps_ctx(const EmCtx& c, const WarpOut& w) {
+  if (c.rectified) {
+    Taps t;
+    const double fl = floor(w.pu);
+    t.iu = (int)fl;
+    t.fu = dsub(w.pu, fl);
+    t.iv = (int)w.pv;
+    t.fv = 0.0;
+    t.su = 1;
+    t.sv = c.W;
+    return t;
+  }
+  return taps_of(w.pu, w.pv, c.W, c.H);
+}
+
 // ---------------------------------------------------------------------------
 // energy (solver.py:229-260)
 
@@ -116,7 +134,7 @@ __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, 
     if (!((bits >> k) & 1u)) continue;
     const WarpOut w = warp_ctx(c, k, u, v, d);
     if (!in_margin(c.rig, k, w)) continue;
-    const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
+    const Taps t = taps_ctx(c, w);
     sample_desc(c.desc + (size_t)k * c.HW, c.W, t, [&](int ch, double f) {
       s1[ch] = dadd(s1[ch], f);
       s2[ch] = dadd(s2[ch], dmul(f, f));
@@ -230,24 +248,13 @@ __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
     for (int j = 0; j < c.n_coarse; ++j) offer(dadd(1.0, dmul(4.0, (double)j)));
     // support disparities within the radius (solver.py:286-321, 373-400)
     if (c.sup_tile_start) {
+      // one bit test per distinct support value of the pixel's tile
       const int tile = (y / ST_TH) * c.tiles_x + (x / ST_TW);
-      const uint32_t r1 = c.sup_tile_start[tile + 1];
-      uint32_t r = c.sup_tile_start[tile];
-      const int ir = c.sup_ir;
-      while (r < r1) {
-        const float val = c.sup_value[r];
-        bool hit = false;
-        do {
-          if (!hit) {
-            const uint32_t uv = c.sup_uv[r];
-            const int dx = x - (int)(int16_t)(uv & 0xffffu);
-            const int dy = y - (int)(int16_t)(uv >> 16);
-            hit = abs(dx) <= ir && abs(dy) <= ir && (double)(dx * dx + dy * dy) <= c.sup_r2;
-          }
-          ++r;
-        } while (r < r1 && c.sup_value[r] == val);
-        if (hit) offer((double)val);
-      }
+      const uint32_t g1 = __ldg(c.sup_tile_start + tile + 1);
+      const int row = y % ST_TH, col = x % ST_TW;
+      for (uint32_t g = __ldg(c.sup_tile_start + tile); g < g1; ++g)
+        if ((__ldg(c.sup_mask + (size_t)g * ST_TH + row) >> col) & 1u)
+          offer((double)__ldg(c.sup_value + g));
     }
 
     uint8_t status = ST_STATUS_VALID;
@@ -543,7 +550,7 @@ __device__ __forceinline__ uint32_t gather_pixel(const EmCtx& c, double u, doubl
   for (int k = 0; k < c.rig.num_views; ++k) {
     const WarpOut w = warp_ctx(c, k, u, v, d);
     if (in_margin(c.rig, k, w)) {
-      const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
+      const Taps t = taps_ctx(c, w);
       sample_desc(c.desc + (size_t)k * c.HW, c.W, t,
                   [&](int ch, double x) { f[(k * 16 + ch) * stride] = x; });
       q[k] = sample_prior(c.priors + (size_t)k * c.HW, c.W, t);
@@ -589,7 +596,7 @@ __global__ void k_initial_masks(EmCtx c, const int64_t* __restrict__ pix_list, i
   for (int k = 0; k < c.rig.num_views; ++k) {
     const WarpOut w = warp_ctx(c, k, u, v, d);
     if (!in_margin(c.rig, k, w)) continue;
-    const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
+    const Taps t = taps_ctx(c, w);
     const double q = sample_prior(c.priors + (size_t)k * c.HW, c.W, t);
     vb |= 1u << k;
     if (q >= c.p.threshold) sb |= 1u << k;
@@ -611,7 +618,7 @@ __global__ void k_gather_rays(EmCtx c, const int64_t* __restrict__ pix, const do
     double* out = desc + ((size_t)i * K + k) * 16;
     const WarpOut w = warp_to(c.rig, k, u, v, d[i]);
     if (in_margin(c.rig, k, w)) {
-      const Taps t = taps_of(w.pu, w.pv, c.W, c.H);
+      const Taps t = taps_ctx(c, w);
       sample_desc(c.desc + (size_t)k * c.HW, c.W, t, [&](int ch, double x) { out[ch] = x; });
       q[(size_t)i * K + k] = sample_prior(c.priors + (size_t)k * c.HW, c.W, t);
       valid[(size_t)i * K + k] = 1;

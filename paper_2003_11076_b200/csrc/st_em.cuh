@@ -26,7 +26,7 @@ struct EmCtx {
   int n_coarse;
   const uint32_t* sup_tile_start;
   const float* sup_value;
-  const uint32_t* sup_uv;
+  const uint32_t* sup_mask;
   int tiles_x;
   int sup_ir;
   double sup_r2;

@@ -68,24 +68,70 @@ __global__ void k_sup_emit(const double* __restrict__ uv, const double* __restri
     }
 }
 
-__global__ void k_sup_finish(const unsigned long long* __restrict__ keys, int64_t n_rec,
-                             int n_tiles, uint32_t* __restrict__ tile_start,
-                             float* __restrict__ value) {
+// After the sort: records with equal (tile, value) form one group.  heads[i]
+// flags the first record of each group.
+__global__ void k_sup_heads(const unsigned long long* __restrict__ keys, int64_t n_rec,
+                            uint32_t* __restrict__ heads) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_rec) value[i] = __uint_as_float((uint32_t)(keys[i] & 0xffffffffull));
-  if (i <= n_tiles) {
-    // lower_bound of tile i in the sorted keys
-    int64_t lo = 0, hi = n_rec;
-    const unsigned long long want = (unsigned long long)i << 32;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (keys[mid] < want)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    tile_start[i] = (uint32_t)lo;
+  if (i < n_rec) heads[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+}
+
+// Each record ORs the pixels of its tile inside its disk (solver.py:290-308:
+// du^2 + dv^2 <= r^2, |du|, |dv| <= floor(r), in the image) into its group's
+// 32x8 coverage mask; group heads also publish the group's key and value.
+__global__ void k_sup_cover(const unsigned long long* __restrict__ keys,
+                            const uint32_t* __restrict__ vals, const uint32_t* __restrict__ gid_incl,
+                            int64_t n_rec, SupGeom g, double r2,
+                            unsigned long long* __restrict__ gkey, float* __restrict__ gvalue,
+                            uint32_t* __restrict__ gmask) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_rec) return;
+  const unsigned long long key = keys[i];
+  const uint32_t grp = gid_incl[i] - 1;
+  if (i == 0 || keys[i - 1] != key) {
+    gkey[grp] = key;
+    gvalue[grp] = __uint_as_float((uint32_t)(key & 0xffffffffull));
   }
+  const int tile = (int)(key >> 32);
+  const int tx = tile % g.tiles_x, ty = tile / g.tiles_x;
+  const uint32_t uv = vals[i];
+  const int pu = (int)(int16_t)(uv & 0xffffu), pv = (int)(int16_t)(uv >> 16);
+  for (int r = 0; r < ST_TH; ++r) {
+    const int y = ty * ST_TH + r;
+    if (y >= g.H) break;
+    const int dy = y - pv;
+    if (abs(dy) > g.ir) continue;
+    // largest |dx| with dx^2 + dy^2 <= r^2 (compared in double like numpy)
+    int dxm = (int)floor(sqrt(fmax(r2 - (double)(dy * dy), 0.0)));
+    while ((double)((dxm + 1) * (dxm + 1) + dy * dy) <= r2) ++dxm;
+    while (dxm >= 0 && (double)(dxm * dxm + dy * dy) > r2) --dxm;
+    if (dxm < 0) continue;
+    dxm = min(dxm, g.ir);
+    const int x0 = max(max(pu - dxm, tx * ST_TW), 0);
+    const int x1 = min(min(pu + dxm, tx * ST_TW + ST_TW - 1), g.W - 1);
+    if (x0 > x1) continue;
+    const int c0 = x0 - tx * ST_TW, nbits = x1 - x0 + 1;
+    const uint32_t bits = (nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u)) << c0;
+    atomicOr(gmask + (size_t)grp * ST_TH + r, bits);
+  }
+}
+
+__global__ void k_sup_group_start(const unsigned long long* __restrict__ gkey,
+                                  const uint32_t* __restrict__ n_groups_ptr, int n_tiles,
+                                  uint32_t* __restrict__ tile_start) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n_tiles) return;
+  // lower_bound of tile i in the sorted group keys
+  int64_t lo = 0, hi = n_groups_ptr ? (int64_t)*n_groups_ptr : 0;
+  const unsigned long long want = (unsigned long long)i << 32;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (gkey[mid] < want)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  tile_start[i] = (uint32_t)lo;
 }
 
 }  // namespace st
@@ -98,7 +144,8 @@ namespace {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct SupLayout {
-  size_t counts, offs, keys_in, keys_out, vals_in, vals_out, tile_start, value, cub, total;
+  size_t counts, offs, keys_in, keys_out, vals_in, vals_out, heads, gid, gkey, gvalue, gmask,
+      tile_start, cub, total;
   size_t cub_bytes;
   int64_t max_rec;
   int tiles_x, tiles_y;
@@ -116,22 +163,29 @@ SupLayout sup_layout(int n, int W, int H, double radius) {
   L.tiles_y = (H + ST_TH - 1) / ST_TH;
   const int n_tiles = L.tiles_x * L.tiles_y;
   L.max_rec = (int64_t)n * tiles_per_point_max(ir < 0 ? 0 : ir);
-  size_t scan_bytes = 0, sort_bytes = 0;
+  size_t scan_bytes = 0, sort_bytes = 0, incl_bytes = 0;
+  const int mr = (int)(L.max_rec > 0 ? L.max_rec : 1);
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                 n + 1);
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (unsigned long long*)nullptr,
                                   (unsigned long long*)nullptr, (uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, (int)(L.max_rec > 0 ? L.max_rec : 1));
-  L.cub_bytes = scan_bytes > sort_bytes ? scan_bytes : sort_bytes;
+                                  (uint32_t*)nullptr, mr);
+  cub::DeviceScan::InclusiveSum(nullptr, incl_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, mr);
+  L.cub_bytes = std::max(scan_bytes, std::max(sort_bytes, incl_bytes));
+  const size_t R = (size_t)L.max_rec + 1;
   size_t o = 0;
   L.counts = o;     o += align_up(sizeof(uint32_t) * (n + 1));
   L.offs = o;       o += align_up(sizeof(uint32_t) * (n + 1));
-  L.keys_in = o;    o += align_up(sizeof(unsigned long long) * (L.max_rec + 1));
-  L.keys_out = o;   o += align_up(sizeof(unsigned long long) * (L.max_rec + 1));
-  L.vals_in = o;    o += align_up(sizeof(uint32_t) * (L.max_rec + 1));
-  L.vals_out = o;   o += align_up(sizeof(uint32_t) * (L.max_rec + 1));
+  L.keys_in = o;    o += align_up(sizeof(unsigned long long) * R);
+  L.keys_out = o;   o += align_up(sizeof(unsigned long long) * R);
+  L.vals_in = o;    o += align_up(sizeof(uint32_t) * R);
+  L.vals_out = o;   o += align_up(sizeof(uint32_t) * R);
+  L.heads = o;      o += align_up(sizeof(uint32_t) * R);
+  L.gid = o;        o += align_up(sizeof(uint32_t) * R);
+  L.gkey = o;       o += align_up(sizeof(unsigned long long) * R);
+  L.gvalue = o;     o += align_up(sizeof(float) * R);
+  L.gmask = o;      o += align_up(sizeof(uint32_t) * ST_TH * R);
   L.tile_start = o; o += align_up(sizeof(uint32_t) * (n_tiles + 1));
-  L.value = o;      o += align_up(sizeof(float) * (L.max_rec + 1));
   L.cub = o;        o += align_up(L.cub_bytes);
   L.total = o;
   return L;
@@ -162,7 +216,11 @@ extern "C" int st_support_build(const double* support_uv, const double* support_
   uint32_t* vals_in = (uint32_t*)(ws + L.vals_in);
   uint32_t* vals_out = (uint32_t*)(ws + L.vals_out);
   uint32_t* tile_start = (uint32_t*)(ws + L.tile_start);
-  float* value = (float*)(ws + L.value);
+  uint32_t* heads = (uint32_t*)(ws + L.heads);
+  uint32_t* gid = (uint32_t*)(ws + L.gid);
+  auto* gkey = (unsigned long long*)(ws + L.gkey);
+  float* gvalue = (float*)(ws + L.gvalue);
+  uint32_t* gmask = (uint32_t*)(ws + L.gmask);
   void* cub_tmp = ws + L.cub;
   const int n_tiles = L.tiles_x * L.tiles_y;
 
@@ -196,15 +254,26 @@ extern "C" int st_support_build(const double* support_uv, const double* support_
       ST_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, keys_in, keys_out, vals_in,
                                                     vals_out, (int)total, 0, 32 + tile_bits, s));
       sthost::count_launch();
+      // (tile, value) groups and their 32x8 pixel coverage masks
+      const unsigned rb = (unsigned)((total + 255) / 256);
+      st::k_sup_heads<<<rb, 256, 0, s>>>(keys_out, total, heads);
+      ST_LAUNCH_CHECK("k_sup_heads");
+      tb = L.cub_bytes;
+      ST_CUDA_CHECK(cub::DeviceScan::InclusiveSum(cub_tmp, tb, heads, gid, (int)total, s));
+      sthost::count_launch();
+      ST_CUDA_CHECK(cudaMemsetAsync(gmask, 0, sizeof(uint32_t) * ST_TH * (size_t)total, s));
+      const double r = p->neighborhood_radius;
+      st::k_sup_cover<<<rb, 256, 0, s>>>(keys_out, vals_out, gid, total, g, r * r, gkey, gvalue,
+                                         gmask);
+      ST_LAUNCH_CHECK("k_sup_cover");
     }
   }
-  const int64_t m = total > n_tiles + 1 ? total : n_tiles + 1;
-  st::k_sup_finish<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(keys_out, total, n_tiles,
-                                                                tile_start, value);
-  ST_LAUNCH_CHECK("k_sup_finish");
+  st::k_sup_group_start<<<(unsigned)((n_tiles + 1 + 255) / 256), 256, 0, s>>>(
+      gkey, total > 0 ? gid + total - 1 : nullptr, n_tiles, tile_start);
+  ST_LAUNCH_CHECK("k_sup_group_start");
   frame->sup_tile_start = tile_start;
-  frame->sup_value = value;
-  frame->sup_uv = vals_out;
+  frame->sup_value = gvalue;
+  frame->sup_mask = gmask;
   if (n_records) *n_records = total;
   return ST_OK;
 }
