@@ -138,12 +138,25 @@ int prepare_estep_kernels() {
   static bool done = false;
   if (done) return ST_OK;
   const int max_smem = estep_smem(ST_MAX_VIEWS);
-  ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_at, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     max_smem));
+  ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_at<0>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_rays,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   done = true;
   return ST_OK;
+}
+
+// E-step launch with the view count as a template parameter where it is small.
+void launch_e_step(int K, unsigned blocks, cudaStream_t s, const st::EmCtx& c,
+                   const st::EStepArgs& a) {
+  const int smem = estep_smem(K);
+  switch (K) {
+    case 2: st::k_e_step_at<2><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
+    case 3: st::k_e_step_at<3><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
+    case 4: st::k_e_step_at<4><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
+    case 5: st::k_e_step_at<5><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
+    default: st::k_e_step_at<0><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
+  }
 }
 
 }  // namespace
@@ -356,8 +369,7 @@ int st_e_step_at(const st_frame* f, const st_rig* rig, const st_params* p, const
   a.static_out = static_out;
   a.valid_out = valid_out;
   a.scatter = 0;
-  st::k_e_step_at<<<blocks_for(n, ESTEP_BLOCK), ESTEP_BLOCK, estep_smem(rig->num_views),
-                    (cudaStream_t)stream>>>(c, a);
+  launch_e_step(rig->num_views, blocks_for(n, ESTEP_BLOCK), (cudaStream_t)stream, c, a);
   ST_LAUNCH_CHECK("k_e_step_at");
   return ST_OK;
 }
@@ -558,8 +570,7 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       e.static_out = static_bits;
       e.valid_out = valid_bits;
       e.scatter = 1;
-      st::k_e_step_at<<<blocks_for(n_act, ESTEP_BLOCK), ESTEP_BLOCK, estep_smem(rig->num_views),
-                        s>>>(c, e);
+      launch_e_step(rig->num_views, blocks_for(n_act, ESTEP_BLOCK), s, c, e);
       ST_LAUNCH_CHECK("k_e_step_at");
       ev.record(2, s);
       const int sblk = (int)blocks_for(n_act, STATS_BLOCK);

@@ -389,6 +389,7 @@ struct RayPriors {
   double l0[ST_MAX_VIEWS];
 };
 
+// log of the clamped Bernoulli factors (solver.py:137-140).
 __device__ __forceinline__ void clamp_logs(double q, double eps, double& l1, double& l0) {
   const double qc = fmin(fmax(q, eps), dsub(1.0, eps));  // np.clip(q, eps, 1 - eps)
   l1 = log(qc);
@@ -420,6 +421,41 @@ __device__ __forceinline__ double div_n(double x, int n) {
   }
 }
 
+__host__ __device__ constexpr int popc_c(int x) { return x ? (x & 1) + popc_c(x >> 1) : 0; }
+
+template <int N>
+__device__ __forceinline__ double div_c(double x) {
+  if constexpr (N == 1) return x;
+  else if constexpr ((N & (N - 1)) == 0) return dmul(x, 1.0 / N);  // exact scaling
+  else return div_small(x, (double)N, 1.0 / N);                      // RN(1/N) folded at compile time
+}
+
+// All non-empty view masks in depth-first order: mask C = M | (1 << KB) takes
+// its per-channel sums from its prefix M plus view KB, which is exactly the
+// reference's in-order accumulation over the selected views (BLAS dgemm with
+// a 0/1 operand, solver.py:148-149).  Masks with one view have variance 0 and
+// are deficient under min_static_rays >= 2, so they are not accumulated.
+template <int K, int M, int KB>
+__device__ __forceinline__ void mask_dfs(const double (&fk)[K], const double (&sq)[K], double a1,
+                                         double a2, double (&var)[1 << K]) {
+  if constexpr (KB < K) {
+    constexpr int C = M | (1 << KB);
+    constexpr int POP = popc_c(C);
+    double b1, b2;
+    if constexpr (M == 0) {
+      b1 = fk[KB];
+      b2 = sq[KB];
+    } else {
+      b1 = dadd(a1, fk[KB]);
+      b2 = dadd(a2, sq[KB]);
+    }
+    // (s2 - s1*s1/n), summed over channels in order (axis-1 reduce)
+    if constexpr (POP >= 2) var[C] = dadd(var[C], dsub(b2, div_c<POP>(dmul(b1, b1))));
+    mask_dfs<K, C, KB + 1>(fk, sq, b1, b2, var);  // supersets of C
+    mask_dfs<K, M, KB + 1>(fk, sq, a1, a2, var);  // M with a later view instead
+  }
+}
+
 // Register path for K <= 5 (<= 32 masks, fully unrolled).
 template <int K>
 __device__ __forceinline__ uint32_t estep_small(const double* __restrict__ f, int stride,
@@ -436,20 +472,7 @@ __device__ __forceinline__ uint32_t estep_small(const double* __restrict__ f, in
       fk[k] = f[(k * 16 + ch) * stride];
       sq[k] = dmul(fk[k], fk[k]);
     }
-#pragma unroll
-    for (int m = 1; m < M; ++m) {
-      double a1 = 0.0, a2 = 0.0;
-      int n = 0;
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-        if ((m >> k) & 1) {
-          a1 = n ? dadd(a1, fk[k]) : fk[k];
-          a2 = n ? dadd(a2, sq[k]) : sq[k];
-          ++n;
-        }
-      // (s2 - s1*s1/n), summed over channels in order (axis-1 reduce)
-      var[m] = dadd(var[m], dsub(a2, div_n(dmul(a1, a1), n)));
-    }
+    mask_dfs<K, 0, 0>(fk, sq, 0.0, 0.0, var);
   }
   double best = -INFINITY;
   int bpop = -1;
@@ -564,6 +587,9 @@ __device__ __forceinline__ uint32_t gather_pixel(const EmCtx& c, double u, doubl
   return vb;
 }
 
+// KT > 0: the view count is a compile-time constant, so the per-view arrays
+// below stay in registers; KT == 0 handles any K (<= 12) at run time.
+template <int KT>
 __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a) {
   extern __shared__ double sh_f[];
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -573,15 +599,50 @@ __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a)
   if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) return;  // solver.py:476-478
   const int64_t pix = a.pix ? a.pix[i] : i;
   const double u = (double)(pix % c.W), v = (double)(pix / c.W);
+  const double d = a.d[i];
   double* f = sh_f + threadIdx.x;
-  double q[ST_MAX_VIEWS], l1[ST_MAX_VIEWS], l0[ST_MAX_VIEWS];
-  const uint32_t vb = gather_pixel(c, u, v, a.d[i], f, blockDim.x, q);
-  for (int k = 0; k < c.rig.num_views; ++k) clamp_logs(q[k], c.p.epsilon_prior, l1[k], l0[k]);
-  const uint32_t m = estep_dispatch(c.rig.num_views, f, blockDim.x, l1, l0, vb, c.p);
+  const int stride = blockDim.x;
+  constexpr int KA = KT > 0 ? KT : ST_MAX_VIEWS;
+  const int K = KT > 0 ? KT : c.rig.num_views;
+  double q[KA], l1[KA], l0[KA];
+  uint32_t vb = 0;
+  // gather_rays (solver.py:206-227): invalid rays carry desc 0 and q 0.5
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {
+    if (KT == 0 && k >= K) break;
+    const WarpOut w = warp_ctx(c, k, u, v, d);
+    if (in_margin(c.rig, k, w)) {
+      const Taps tp = taps_ctx(c, w);
+      sample_desc(c.desc + (size_t)k * c.HW, c.W, tp,
+                  [&](int ch, double x) { f[(k * 16 + ch) * stride] = x; });
+      q[k] = sample_prior(c.priors + (size_t)k * c.HW, c.W, tp);
+      vb |= 1u << k;
+    } else {
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) f[(k * 16 + ch) * stride] = 0.0;
+      q[k] = 0.5;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {
+    if (KT == 0 && k >= K) break;
+    clamp_logs(q[k], c.p.epsilon_prior, l1[k], l0[k]);
+  }
+  uint32_t m;
+  if constexpr (KT > 0)
+    m = estep_small<KT>(f, stride, l1, l0, vb, c.p);
+  else
+    m = estep_generic(K, f, stride, l1, l0, vb, c.p);
   const int64_t o = a.scatter ? pix : i;
   a.static_out[o] = m;
   a.valid_out[o] = vb;
 }
+
+template __global__ void k_e_step_at<0>(EmCtx, EStepArgs);
+template __global__ void k_e_step_at<2>(EmCtx, EStepArgs);
+template __global__ void k_e_step_at<3>(EmCtx, EStepArgs);
+template __global__ void k_e_step_at<4>(EmCtx, EStepArgs);
+template __global__ void k_e_step_at<5>(EmCtx, EStepArgs);
 
 // initial_masks (solver.py:421-432): valid & q >= threshold at mu.
 __global__ void k_initial_masks(EmCtx c, const int64_t* __restrict__ pix_list, int64_t n,

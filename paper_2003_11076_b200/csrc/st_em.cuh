@@ -81,6 +81,7 @@ __global__ void k_flag_mstep(const int64_t* active, int64_t n, const uint32_t* s
 __global__ void k_em_stats(int64_t n, int with_prev, const double* e, const double* pe,
                            const uint8_t* chg, const Partial* work, int n_work_parts,
                            Partial* parts);
+template <int KT>
 __global__ void k_e_step_at(EmCtx c, EStepArgs a);
 __global__ void k_initial_masks(EmCtx c, const int64_t* pix, int64_t n, uint32_t* static_out,
                                 uint32_t* valid_out);

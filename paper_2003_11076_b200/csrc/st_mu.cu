@@ -24,6 +24,7 @@
 #include <float.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <cub/cub.cuh>
@@ -32,7 +33,7 @@
 
 namespace st {
 
-#define MU_CHUNK 32
+#define MU_CHUNK 8
 #define QH_EPS (100.0 * DBL_EPSILON)
 
 struct TriDev {
@@ -46,10 +47,26 @@ struct MuWs {
   unsigned *cnt, *tmin, *tmax;
   int32_t *res0, *res1, *final_s, *chunk_of, *len, *end0, *end1;
   uint8_t* chosen;
+  unsigned long long *vmin, *vmax;  // range of the claimers' plane values (order keys)
   int32_t *chunks, *runs;  // worklists of chunk starts / run starts
   unsigned* counts;        // [0] chunks, [1] runs
   int chunk;  // chunk length for the speculative walks (MU_CHUNK, env ST_MU_CHUNK)
 };
+
+// prior.py:296: pl[:, 0] * u + pl[:, 1] * v + pl[:, 2], left to right.
+__device__ __forceinline__ double plane_at(const TriDev& d, int t, double u, double v) {
+  const double* pl = d.planes + 3 * t;
+  return dadd(dadd(dmul(pl[0], u), dmul(pl[1], v)), pl[2]);
+}
+
+// Doubles as unsigned keys with the same order (for atomicMin/atomicMax).
+__device__ __forceinline__ unsigned long long order_key(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_value(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
 
 // scipy _barycentric_inside (ndim = 2), same operation order.
 __device__ __forceinline__ bool bary_inside(const double* __restrict__ T, double x0, double x1) {
@@ -126,6 +143,10 @@ __global__ void k_claim(TriDev d, int W, const int4* __restrict__ bbox,
         atomicAdd(w.cnt + p, 1u);
         atomicMin(w.tmin + p, (unsigned)t);
         atomicMax(w.tmax + p, (unsigned)t);
+        // range of the claimers' plane values at this pixel (order-preserving keys)
+        const unsigned long long key = order_key(plane_at(d, t, (double)x, (double)y));
+        atomicMin(w.vmin + p, key);
+        atomicMax(w.vmax + p, key);
       }
     }
   }
@@ -220,6 +241,10 @@ __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0
   }
   start = s;
   const int cycles = 1 + d.n_tri / 4;
+  // Brent cycle detection: the directed step depends on s alone, so a
+  // revisited simplex means the walk loops until the cap above and then
+  // takes the brute-force answer -- which we can return at once.
+  int saved = s, power = 1, lam = 0;
   for (int cyc = 0; cyc < cycles; ++cyc) {
     if (s == -1) {
       start = s;
@@ -259,7 +284,15 @@ __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0
         inside = 0;  // outside or nan (degenerate)
       }
     }
-    if (inside == -1) continue;
+    if (inside == -1) {
+      if (s == saved) break;  // cycle: same result as exhausting the cap
+      if (++lam == power) {
+        saved = s;
+        power <<= 1;
+        lam = 0;
+      }
+      continue;
+    }
     if (inside == 1) {
       start = s;
       return s;
@@ -324,6 +357,25 @@ __global__ void k_walk_chunks(TriDev d, int W, int64_t npx, MuWs w) {
     opts[1] = (int)w.tmax[p - 1];
     nopt = 2;
   }
+  // A chunk whose pixels get bit-identical plane values from every claiming
+  // simplex, and that ends its run (so no later walk starts from its end
+  // state), cannot influence mu: skip the walk.  This is the common case
+  // (including the image-corner vertices, whose walks start a full row away).
+  {
+    int64_t q = p;
+    bool agnostic = true;
+    do {
+      agnostic = agnostic && w.cnt[q] > 0 && w.vmin[q] == w.vmax[q];
+      w.chunk_of[q] = (int32_t)p;
+      ++q;
+    } while (q < npx && ambiguous(w, q) && !chunk_start(w, q));
+    const bool ends_run = q >= npx || !ambiguous(w, q);
+    if (agnostic && ends_run) {
+      w.len[p] = (int32_t)(q - p);
+      w.end0[p] = w.end1[p] = -1;  // never read: the run ends here
+      return;
+    }
+  }
   int64_t q = p;
   int st0 = opts[0], st1 = nopt > 1 ? opts[1] : 0;
   TriCache tc0, tc1;
@@ -380,8 +432,12 @@ __global__ void k_mu_eval(TriDev d, int W, int64_t npx, MuWs w, double clip_dmax
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npx) return;
   int s;
+  bool agnostic = false;
   if (!ambiguous(w, p)) {
     s = (int)w.tmin[p];
+  } else if (w.cnt[p] > 0 && w.vmin[p] == w.vmax[p]) {
+    s = 0;
+    agnostic = true;  // every claimer yields the same value: no walk needed
   } else {
     const int64_t c = w.chunk_of[p];
     const uint8_t ch = w.chosen[c];
@@ -389,6 +445,12 @@ __global__ void k_mu_eval(TriDev d, int W, int64_t npx, MuWs w, double clip_dmax
   }
   const double u = (double)(p % W), v = (double)(p / W);
   double m;
+  if (agnostic) {
+    m = key_value(w.vmin[p]);
+    if (clip_dmax > 0.0) m = fmin(fmax(m, 1e-6), clip_dmax);
+    mu[p] = m;
+    return;
+  }
   if (s >= 0) {
     // prior.py:296: pl[:, 0] * u + pl[:, 1] * v + pl[:, 2]
     const double* pl = d.planes + 3 * s;
@@ -418,7 +480,7 @@ namespace {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct MuLayout {
-  size_t off[14];
+  size_t off[16];
   size_t bbox, area, start, cub, cub_bytes;
   size_t total;
 };
@@ -427,8 +489,8 @@ MuLayout mu_layout(int W, int H, int n_tri) {
   MuLayout L;
   const size_t npx = (size_t)W * H;
   size_t o = 0;
-  const size_t sz[14] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 1, 4, 4, 0};
-  for (int i = 0; i < 14; ++i) {
+  const size_t sz[16] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 1, 4, 4, 0, 8, 8};
+  for (int i = 0; i < 16; ++i) {
     L.off[i] = o;
     o += align_up(sz[i] ? sz[i] * npx : 256);  // the counts slot is fixed-size
   }
@@ -484,6 +546,8 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   w.chunks = (int32_t*)(ws + L.off[11]);
   w.runs = (int32_t*)(ws + L.off[12]);
   w.counts = (unsigned*)(ws + L.off[13]);
+  w.vmin = (unsigned long long*)(ws + L.off[14]);
+  w.vmax = (unsigned long long*)(ws + L.off[15]);
   static const int chunk_env = [] {
     const char* e = getenv("ST_MU_CHUNK");
     const int v = e ? atoi(e) : 0;
@@ -507,14 +571,27 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   d.hi0 = tri->max_bound[0];
   d.hi1 = tri->max_bound[1];
   const int64_t npx = (int64_t)W * H;
+  static const bool prof_on = getenv("ST_MU_PROFILE") != nullptr;  // diagnostics
+  cudaEvent_t pev[8];
+  int npev = 0;
+  auto prof = [&]() {
+    if (prof_on && npev < 8) {
+      cudaEventCreate(&pev[npev]);
+      cudaEventRecord(pev[npev++], s);
+    }
+  };
+  prof();
   ST_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned) * npx, s));
   ST_CUDA_CHECK(cudaMemsetAsync(w.tmin, 0xff, sizeof(unsigned) * npx, s));
   ST_CUDA_CHECK(cudaMemsetAsync(w.tmax, 0, sizeof(unsigned) * npx, s));
-  ST_CUDA_CHECK(cudaMemsetAsync(w.counts, 0, 2 * sizeof(unsigned), s));
+  ST_CUDA_CHECK(cudaMemsetAsync(w.counts, 0, 8 * sizeof(unsigned), s));
+  ST_CUDA_CHECK(cudaMemsetAsync(w.vmin, 0xff, sizeof(unsigned long long) * npx, s));
+  ST_CUDA_CHECK(cudaMemsetAsync(w.vmax, 0, sizeof(unsigned long long) * npx, s));
   if (d.n_tri > 0) {
     int4* bbox = (int4*)(ws + L.bbox);
     auto* area = (unsigned long long*)(ws + L.area);
     auto* start = (unsigned long long*)(ws + L.start);
+    prof();
     ST_CUDA_CHECK(cudaMemsetAsync(area + d.n_tri, 0, sizeof(unsigned long long), s));
     st::k_tri_bbox<<<(d.n_tri + 127) / 128, 128, 0, s>>>(d, W, H, bbox, area);
     ST_LAUNCH_CHECK("k_tri_bbox");
@@ -528,14 +605,30 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
     ST_LAUNCH_CHECK("k_claim");
   }
   const unsigned blocks = (unsigned)((npx + 255) / 256);
+  prof();
   st::k_mu_lists<<<blocks, 256, 0, s>>>(npx, w);
   ST_LAUNCH_CHECK("k_mu_lists");
+  prof();
   // worklist grids are sized for the worst case; surplus threads exit at once
   st::k_walk_chunks<<<(unsigned)((npx + 127) / 128), 128, 0, s>>>(d, W, npx, w);
   ST_LAUNCH_CHECK("k_walk_chunks");
+  prof();
   st::k_resolve_runs<<<blocks, 256, 0, s>>>(d, W, npx, w);
   ST_LAUNCH_CHECK("k_resolve_runs");
+  prof();
   st::k_mu_eval<<<blocks, 256, 0, s>>>(d, W, npx, w, clip_dmax, mu_out);
   ST_LAUNCH_CHECK("k_mu_eval");
+  prof();
+  if (prof_on && npev > 1) {
+    cudaEventSynchronize(pev[npev - 1]);
+    fprintf(stderr, "mu_raster stages (ms): memset/bbox/claim/lists/walk/resolve/eval:");
+    for (int i = 1; i < npev; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pev[i - 1], pev[i]);
+      fprintf(stderr, " %.4f", ms);
+    }
+    fprintf(stderr, "\n");
+    for (int i = 0; i < npev; ++i) cudaEventDestroy(pev[i]);
+  }
   return ST_OK;
 }
