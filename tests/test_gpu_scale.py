@@ -1,0 +1,89 @@
+"""Parity at BASELINE.json's sizes.
+
+C1 (640x480, K=5, d_max 32): the GPU path against the CPU oracle on the
+same reference-identical inputs (renderer port checked against recorded
+digests; support recorded from the reference's harvest), whole frame.
+C2 (1280x720, d_max 64): size-independent properties -- determinism, the
+reference's dynamic_only == full-solve-on-active-pixels identity, banded ==
+full, forced iterations extend the reference iterations.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def st():
+    import paper_2003_11076_b200 as pkg
+    pkg.device.require_cuda()
+    return pkg
+
+
+def _inputs(cfg):
+    import bench
+    frame, rig, tri, exact = bench.load_inputs(cfg)
+    assert exact, "renderer port no longer reproduces the reference frame"
+    sp, pp = bench.params_for(cfg)
+    return frame, rig, tri, sp, pp
+
+
+@pytest.mark.slow
+def test_c1_full_frame_matches_oracle(st):
+    import oracle
+    frame, rig, tri, sp, pp = _inputs("C1")
+    r = st.reconstruct(frame, rig, tri, sp, pp)
+    k = len(rig)
+    a = np.stack([rig.warp_coefficients(i)[0] for i in range(k)])
+    b = np.stack([rig.warp_coefficients(i)[1] for i in range(k)])
+    sup_uv, sup_d = tri.support_points()
+    mu = oracle.mu_raster(tri.points, tri.disparities, tri.triangles, tri.planes, 640, 480)
+    p = oracle.OracleParams(d_max=pp.d_max, max_iters=sp.max_iters)
+    o = oracle.OracleSolver(frame.images, frame.priors, a, b, rig.ref_index, mu, sup_uv, sup_d,
+                            params=p)
+    want = o.solve()
+    img, prov, nr = oracle.synthesize(frame.images, a, b, rig.ref_index, want["values"],
+                                      want["status"], want["static_bits"])
+    assert r.stats.iterations_run == want["stats"]["iterations_run"]
+    assert r.stats.converged_after == want["stats"]["converged_after"]
+    agree = (r.disparity.values == want["values"]).mean()
+    assert agree >= 0.999, agree
+    assert (r.disparity.status == want["status"]).mean() >= 0.999
+    assert (r.segmentation.static_bits == want["static_bits"]).mean() >= 0.999
+    assert (r.segmentation.valid_bits == want["valid_bits"]).mean() >= 0.999
+    assert (r.image == img).all(axis=2).mean() >= 0.999
+    assert (r.provenance == prov).mean() >= 0.999
+    assert np.allclose(r.stats.mean_energy, want["stats"]["mean_energy"], rtol=1e-9)
+    # report exact agreement for the record
+    print(f"C1 parity: values {agree:.6f}, image {(r.image == img).all(axis=2).mean():.6f}")
+
+
+def test_c2_properties(st):
+    frame, rig, tri, sp, pp = _inputs("C2")
+    a = st.reconstruct(frame, rig, tri, sp, pp)
+    b = st.reconstruct(frame, rig, tri, sp, pp)
+    # byte-identical artefacts run to run (test_acceptance.py:310-332)
+    for x, y in ((a.disparity.values, b.disparity.values), (a.image, b.image),
+                 (a.segmentation.static_bits, b.segmentation.static_bits)):
+        assert np.array_equal(x, y)
+    assert a.stats.mean_energy == b.stats.mean_energy
+    # dynamic_only solves exactly the full solve's values on the active
+    # pixels (test_solver.py:323-337)
+    dyn = st.reconstruct(frame, rig, tri, sp, pp, dynamic_only=True)
+    active = frame.priors[rig.ref_index] < np.float32(sp.threshold)
+    assert active.any()
+    assert np.array_equal(dyn.disparity.values[active], a.disparity.values[active])
+    assert np.array_equal(dyn.segmentation.static_bits[active],
+                          a.segmentation.static_bits[active])
+    assert (dyn.provenance[~active] == st.PROV_COPIED).all()
+    # static rays are a subset of valid rays
+    assert not (a.segmentation.static_bits & ~a.segmentation.valid_bits).any()
+    # forcing more iterations keeps the reference iterations' statistics
+    f = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=5)
+    assert f.stats.iterations_run == 5
+    assert np.allclose(f.stats.mean_energy[:a.stats.iterations_run], a.stats.mean_energy,
+                       rtol=1e-12)
+    # energy descent (test_solver.py:305-320)
+    for i, prev in enumerate(f.stats.prev_energy):
+        assert f.stats.mean_energy[i + 1] <= prev + 1e-9
