@@ -48,29 +48,75 @@ def delaunay_of(tri):
     return dl
 
 
+class _Staging:
+    """Two reusable page-locked staging buffers for the triangulation tables."""
+
+    def __init__(self):
+        self.bufs = [None, None]
+        self.events = [None, None]
+        self.turn = 0
+
+    def take(self, nbytes):
+        import torch
+        i = self.turn
+        self.turn ^= 1
+        if self.events[i] is not None:
+            self.events[i].synchronize()  # its previous upload has left
+        if self.bufs[i] is None or self.bufs[i].numel() < nbytes:
+            self.bufs[i] = torch.empty(max(nbytes, 1 << 20) * 5 // 4, dtype=torch.uint8,
+                                       pin_memory=True)
+        return i, self.bufs[i]
+
+    def mark(self, i):
+        import torch
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.events[i] = ev
+
+
+_STAGING = _Staging()
+
+
 class TriDevice:
     """A TriangulationPrior on the device: vertices, planes, the Qhull walk
-    tables `st_mu_raster` replays, and the support list."""
+    tables `st_mu_raster` replays, and the support list -- packed into one
+    pinned staging buffer and sent with a single asynchronous copy."""
 
     def __init__(self, tri):
-        from .device import upload
+        import torch
+        from .device import dev
         dl = delaunay_of(tri)
-        f64 = lambda a, *s: upload(np.ascontiguousarray(a, dtype=np.float64).reshape(*s))  # noqa
-        pts = np.asarray(tri.points, dtype=np.float64).reshape(-1, 2)
-        self.n_pts = pts.shape[0]
-        self.points = f64(pts, -1, 2)
-        self.disparities = f64(tri.disparities, -1)
-        self.triangles = upload(np.ascontiguousarray(tri.triangles, dtype=np.int32).reshape(-1, 3))
-        self.n_tri = int(self.triangles.shape[0])
-        self.planes = f64(tri.planes, -1, 3)
-        self.neighbors = upload(np.ascontiguousarray(dl.neighbors, dtype=np.int32))
-        self.transform = f64(dl.transform, -1, 3, 2)
-        self.equations = f64(dl.equations, -1, 4)
         sp, sd = tri.support_points()
         sp = np.asarray(sp, dtype=np.float64).reshape(-1, 2)
+        parts = [
+            ("points", np.asarray(tri.points, dtype=np.float64).reshape(-1, 2)),
+            ("disparities", np.asarray(tri.disparities, dtype=np.float64).reshape(-1)),
+            ("triangles", np.asarray(tri.triangles, dtype=np.int32).reshape(-1, 3)),
+            ("planes", np.asarray(tri.planes, dtype=np.float64).reshape(-1, 3)),
+            ("neighbors", np.asarray(dl.neighbors, dtype=np.int32).reshape(-1, 3)),
+            ("transform", np.asarray(dl.transform, dtype=np.float64).reshape(-1, 3, 2)),
+            ("equations", np.asarray(dl.equations, dtype=np.float64).reshape(-1, 4)),
+            ("sup_uv", sp),
+            ("sup_d", np.asarray(sd, dtype=np.float64).reshape(-1)),
+        ]
+        offs, total = [], 0
+        for _, a in parts:
+            offs.append(total)
+            total += (a.nbytes + 255) & ~255
+        i, stage = _STAGING.take(total)
+        host = stage.numpy()
+        for (_, a), o in zip(parts, offs):
+            np.copyto(host[o:o + a.nbytes].view(a.dtype).reshape(a.shape), a)
+        self.buffer = torch.empty(max(total, 1), dtype=torch.uint8, device=dev())
+        self.buffer[:total].copy_(stage[:total], non_blocking=True)
+        _STAGING.mark(i)
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32}
+        for (name, a), o in zip(parts, offs):
+            view = self.buffer[o:o + a.nbytes].view(tdt[a.dtype]).reshape(a.shape)
+            setattr(self, name, view if a.size else None)
+        self.n_pts = parts[0][1].shape[0]
+        self.n_tri = parts[2][1].shape[0]
         self.n_sup = int(sp.shape[0])
-        self.sup_uv = f64(sp, -1, 2) if self.n_sup else None
-        self.sup_d = f64(sd, -1) if self.n_sup else None
         s = N.StTri()
         s.points, s.disparities = self.points.data_ptr(), self.disparities.data_ptr()
         s.simplices, s.planes = self.triangles.data_ptr(), self.planes.data_ptr()
@@ -87,6 +133,9 @@ class TriDevice:
     @property
     def nbytes(self):
         return self.n_pts * 24 + self.n_tri * (12 + 24 + 12 + 48 + 32) + self.n_sup * 24
+
+    def tensors(self):
+        return [self.buffer]
 
 
 def mu_raster_device(tri, width, height, clip_dmax=0.0, tri_dev=None):

@@ -157,15 +157,126 @@ class FramePipeline:
     def fetch(self):
         """D2H of every artefact into fresh pinned host buffers (torch's caching
         host allocator recycles them once the caller drops the arrays)."""
+        host = self.fetch_async(self.t.cuda.current_stream())
+        self.t.cuda.current_stream().synchronize()
+        return host
+
+    def fetch_async(self, stream):
+        """Enqueue the D2H copies on `stream`; the arrays are valid once it syncs."""
         t = self.t
         outs = []
-        for d in (self.values, self.status, self.sbits, self.vbits, self.image, self.prov,
-                  self.n_rays):
-            h = t.empty(d.shape, dtype=d.dtype, pin_memory=True)
-            h.copy_(d, non_blocking=True)
-            outs.append(h)
-        t.cuda.current_stream().synchronize()
+        with t.cuda.stream(stream):
+            for d in (self.values, self.status, self.sbits, self.vbits, self.image, self.prov,
+                      self.n_rays):
+                h = t.empty(d.shape, dtype=d.dtype, pin_memory=True)
+                h.copy_(d, non_blocking=True)
+                outs.append(h)
         return [h.numpy() for h in outs]
+
+
+def _outputs_of(pipe, stats, host):
+    values, status, sbits, vbits, img, prov, nr = host
+    return Reconstruction(
+        disparity=DisparityMap(values=values, status=status),
+        segmentation=SegmentationState(static_bits=sbits.view(np.uint32),
+                                       valid_bits=vbits.view(np.uint32)),
+        stats=stats, image=img, provenance=prov, n_rays=nr)
+
+
+def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=False,
+                       median_radius=1, forced_iters=0):
+    """Pipelined `reconstruct` over a sequence of (frame, tri) pairs.
+
+    Yields one Reconstruction per frame, in order.  Two device pipelines
+    alternate: while frame i computes on the caller's stream, a host thread
+    uploads frame i+1 (pinned frames copy by DMA) and its triangulation on a
+    copy stream, and frame i-1's artefacts stream back to pinned host memory
+    on a third stream.  Every frame gets the full per-frame work of
+    `reconstruct`.
+    """
+    import queue
+    import threading
+
+    t = require_cuda()
+    params = params or SolverParams()
+    prior_params = prior_params or PriorParams()
+    it = iter(items)
+    first = next(it, None)
+    if first is None:
+        return
+    h, w = first[0].shape
+    pipes = [FramePipeline(rig, w, h, params, prior_params) for _ in range(2)]
+    main = t.cuda.current_stream()
+    copy_s, out_s = t.cuda.Stream(), t.cuda.Stream()
+    free = [None, None]          # event: pipe's inputs/outputs no longer in use
+    free_lock = threading.Condition()
+    q = queue.Queue(maxsize=1)
+    error = []
+
+    device = t.cuda.current_device()
+
+    def prep():
+        t.cuda.set_device(device)
+        try:
+            for i, (frame, tri) in enumerate(_chain(first, it)):
+                pipe = pipes[i % 2]
+                with free_lock:
+                    while i >= 2 and free[i % 2] is None:
+                        free_lock.wait()
+                    ev = free[i % 2]
+                    free[i % 2] = None
+                with t.cuda.stream(copy_s):
+                    if ev is not None:
+                        copy_s.wait_event(ev)
+                    pipe.load(frame.images, frame.priors)
+                    td = TriDevice(tri)
+                    loaded = t.cuda.Event()
+                    loaded.record(copy_s)
+                q.put((pipe, td, loaded))
+        except Exception as exc:  # noqa: BLE001 -- surfaced in the consumer
+            error.append(exc)
+        q.put(None)
+
+    worker = threading.Thread(target=prep, daemon=True)
+    worker.start()
+    pending = None
+    i = 0
+    while True:
+        item = q.get()
+        if item is None:
+            break
+        pipe, td, loaded = item
+        main.wait_event(loaded)
+        for x in td.tensors():
+            x.record_stream(main)
+        stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
+                         median_radius=median_radius)
+        done = t.cuda.Event()
+        done.record(main)
+        with t.cuda.stream(out_s):
+            out_s.wait_event(done)
+            host = pipe.fetch_async(out_s)
+            fetched = t.cuda.Event()
+            fetched.record(out_s)
+        with free_lock:
+            free[i % 2] = fetched
+            free_lock.notify_all()
+        if pending is not None:
+            pending[2].synchronize()
+            yield _outputs_of(*pending[:2], pending[3])
+        pending = (pipe, stats, fetched, host)
+        i += 1
+    worker.join()
+    if error:
+        raise error[0]
+    if pending is not None:
+        pending[2].synchronize()
+        yield _outputs_of(*pending[:2], pending[3])
+
+
+def _chain(first, rest):
+    yield first
+    yield from rest
 
 
 _PIPES = {}
