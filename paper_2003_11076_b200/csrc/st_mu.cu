@@ -17,7 +17,10 @@
 //      whose predecessor has <= 2 claimers; each chunk is walked once per
 //      possible incoming start (the predecessor's claimers), replaying
 //      _find_simplex / _find_simplex_directed step by step.
-//   3. k_resolve_runs: one thread per run links its chunks (a few lookups).
+//      When both speculative walks end in the same simplex (the usual case)
+//      the next chunk's start is decided right there.
+//   3. k_resolve_chunks: the remaining links are followed forward from every
+//      decided chunk (a few lookups each).
 //   4. k_mu_eval: pick the resolved simplex, evaluate its plane left to
 //      right, clip.
 #include <cuda_runtime.h>
@@ -335,9 +338,7 @@ __global__ void k_mu_lists(int64_t npx, MuWs w) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = p < npx;
   const bool cs = in && chunk_start(w, p);
-  const bool rs = in && ambiguous(w, p) && (p == 0 || !ambiguous(w, p - 1));
   append_lane(cs, (int32_t)p, w.chunks, w.counts);
-  append_lane(rs, (int32_t)p, w.runs, w.counts + 1);
 }
 
 __global__ void k_walk_chunks(TriDev d, int W, int64_t npx, MuWs w) {
@@ -376,6 +377,7 @@ __global__ void k_walk_chunks(TriDev d, int W, int64_t npx, MuWs w) {
       return;
     }
   }
+  if (nopt == 1) w.chosen[p] = 0;  // a run start: its incoming start is known
   int64_t q = p;
   int st0 = opts[0], st1 = nopt > 1 ? opts[1] : 0;
   TriCache tc0, tc1;
@@ -389,19 +391,29 @@ __global__ void k_walk_chunks(TriDev d, int W, int64_t npx, MuWs w) {
   w.len[p] = (int32_t)(q - p);
   w.end0[p] = st0;
   w.end1[p] = nopt > 1 ? st1 : st0;
+  // Both speculative walks ended in the same simplex (the usual, "sticky"
+  // case): the next chunk's incoming start no longer depends on this
+  // chunk's choice, so decide it here.
+  if (w.end0[p] == w.end1[p] && q < npx && ambiguous(w, q)) {
+    if ((int)w.tmin[q - 1] == st0)
+      w.chosen[q] = 0;
+    else if ((int)w.tmax[q - 1] == st0)
+      w.chosen[q] = 1;
+  }
 }
 
-__global__ void k_resolve_runs(TriDev d, int W, int64_t npx, MuWs w) {
+// Links the chunks the walk kernel could not decide locally: from every
+// decided chunk, follow the run forward while the next chunk is undecided.
+__global__ void k_resolve_chunks(TriDev d, int W, int64_t npx, MuWs w) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)w.counts[1]) return;
-  const int64_t p = w.runs[t];
-  int64_t c = p;
-  w.chosen[c] = 0;
-  int carry = w.end0[c];
+  if (t >= (int64_t)w.counts[0]) return;
+  int64_t c = w.chunks[t];
+  uint8_t ch = w.chosen[c];
+  if (ch == 0xff) return;  // undecided: resolved by the thread of a decided predecessor
   for (;;) {
     const int64_t nxt = c + w.len[c];
-    if (nxt >= npx || !ambiguous(w, nxt)) break;
-    // nxt starts a chunk of the same run; its predecessor has two claimers
+    if (nxt >= npx || !ambiguous(w, nxt) || w.chosen[nxt] != 0xff) break;
+    const int carry = ch == 1 ? w.end1[c] : w.end0[c];  // (a replayed chunk keeps its end in end0)
     uint8_t pick;
     if ((int)w.tmin[nxt - 1] == carry) {
       pick = 0;
@@ -411,19 +423,16 @@ __global__ void k_resolve_runs(TriDev d, int W, int64_t npx, MuWs w) {
       // the incoming start is not a claimer of the predecessor (never seen
       // in practice): replay this chunk sequentially from the true start
       int st = carry;
-      int64_t q = nxt;
       const int64_t e = nxt + w.len[nxt];
       TriCache tc;
-      for (; q < e; ++q)
+      for (int64_t q = nxt; q < e; ++q)
         w.final_s[q] = find_simplex(d, w, q, (double)(q % W), (double)(q / W), st, tc);
-      w.chosen[nxt] = 2;
-      carry = st;
-      c = nxt;
-      continue;
+      w.end0[nxt] = st;
+      pick = 2;
     }
     w.chosen[nxt] = pick;
-    carry = pick ? w.end1[nxt] : w.end0[nxt];
     c = nxt;
+    ch = pick;
   }
 }
 
@@ -582,6 +591,7 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   };
   prof();
   ST_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned) * npx, s));
+  ST_CUDA_CHECK(cudaMemsetAsync(w.chosen, 0xff, npx, s));  // every chunk undecided
   ST_CUDA_CHECK(cudaMemsetAsync(w.tmin, 0xff, sizeof(unsigned) * npx, s));
   ST_CUDA_CHECK(cudaMemsetAsync(w.tmax, 0, sizeof(unsigned) * npx, s));
   ST_CUDA_CHECK(cudaMemsetAsync(w.counts, 0, 8 * sizeof(unsigned), s));
@@ -613,8 +623,8 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   st::k_walk_chunks<<<(unsigned)((npx + 127) / 128), 128, 0, s>>>(d, W, npx, w);
   ST_LAUNCH_CHECK("k_walk_chunks");
   prof();
-  st::k_resolve_runs<<<blocks, 256, 0, s>>>(d, W, npx, w);
-  ST_LAUNCH_CHECK("k_resolve_runs");
+  st::k_resolve_chunks<<<(unsigned)((npx + 127) / 128), 128, 0, s>>>(d, W, npx, w);
+  ST_LAUNCH_CHECK("k_resolve_chunks");
   prof();
   st::k_mu_eval<<<blocks, 256, 0, s>>>(d, W, npx, w, clip_dmax, mu_out);
   ST_LAUNCH_CHECK("k_mu_eval");
