@@ -3,6 +3,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -138,7 +139,7 @@ int prepare_estep_kernels() {
   static bool done = false;
   if (done) return ST_OK;
   const int max_smem = estep_smem(ST_MAX_VIEWS);
-  ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_at<0>,
+  ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_at,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_rays,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
@@ -146,16 +147,31 @@ int prepare_estep_kernels() {
   return ST_OK;
 }
 
-// E-step launch with the view count as a template parameter where it is small.
-void launch_e_step(int K, unsigned blocks, cudaStream_t s, const st::EmCtx& c,
-                   const st::EStepArgs& a) {
-  const int smem = estep_smem(K);
+// E-step launch: the register-resident screened kernel for K <= 5 views
+// (templated on K and on the rectified-rig shortcut), the shared-memory
+// enumeration for larger rigs.  `n` bounds the rows (list or dense).
+template <int K>
+void launch_taps(unsigned blocks, cudaStream_t s, const st::EmCtx& c, const st::EStepArgs& a) {
+  if (c.rectified)
+    st::k_e_step_taps<K, true><<<blocks, ESTEP_TAPS_BLOCK, 0, s>>>(c, a);
+  else
+    st::k_e_step_taps<K, false><<<blocks, ESTEP_TAPS_BLOCK, 0, s>>>(c, a);
+}
+
+void launch_e_step(int K, int64_t n, cudaStream_t s, const st::EmCtx& c,
+                   const st::EStepArgs& args) {
+  const bool exhaustive = getenv("ST_ESTEP_EXHAUSTIVE") != nullptr;  // cross-check
+  st::EStepArgs a = args;
+  a.exhaustive = exhaustive ? 1 : 0;
+  const unsigned bt = blocks_for(n, ESTEP_TAPS_BLOCK);
   switch (K) {
-    case 2: st::k_e_step_at<2><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
-    case 3: st::k_e_step_at<3><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
-    case 4: st::k_e_step_at<4><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
-    case 5: st::k_e_step_at<5><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
-    default: st::k_e_step_at<0><<<blocks, ESTEP_BLOCK, smem, s>>>(c, a); break;
+    case 2: launch_taps<2>(bt, s, c, a); break;
+    case 3: launch_taps<3>(bt, s, c, a); break;
+    case 4: launch_taps<4>(bt, s, c, a); break;
+    case 5: launch_taps<5>(bt, s, c, a); break;
+    default:
+      st::k_e_step_at<<<blocks_for(n, ESTEP_BLOCK), ESTEP_BLOCK, estep_smem(K), s>>>(c, a);
+      break;
   }
 }
 
@@ -369,7 +385,7 @@ int st_e_step_at(const st_frame* f, const st_rig* rig, const st_params* p, const
   a.static_out = static_out;
   a.valid_out = valid_out;
   a.scatter = 0;
-  launch_e_step(rig->num_views, blocks_for(n, ESTEP_BLOCK), (cudaStream_t)stream, c, a);
+  launch_e_step(rig->num_views, n, (cudaStream_t)stream, c, a);
   ST_LAUNCH_CHECK("k_e_step_at");
   return ST_OK;
 }
@@ -570,7 +586,7 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       e.static_out = static_bits;
       e.valid_out = valid_bits;
       e.scatter = 1;
-      launch_e_step(rig->num_views, blocks_for(n_act, ESTEP_BLOCK), s, c, e);
+      launch_e_step(rig->num_views, n_act, s, c, e);
       ST_LAUNCH_CHECK("k_e_step_at");
       ev.record(2, s);
       const int sblk = (int)blocks_for(n_act, STATS_BLOCK);

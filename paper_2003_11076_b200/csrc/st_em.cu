@@ -430,76 +430,181 @@ __device__ __forceinline__ double div_c(double x) {
   else return div_small(x, (double)N, 1.0 / N);                      // RN(1/N) folded at compile time
 }
 
-// All non-empty view masks in depth-first order: mask C = M | (1 << KB) takes
-// its per-channel sums from its prefix M plus view KB, which is exactly the
-// reference's in-order accumulation over the selected views (BLAS dgemm with
-// a 0/1 operand, solver.py:148-149).  Masks with one view have variance 0 and
-// are deficient under min_static_rays >= 2, so they are not accumulated.
+// fp32 screening sums: every non-empty mask's per-channel prefix b1 in
+// depth-first order (C = M | 1 << KB extends its prefix M by view KB),
+// accumulating b1^2; sum_c b2 is recovered later from per-view totals.
 template <int K, int M, int KB>
-__device__ __forceinline__ void mask_dfs(const double (&fk)[K], const double (&sq)[K], double a1,
-                                         double a2, double (&var)[1 << K]) {
+__device__ __forceinline__ void mask_dfs32(const float (&g)[K], float a1, float (&acc)[1 << K]) {
   if constexpr (KB < K) {
     constexpr int C = M | (1 << KB);
-    constexpr int POP = popc_c(C);
-    double b1, b2;
-    if constexpr (M == 0) {
-      b1 = fk[KB];
-      b2 = sq[KB];
-    } else {
-      b1 = dadd(a1, fk[KB]);
-      b2 = dadd(a2, sq[KB]);
-    }
-    // (s2 - s1*s1/n), summed over channels in order (axis-1 reduce)
-    if constexpr (POP >= 2) var[C] = dadd(var[C], dsub(b2, div_c<POP>(dmul(b1, b1))));
-    mask_dfs<K, C, KB + 1>(fk, sq, b1, b2, var);  // supersets of C
-    mask_dfs<K, M, KB + 1>(fk, sq, a1, a2, var);  // M with a later view instead
+    const float b1 = M == 0 ? g[KB] : a1 + g[KB];
+    if constexpr (popc_c(C) >= 2) acc[C] = fmaf(b1, b1, acc[C]);
+    mask_dfs32<K, C, KB + 1>(g, b1, acc);  // supersets of C
+    mask_dfs32<K, M, KB + 1>(g, a1, acc);  // M with a later view instead
   }
 }
 
-// Register path for K <= 5 (<= 32 masks, fully unrolled).
-template <int K>
-__device__ __forceinline__ uint32_t estep_small(const double* __restrict__ f, int stride,
-                                                const double* l1, const double* l0,
-                                                uint32_t vbits, const st_params& p) {
-  constexpr int M = 1 << K;
-  double var[M];
+// Exact score of one mask in the reference's arithmetic order: per channel
+// the in-order sums over the selected views (BLAS dgemm with a 0/1 operand,
+// solver.py:148-149), (s2 - s1*s1/n) summed over channels in order, then
+// prior - beta * var (solver.py:150-156).  `load(k, w, f)` yields channels
+// 4w..4w+3 of view k exactly as gather_rays samples them.
+template <int K, typename Load>
+__device__ __forceinline__ double score_exact(uint32_t m, Load& load, const double* l1,
+                                              const double* l0, const st_params& p) {
+  const int pop = __popc(m);
+  double vr;
+  if (pop < p.min_static_rays) {
+    vr = variance_ceiling();
+  } else if (pop == 0) {
+    vr = 0.0;
+  } else {
+    double acc = 0.0;
+#pragma unroll 1
+    for (int w = 0; w < 4; ++w) {
+      double a1[4], a2[4];
+      bool first = true;
 #pragma unroll
-  for (int m = 0; m < M; ++m) var[m] = 0.0;
-  for (int ch = 0; ch < 16; ++ch) {
-    double fk[K], sq[K];
+      for (int k = 0; k < K; ++k) {
+        if (!((m >> k) & 1)) continue;
+        double x[4];
+        load(k, w, x);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double x2 = dmul(x[j], x[j]);
+          a1[j] = first ? x[j] : dadd(a1[j], x[j]);
+          a2[j] = first ? x2 : dadd(a2[j], x2);
+        }
+        first = false;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc = dadd(acc, dsub(a2[j], div_n(dmul(a1[j], a1[j]), pop)));
+    }
+    vr = fmax(div_n(acc, pop), 0.0);
+  }
+  double a = 0.0, b = 0.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if ((m >> k) & 1)
+      a = dadd(a, l1[k]);
+    else
+      b = dadd(b, l0[k]);
+  }
+  return dsub(dadd(a, b), dmul(p.beta, vr));
+}
+
+// E-step argmax for K <= 5 (<= 32 masks): screen in fp32, decide in fp64.
+//
+// Every mask is scored in fp32 on data centred at the first valid view
+// (variance is shift-invariant), with sum_c b2 = sum_{k in m} Q_k taken from
+// per-view totals, so one mask-channel costs an FADD and an FFMA.  D below
+// majorises |score32(m) - score64(m)| for every admissible mask: variance
+// numerator error <= 50u*S2c (u = 2^-24, S2c = centred sum of squares over
+// the valid views), the fp64 recipe's own error <= 2^-47*S2u, the prior sum
+// <= (K+3)u*L, beta*v rounding <= 2u*beta*max(ceiling, S2c), all doubled.
+// The reference's argmax m* therefore has score32(m*) >= best32 - 2D, and
+// only the masks in that window are re-scored exactly (score_exact) under
+// the reference's tie rules -- normally one.  `exhaustive` re-scores every
+// admissible mask (the cross-check behind ST_ESTEP_EXHAUSTIVE).
+template <int K, typename Load>
+__device__ __forceinline__ uint32_t estep_small(Load& load, const double* l1, const double* l0,
+                                                uint32_t vbits, const st_params& p,
+                                                bool exhaustive) {
+  constexpr int M = 1 << K;
+  constexpr float U = 5.9604645e-08f;  // 2^-24
+  if (!vbits) return 0;                // only the empty mask is admissible
+  const int k0 = __ffs(vbits) - 1;
+  float acc[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m] = 0.0f;
+  float q[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) q[k] = 0.0f;
+  float s2u = 0.0f;
+#pragma unroll 1
+  for (int w = 0; w < 4; ++w) {
+    double ref[4];
+#pragma unroll
+    for (int k = 0; k < K; ++k)  // compile-time view index keeps the taps in registers
+      if (k == k0) load(k, w, ref);
+    float g[K][4];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      fk[k] = f[(k * 16 + ch) * stride];
-      sq[k] = dmul(fk[k], fk[k]);
+      double x[4] = {0.0, 0.0, 0.0, 0.0};  // invalid rays hold 0
+      if ((vbits >> k) & 1) load(k, w, x);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        g[k][j] = __double2float_rn(dsub(x[j], ref[j]));
+        q[k] = fmaf(g[k][j], g[k][j], q[k]);
+        const float xf = __double2float_rn(x[j]);
+        s2u = fmaf(xf, xf, s2u);
+      }
     }
-    mask_dfs<K, 0, 0>(fk, sq, 0.0, 0.0, var);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float gj[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) gj[k] = g[k][j];
+      mask_dfs32<K, 0, 0>(gj, 0.0f, acc);
+    }
   }
+  float s2c = 0.0f, lsum = 0.0f, l0tot = 0.0f, dl[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if ((vbits >> k) & 1) s2c += q[k];
+    const float f1 = __double2float_rn(l1[k]), f0 = __double2float_rn(l0[k]);
+    dl[k] = f1 - f0;
+    l0tot += f0;
+    lsum += fabsf(f1) + fabsf(f0);
+  }
+  const float beta = (float)p.beta;
+  const float ceil32 = (float)variance_ceiling();
+  constexpr float inv_n[6] = {1.0f, 1.0f, 0.5f, 1.0f / 3.0f, 0.25f, 0.2f};
+  float sc[M];
+  float best32 = -INFINITY;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int pop = __popc(m);
+    float v;
+    if (pop < p.min_static_rays) {
+      v = ceil32;
+    } else if (pop < 2) {
+      v = 0.0f;
+    } else {
+      float qs = 0.0f;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if ((m >> k) & 1) qs += q[k];
+      v = fmaxf((qs - acc[m] * inv_n[pop]) * inv_n[pop], 0.0f);
+    }
+    float pr = l0tot;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if ((m >> k) & 1) pr += dl[k];
+    sc[m] = pr - beta * v;
+    if (!((uint32_t)m & ~vbits)) best32 = fmaxf(best32, sc[m]);
+  }
+  const float D = 2.0f * (fabsf(beta) * (64.0f * U * s2c + 2.0f * U * fmaxf(ceil32, s2c) +
+                                         7.1054274e-15f * s2u + 2.0f * U * ceil32) +
+                          (2.0f * K + 6.0f) * U * lsum);
+  const float thr = best32 - 2.0f * D;
+  const bool all = exhaustive || !(thr > -INFINITY);  // non-finite bound: decide exhaustively
+  uint32_t cand = 0;
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+    if (all || sc[m] >= thr) cand |= 1u << m;
   double best = -INFINITY;
   int bpop = -1;
   uint32_t bm = 0;
-#pragma unroll
-  for (int m = 0; m < M; ++m) {
-    if ((uint32_t)m & ~vbits) continue;  // touches an invalid ray
+  for (; cand; cand &= cand - 1) {
+    const uint32_t m = __ffs(cand) - 1;
+    if (m & ~vbits) continue;  // touches an invalid ray
+    const double s = score_exact<K>(m, load, l1, l0, p);
     const int pop = __popc(m);
-    double vr;
-    if (pop < p.min_static_rays) {
-      vr = variance_ceiling();
-    } else {
-      vr = fmax(div_n(var[m], pop > 0 ? pop : 1), 0.0);
-    }
-    double a = 0.0, b = 0.0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if ((m >> k) & 1)
-        a = dadd(a, l1[k]);
-      else
-        b = dadd(b, l0[k]);
-    }
-    const double s = dsub(dadd(a, b), dmul(p.beta, vr));
-    if (prefer(s, pop, (uint32_t)m, best, bpop, bm)) {
+    if (prefer(s, pop, m, best, bpop, bm)) {
       best = s;
       bpop = pop;
-      bm = (uint32_t)m;
+      bm = m;
     }
   }
   return bm;
@@ -553,43 +658,111 @@ __device__ uint32_t estep_generic(int K, const double* __restrict__ f, int strid
   return bm;
 }
 
+// Loader over rays staged in shared memory: element (k, ch) of thread t at
+// smem[(k * 16 + ch) * stride + t].
+struct SmemRays {
+  const double* f;
+  int stride;
+  __device__ __forceinline__ void operator()(int k, int w, double (&x)[4]) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = f[(k * 16 + 4 * w + j) * stride];
+  }
+};
+
 __device__ __forceinline__ uint32_t estep_dispatch(int K, const double* f, int stride,
                                                    const double* l1, const double* l0,
                                                    uint32_t vbits, const st_params& p) {
+  SmemRays ld{f, stride};
   switch (K) {
-    case 2: return estep_small<2>(f, stride, l1, l0, vbits, p);
-    case 3: return estep_small<3>(f, stride, l1, l0, vbits, p);
-    case 4: return estep_small<4>(f, stride, l1, l0, vbits, p);
-    case 5: return estep_small<5>(f, stride, l1, l0, vbits, p);
+    case 2: return estep_small<2>(ld, l1, l0, vbits, p, false);
+    case 3: return estep_small<3>(ld, l1, l0, vbits, p, false);
+    case 4: return estep_small<4>(ld, l1, l0, vbits, p, false);
+    case 5: return estep_small<5>(ld, l1, l0, vbits, p, false);
     default: return estep_generic(K, f, stride, l1, l0, vbits, p);
   }
 }
 
-// Gather one pixel's rays at disparity d into smem (solver.py:206-227) and
-// return the valid bits; q of invalid rays is 0.5, descriptors 0.
-__device__ __forceinline__ uint32_t gather_pixel(const EmCtx& c, double u, double v, double d,
-                                                 double* f, int stride, double* q) {
-  uint32_t vb = 0;
-  for (int k = 0; k < c.rig.num_views; ++k) {
-    const WarpOut w = warp_ctx(c, k, u, v, d);
-    if (in_margin(c.rig, k, w)) {
-      const Taps t = taps_ctx(c, w);
-      sample_desc(c.desc + (size_t)k * c.HW, c.W, t,
-                  [&](int ch, double x) { f[(k * 16 + ch) * stride] = x; });
-      q[k] = sample_prior(c.priors + (size_t)k * c.HW, c.W, t);
-      vb |= 1u << k;
-    } else {
+// Channels 4w..4w+3 of one descriptor sample, recomputed from the uint8 map
+// with exactly sample_desc's arithmetic (sampling.py:49-55).
+template <bool RECT>
+__device__ __forceinline__ void desc_word(const uint32_t* __restrict__ plane, int idx, int su,
+                                          int sv, double fu, double fv, int w,
+                                          double (&f)[4]) {
+  const uint32_t* p = plane + (size_t)idx * 4 + w;
+  const uint32_t a = __ldg(p), b = __ldg(p + 4 * su);
+  if (RECT || fv == 0.0) {
+    lerp_word(a, b, fu, f);
+  } else {
+    const uint32_t e = __ldg(p + 4 * (size_t)sv), g = __ldg(p + 4 * ((size_t)sv + su));
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) f[(k * 16 + ch) * stride] = 0.0;
-      q[k] = 0.5;
+    for (int j = 0; j < 4; ++j) {
+      const int sh = 8 * j;
+      const double top = lerp_u8((a >> sh) & 0xff, (b >> sh) & 0xff, fu);
+      const double bot = lerp_u8((e >> sh) & 0xff, (g >> sh) & 0xff, fu);
+      f[j] = dadd(top, dmul(fv, dsub(bot, top)));
     }
   }
-  return vb;
 }
 
-// KT > 0: the view count is a compile-time constant, so the per-view arrays
-// below stay in registers; KT == 0 handles any K (<= 12) at run time.
-template <int KT>
+// E-step at the solver's disparities for K <= 5 views (solver.py:409-419).
+// No ray staging: each view keeps only its tap (index, weights) in
+// registers and the screen / exact re-score re-read the 16-byte descriptor
+// words (L1-resident), so occupancy is bounded by registers alone.  RECT:
+// rectified rig, vertical weight identically 0.
+template <int KT, bool RECT>
+__global__ void __launch_bounds__(ESTEP_TAPS_BLOCK) k_e_step_taps(EmCtx c, EStepArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
+  if (t >= n_work) return;
+  const int64_t i = a.list ? (int64_t)a.list[t] : t;
+  if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) return;  // solver.py:476-478
+  const int64_t pix = a.pix ? a.pix[i] : i;
+  const double u = (double)(pix % c.W), v = (double)(pix / c.W);
+  const double d = a.d[i];
+  int idx[KT];
+  double fu[KT], fv[KT], l1[KT], l0[KT];
+  uint32_t vb = 0;
+  // gather_rays (solver.py:206-227): invalid rays carry q 0.5
+#pragma unroll
+  for (int k = 0; k < KT; ++k) {
+    const WarpOut w = warp_ctx(c, k, u, v, d);
+    double q = 0.5;
+    idx[k] = 0;
+    fu[k] = 0.0;
+    fv[k] = 0.0;
+    if (in_margin(c.rig, k, w)) {
+      const Taps tp = taps_ctx(c, w);
+      idx[k] = tp.iv * c.W + tp.iu;
+      fu[k] = tp.fu;
+      if (!RECT) fv[k] = tp.fv;
+      q = sample_prior(c.priors + (size_t)k * c.HW, c.W, tp);
+      vb |= 1u << k;
+    }
+    clamp_logs(q, c.p.epsilon_prior, l1[k], l0[k]);
+  }
+  const int su = c.W > 1 ? 1 : 0, sv = c.H > 1 ? c.W : 0;  // taps_of's steps
+  const uint32_t* desc = reinterpret_cast<const uint32_t*>(c.desc);
+  auto load = [&](int k, int w, double (&x)[4]) {
+    desc_word<RECT>(desc + (size_t)k * c.HW * 4, idx[k], su, sv, fu[k], RECT ? 0.0 : fv[k], w,
+                    x);
+  };
+  const uint32_t m = estep_small<KT>(load, l1, l0, vb, c.p, a.exhaustive != 0);
+  const int64_t o = a.scatter ? pix : i;
+  a.static_out[o] = m;
+  a.valid_out[o] = vb;
+}
+
+template __global__ void k_e_step_taps<2, false>(EmCtx, EStepArgs);
+template __global__ void k_e_step_taps<3, false>(EmCtx, EStepArgs);
+template __global__ void k_e_step_taps<4, false>(EmCtx, EStepArgs);
+template __global__ void k_e_step_taps<5, false>(EmCtx, EStepArgs);
+template __global__ void k_e_step_taps<2, true>(EmCtx, EStepArgs);
+template __global__ void k_e_step_taps<3, true>(EmCtx, EStepArgs);
+template __global__ void k_e_step_taps<4, true>(EmCtx, EStepArgs);
+template __global__ void k_e_step_taps<5, true>(EmCtx, EStepArgs);
+
+// E-step for 6 <= K <= 12 views: rays staged in shared memory, masks
+// enumerated one at a time (estep_generic).
 __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a) {
   extern __shared__ double sh_f[];
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -602,47 +775,30 @@ __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a)
   const double d = a.d[i];
   double* f = sh_f + threadIdx.x;
   const int stride = blockDim.x;
-  constexpr int KA = KT > 0 ? KT : ST_MAX_VIEWS;
-  const int K = KT > 0 ? KT : c.rig.num_views;
-  double q[KA], l1[KA], l0[KA];
+  const int K = c.rig.num_views;
+  double l1[ST_MAX_VIEWS], l0[ST_MAX_VIEWS];
   uint32_t vb = 0;
   // gather_rays (solver.py:206-227): invalid rays carry desc 0 and q 0.5
-#pragma unroll
-  for (int k = 0; k < KA; ++k) {
-    if (KT == 0 && k >= K) break;
+  for (int k = 0; k < K; ++k) {
     const WarpOut w = warp_ctx(c, k, u, v, d);
+    double q = 0.5;
     if (in_margin(c.rig, k, w)) {
       const Taps tp = taps_ctx(c, w);
       sample_desc(c.desc + (size_t)k * c.HW, c.W, tp,
                   [&](int ch, double x) { f[(k * 16 + ch) * stride] = x; });
-      q[k] = sample_prior(c.priors + (size_t)k * c.HW, c.W, tp);
+      q = sample_prior(c.priors + (size_t)k * c.HW, c.W, tp);
       vb |= 1u << k;
     } else {
 #pragma unroll
       for (int ch = 0; ch < 16; ++ch) f[(k * 16 + ch) * stride] = 0.0;
-      q[k] = 0.5;
     }
+    clamp_logs(q, c.p.epsilon_prior, l1[k], l0[k]);
   }
-#pragma unroll
-  for (int k = 0; k < KA; ++k) {
-    if (KT == 0 && k >= K) break;
-    clamp_logs(q[k], c.p.epsilon_prior, l1[k], l0[k]);
-  }
-  uint32_t m;
-  if constexpr (KT > 0)
-    m = estep_small<KT>(f, stride, l1, l0, vb, c.p);
-  else
-    m = estep_generic(K, f, stride, l1, l0, vb, c.p);
+  const uint32_t m = estep_generic(K, f, stride, l1, l0, vb, c.p);
   const int64_t o = a.scatter ? pix : i;
   a.static_out[o] = m;
   a.valid_out[o] = vb;
 }
-
-template __global__ void k_e_step_at<0>(EmCtx, EStepArgs);
-template __global__ void k_e_step_at<2>(EmCtx, EStepArgs);
-template __global__ void k_e_step_at<3>(EmCtx, EStepArgs);
-template __global__ void k_e_step_at<4>(EmCtx, EStepArgs);
-template __global__ void k_e_step_at<5>(EmCtx, EStepArgs);
 
 // initial_masks (solver.py:421-432): valid & q >= threshold at mu.
 __global__ void k_initial_masks(EmCtx c, const int64_t* __restrict__ pix_list, int64_t n,

@@ -8,6 +8,7 @@
 #define EM_BLOCK 128
 #define STATS_BLOCK 256
 #define ESTEP_BLOCK 64
+#define ESTEP_TAPS_BLOCK 128
 #define ST_MAX_BAND 64
 
 namespace st {
@@ -72,6 +73,7 @@ struct EStepArgs {
   uint32_t* static_out;
   uint32_t* valid_out;
   int scatter;               // 1: write at pixel index, 0: at row i
+  int exhaustive;            // 1: score every mask in fp64 (no fp32 screen)
 };
 
 __global__ void k_m_step(EmCtx c, MStepArgs a);
@@ -81,7 +83,8 @@ __global__ void k_flag_mstep(const int64_t* active, int64_t n, const uint32_t* s
 __global__ void k_em_stats(int64_t n, int with_prev, const double* e, const double* pe,
                            const uint8_t* chg, const Partial* work, int n_work_parts,
                            Partial* parts);
-template <int KT>
+template <int KT, bool RECT>
+__global__ void k_e_step_taps(EmCtx c, EStepArgs a);
 __global__ void k_e_step_at(EmCtx c, EStepArgs a);
 __global__ void k_initial_masks(EmCtx c, const int64_t* pix, int64_t n, uint32_t* static_out,
                                 uint32_t* valid_out);

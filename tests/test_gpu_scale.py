@@ -87,3 +87,17 @@ def test_c2_properties(st):
     # energy descent (test_solver.py:305-320)
     for i, prev in enumerate(f.stats.prev_energy):
         assert f.stats.mean_energy[i + 1] <= prev + 1e-9
+
+
+def test_c2_screened_estep_equals_exhaustive(st, monkeypatch):
+    """The fp32-screened E-step decides exactly what scoring every mask in
+    fp64 decides (st_em.cu estep_small vs estep_small_exact), whole frame."""
+    frame, rig, tri, sp, pp = _inputs("C2")
+    a = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=5)
+    monkeypatch.setenv("ST_ESTEP_EXHAUSTIVE", "1")
+    b = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=5)
+    assert np.array_equal(a.segmentation.static_bits, b.segmentation.static_bits)
+    assert np.array_equal(a.segmentation.valid_bits, b.segmentation.valid_bits)
+    assert np.array_equal(a.disparity.values, b.disparity.values)
+    assert np.array_equal(a.image, b.image)
+    assert list(a.stats.mean_energy) == list(b.stats.mean_energy)
