@@ -89,12 +89,15 @@ def test_c2_properties(st):
         assert f.stats.mean_energy[i + 1] <= prev + 1e-9
 
 
-def test_c2_screened_estep_equals_exhaustive(st, monkeypatch):
-    """The fp32-screened E-step decides exactly what scoring every mask in
-    fp64 decides (st_em.cu estep_small vs estep_small_exact), whole frame."""
-    frame, rig, tri, sp, pp = _inputs("C2")
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_screened_em_equals_exhaustive(st, monkeypatch, cfg):
+    """The fp32-screened E-step and M-step decide exactly what evaluating
+    every mask / surviving candidate in fp64 decides (st_em.cu estep_small,
+    screen_energy), whole frame."""
+    frame, rig, tri, sp, pp = _inputs(cfg)
     a = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=5)
     monkeypatch.setenv("ST_ESTEP_EXHAUSTIVE", "1")
+    monkeypatch.setenv("ST_MSTEP_EXHAUSTIVE", "1")
     b = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=5)
     assert np.array_equal(a.segmentation.static_bits, b.segmentation.static_bits)
     assert np.array_equal(a.segmentation.valid_bits, b.segmentation.valid_bits)
