@@ -172,6 +172,48 @@ int st_support_build(const double* support_uv, const double* support_d, int32_t 
                      void* stream);
 int64_t st_support_workspace(int32_t n, int32_t W, int32_t H, double radius);
 
+/* ---- support harvest (prior.py:51-260) ----------------- */
+
+/* The rig quantities collect_support reads (geometry.py:128-252), with the
+ * pair warps precomputed on the host by the reference's own numpy
+ * expressions (pair_warp_coefficients, geometry.py:221-240). */
+typedef struct st_cams {
+  int32_t num_views;
+  int32_t ref_index;
+  int32_t width, height;                  /* every view */
+  int32_t nn[ST_MAX_VIEWS];               /* nearest_neighbor(k), geometry.py:191-196 */
+  double fx[ST_MAX_VIEWS], fy[ST_MAX_VIEWS], cx[ST_MAX_VIEWS], cy[ST_MAX_VIEWS];
+  double rot[ST_MAX_VIEWS][9];            /* extrinsics rotation, row-major */
+  double trans[ST_MAX_VIEWS][3];
+  double unit_baseline;
+  double fw_a[ST_MAX_VIEWS][9], fw_b[ST_MAX_VIEWS][3];  /* warp k -> nn[k] */
+  double bw_a[ST_MAX_VIEWS][9], bw_b[ST_MAX_VIEWS][3];  /* warp nn[k] -> k */
+  double lr_scale[ST_MAX_VIEWS];          /* fx[k] / fx[nn[k]] (prior.py:132) */
+} st_cams;
+
+/* collect_support up to (not including) deduplicate: detection on the
+ * stride grid (prior.py:51-66) gated by the eroded prior (:215-230, :248-250),
+ * forward SAD scan + uniqueness ratio + left-right check against the nearest
+ * neighbour (:69-138), and reprojection of other views' matches into the
+ * reference (:146-180).  n_d = len(np.arange(0.5, d_max + 0.25, 0.5)) <= 512.
+ * Writes the collected points in the reference's collection order (view,
+ * then raster) to out_u/out_v/out_d/out_src (device, capacity
+ * st_harvest_capacity) and their number to *out_count (device int64). */
+int st_harvest(const uint8_t* desc, const float* priors, const st_cams* cams, double d_max,
+               int32_t n_d, float threshold, int32_t stride, double min_texture,
+               int32_t* out_u, int32_t* out_v, double* out_d, int32_t* out_src,
+               int64_t* out_count, void* workspace, int64_t workspace_bytes, void* stream);
+int64_t st_harvest_capacity(int32_t K, int32_t W, int32_t H, int32_t stride);
+int64_t st_harvest_workspace(int32_t K, int32_t W, int32_t H, int32_t stride);
+
+/* deduplicate (prior.py:183-212) on the host: stable priority sort by
+ * (src != ref, d, v, u), greedy acceptance (pixel free and no accepted
+ * 8-neighbour more than 2 disparity units away), raster sort by (v, u, d).
+ * Writes the accepted input indices to keep (capacity n), count to *n_keep. */
+int st_support_dedup(const int32_t* u, const int32_t* v, const double* d, const int32_t* src,
+                     int64_t n, int32_t ref_index, int32_t W, int32_t H, int64_t* keep,
+                     int64_t* n_keep);
+
 /* solver.py:421-432 initial_masks over pix (nullable = all H*W pixels). */
 int st_initial_masks(const st_frame* f, const st_rig* rig, const st_params* p,
                      const int64_t* pix, int64_t n, uint32_t* static_out,

@@ -55,6 +55,19 @@ class StTri(C.Structure):
                 ("min_bound", C.c_double * 2), ("max_bound", C.c_double * 2)]
 
 
+class StCams(C.Structure):
+    _fields_ = [("num_views", C.c_int32), ("ref_index", C.c_int32),
+                ("width", C.c_int32), ("height", C.c_int32),
+                ("nn", C.c_int32 * MAX_VIEWS),
+                ("fx", C.c_double * MAX_VIEWS), ("fy", C.c_double * MAX_VIEWS),
+                ("cx", C.c_double * MAX_VIEWS), ("cy", C.c_double * MAX_VIEWS),
+                ("rot", (C.c_double * 9) * MAX_VIEWS), ("trans", (C.c_double * 3) * MAX_VIEWS),
+                ("unit_baseline", C.c_double),
+                ("fw_a", (C.c_double * 9) * MAX_VIEWS), ("fw_b", (C.c_double * 3) * MAX_VIEWS),
+                ("bw_a", (C.c_double * 9) * MAX_VIEWS), ("bw_b", (C.c_double * 3) * MAX_VIEWS),
+                ("lr_scale", C.c_double * MAX_VIEWS)]
+
+
 REDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int32, C.c_void_p)
 
 _P = C.c_void_p
@@ -75,6 +88,11 @@ _SIGS = {
     "st_support_build": (C.c_int, [_P, _P, _I32, _I32, _I32, C.POINTER(StParams),
                                    C.POINTER(StFrame), _P, _I64, C.POINTER(C.c_int64), _P]),
     "st_support_workspace": (C.c_int64, [_I32, _I32, _I32, _D]),
+    "st_harvest": (C.c_int, [_P, _P, C.POINTER(StCams), _D, _I32, C.c_float, _I32, _D,
+                             _P, _P, _P, _P, _P, _P, _I64, _P]),
+    "st_harvest_capacity": (C.c_int64, [_I32, _I32, _I32, _I32]),
+    "st_harvest_workspace": (C.c_int64, [_I32, _I32, _I32, _I32]),
+    "st_support_dedup": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P]),
     "st_initial_masks": (C.c_int, [C.POINTER(StFrame), C.POINTER(StRig), C.POINTER(StParams),
                                    _P, _I64, _P, _P, _P]),
     "st_gather_rays": (C.c_int, [C.POINTER(StFrame), C.POINTER(StRig), _P, _P, _I64, _P, _P,
@@ -192,6 +210,45 @@ def make_rig(rig, width, height):
         r.view_w[i] = int(intr.width)
         r.view_h[i] = int(intr.height)
     return r
+
+
+def make_cams(rig, width, height):
+    """st_cams from a CameraRig (geometry.py:128-252): intrinsics, extrinsics,
+    nearest neighbours and both pair warps of every (view, neighbour) pair,
+    computed by the rig's own numpy expressions."""
+    k = len(rig)
+    if k > MAX_VIEWS:
+        raise ValueError(f"mask enumeration is exponential; refusing {k} views "
+                         f"(limit {MAX_VIEWS})")
+    c = StCams()
+    c.num_views = k
+    c.ref_index = int(rig.ref_index)
+    c.width = int(width)
+    c.height = int(height)
+    c.unit_baseline = float(rig.unit_baseline)
+    for i in range(k):
+        intr, extr = rig.cameras[i]
+        nn = int(rig.nearest_neighbor(i))
+        c.nn[i] = nn
+        c.fx[i], c.fy[i], c.cx[i], c.cy[i] = (float(intr.fx), float(intr.fy), float(intr.cx),
+                                              float(intr.cy))
+        rot = np.asarray(extr.rotation, dtype=np.float64).reshape(9)
+        tr = np.asarray(extr.translation, dtype=np.float64).reshape(3)
+        for j in range(9):
+            c.rot[i][j] = float(rot[j])
+        for j in range(3):
+            c.trans[i][j] = float(tr[j])
+        for (dst_a, dst_b), (src, dst) in (((c.fw_a, c.fw_b), (i, nn)),
+                                           ((c.bw_a, c.bw_b), (nn, i))):
+            a, b = rig.pair_warp_coefficients(src, dst)
+            a = np.asarray(a, dtype=np.float64).reshape(9)
+            b = np.asarray(b, dtype=np.float64).reshape(3)
+            for j in range(9):
+                dst_a[i][j] = float(a[j])
+            for j in range(3):
+                dst_b[i][j] = float(b[j])
+        c.lr_scale[i] = float(intr.fx) / float(rig.intrinsics(nn).fx)  # prior.py:132
+    return c
 
 
 def make_params(sp, pp, forced_iters=0, timing=False):

@@ -17,60 +17,6 @@ namespace st {
 // ---------------------------------------------------------------------------
 // sampling
 
-// 16-channel bilinear descriptor sample, fp64 recipe (sampling.py:49-55 on
-// the float32 copy of the uint8 map: tap differences are exact integers).
-// Calls `sink(c, f)` for each channel in order.
-// Four channels of one 32-bit descriptor word pair: exact g0 and g1 - g0 as
-// doubles via the 2^52 trick (one PRMT / paired 16-bit SIMD difference + one
-// DADD each), then the fp64 lerp g0 + fu * (g1 - g0).
-__device__ __forceinline__ void lerp_word(uint32_t wa, uint32_t wb, double fu, double (&f)[4]) {
-  const uint32_t ea = wa & 0x00ff00ffu, eb = wb & 0x00ff00ffu;
-  const uint32_t oa = (wa >> 8) & 0x00ff00ffu, ob = (wb >> 8) & 0x00ff00ffu;
-  const uint32_t de = eb + 0x01000100u - ea;  // bytes 0 and 2: (g1 - g0 + 256) per 16-bit lane
-  const uint32_t dodd = ob + 0x01000100u - oa;  // bytes 1 and 3
-  const uint32_t lanes[4] = {__byte_perm(de, 0u, 0x4410), __byte_perm(dodd, 0u, 0x4410),
-                             __byte_perm(de, 0u, 0x4432), __byte_perm(dodd, 0u, 0x4432)};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const double g0 = __dsub_rn(__hiloint2double(0x43300000, __byte_perm(wa, 0u, 0x4440 | j)),
-                                4503599627370496.0);          // 2^52
-    const double df = __dsub_rn(__hiloint2double(0x43300000, lanes[j]),
-                                4503599627370752.0);          // 2^52 + 256
-    f[j] = dadd(g0, dmul(fu, df));
-  }
-}
-
-template <typename Sink>
-__device__ __forceinline__ void sample_desc(const uint4* __restrict__ plane, int W, const Taps& t,
-                                            Sink&& sink) {
-  const size_t base = (size_t)t.iv * W + t.iu;
-  const uint4 a = __ldg(plane + base);
-  const uint4 b = __ldg(plane + base + t.su);
-  const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
-  const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
-  if (t.fv == 0.0) {
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      double f[4];
-      lerp_word(aw[w], bw[w], t.fu, f);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) sink(4 * w + j, f[j]);
-    }
-  } else {
-    const uint4 e = __ldg(plane + base + t.sv);
-    const uint4 g = __ldg(plane + base + t.sv + t.su);
-    const uint32_t ew[4] = {e.x, e.y, e.z, e.w};
-    const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const int sh = 8 * (c & 3);
-      const double top = lerp_u8((aw[c >> 2] >> sh) & 0xff, (bw[c >> 2] >> sh) & 0xff, t.fu);
-      const double bot = lerp_u8((ew[c >> 2] >> sh) & 0xff, (gw[c >> 2] >> sh) & 0xff, t.fu);
-      sink(c, dadd(top, dmul(t.fv, dsub(bot, top))));
-    }
-  }
-}
-
 // Prior-plane sample (float32 plane, one channel).
 __device__ __forceinline__ double sample_prior(const float* __restrict__ plane, int W,
                                                const Taps& t) {

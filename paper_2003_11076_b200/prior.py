@@ -229,6 +229,93 @@ def triangulate(points, width, height):
                               num_anchors=n_anchor, _lookup=dl)
 
 
+# prior.py:25-30
+SUPPORT_STRIDE = 5
+MIN_TEXTURE = 25.0
+UNIQUENESS_RATIO = 0.9
+SECOND_BEST_EXCLUSION = 1.0
+LEFT_RIGHT_TOL = 1.0
+
+
+def _grid_len(d_max):
+    """len(np.arange(0.5, d_max + 0.25, 0.5)) -- the scan grid (prior.py:114)."""
+    return int(len(np.arange(0.5, float(d_max) + 0.25, 0.5)))
+
+
+def harvest_device(frame, rig, params=None, threshold=0.7, stride=SUPPORT_STRIDE,
+                   min_texture=MIN_TEXTURE):
+    """collect_support up to deduplicate, on the GPU (st_harvest).
+
+    Returns host arrays (u int32, v int32, d float64, source_view int32) of
+    the collected points in the reference's collection order (views in
+    order, each view's matches in raster order, prior.py:245-259).
+    """
+    from .device import download, empty, require_cuda
+    from .frame import device_frame
+    t = require_cuda()
+    params = params or PriorParams()
+    d = device_frame(frame)
+    K, H, W = d.K, d.H, d.W
+    if len(rig) != K:
+        raise ValueError("frame view count does not match the rig")
+    cams = N.make_cams(rig, W, H)
+    lib = N.lib()
+    cap = max(int(lib.st_harvest_capacity(K, W, H, int(stride))), 1)
+    ws = empty((max(int(lib.st_harvest_workspace(K, W, H, int(stride))), 1),), t.uint8)
+    ou = empty((cap,), t.int32)
+    ov = empty((cap,), t.int32)
+    od = empty((cap,), t.float64)
+    osrc = empty((cap,), t.int32)
+    cnt = empty((1,), t.int64)
+    N.invoke("st_harvest", d.desc, d.priors, cams, float(params.d_max), _grid_len(params.d_max),
+             float(threshold), int(stride), float(min_texture), ou, ov, od, osrc, cnt, ws,
+             ws.numel())
+    n = int(cnt.item())
+    return download(ou[:n]), download(ov[:n]), download(od[:n]), download(osrc[:n])
+
+
+def deduplicate_arrays(u, v, d, src, ref_index, width=None, height=None):
+    """deduplicate (prior.py:183-212) over arrays; returns the kept indices
+    in the final raster order (native host code, st_support_dedup)."""
+    import ctypes as C
+    u = np.ascontiguousarray(u, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.int32)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    src = np.ascontiguousarray(src, dtype=np.int32)
+    n = u.shape[0]
+    if n and (u.min() < 0 or v.min() < 0):
+        raise ValueError("support points must have non-negative pixel coordinates")
+    w = int(width) if width is not None else (int(u.max()) + 1 if n else 1)
+    h = int(height) if height is not None else (int(v.max()) + 1 if n else 1)
+    keep = np.empty(max(n, 1), dtype=np.int64)
+    nk = C.c_int64(0)
+    vp = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+    N.check(N.lib().st_support_dedup(vp(u), vp(v), vp(d), vp(src), n, int(ref_index), w, h,
+                                     vp(keep), C.byref(nk)))
+    return keep[:nk.value]
+
+
+def deduplicate(points, ref_index):
+    """prior.py:183-212 on SupportPoint lists."""
+    if not points:
+        return []
+    keep = deduplicate_arrays([p.u for p in points], [p.v for p in points],
+                              [p.d for p in points], [p.source_view for p in points], ref_index)
+    return [points[i] for i in keep]
+
+
+def collect_support(frame, rig, params, threshold, stride=SUPPORT_STRIDE,
+                    min_texture=MIN_TEXTURE):
+    """Full support-point harvest for one frame (prior.py:233-260): detection,
+    matching, left-right check and reprojection on the GPU, deduplication in
+    native host code.  Returns the reference's SupportPoint list."""
+    u, v, d, src = harvest_device(frame, rig, params, threshold, stride, min_texture)
+    h, w = frame.shape if hasattr(frame, "shape") else frame.images[0].shape[:2]
+    keep = deduplicate_arrays(u, v, d, src, rig.ref_index, w, h)
+    return [SupportPoint(u=int(u[i]), v=int(v[i]), d=float(d[i]), source_view=int(src[i]))
+            for i in keep]
+
+
 def prior_log_density(d, mu, params):
     """log(gamma + exp(-(d - mu)^2 / (2 sigma^2))) (prior.py:365-370)."""
     z = (np.asarray(d, dtype=np.float64) - np.asarray(mu, dtype=np.float64)) / params.sigma
