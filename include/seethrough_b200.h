@@ -137,6 +137,24 @@ typedef struct {
   double min_bound[2], max_bound[2];
 } st_tri;
 
+/* The two per-triangle tables the reference computes on the host with
+ * LAPACK, recomputed on the device with the same operation order:
+ *  - planes (n_tri,3): np.linalg.solve([u v 1], d) of triangulate
+ *    (prior.py:351-357) -- OpenBLAS dgesv = getf2 (left-looking, pivot
+ *    scaling by the reciprocal, fused dot updates) + trsv (fused axpy,
+ *    division by the diagonal);
+ *  - transform (n_tri,3,2): scipy Delaunay.transform
+ *    (_get_barycentric_transforms) -- getf2 + trsm on the identity
+ *    (reciprocal diagonal); rows of NaN for flat triangles.
+ * Pixel coordinates must be integers of magnitude < 2^24 (support points
+ * and corner anchors are), which makes the scipy condition-number test
+ * exact: flat <=> integer determinant 0.  *flags (device int32, or-ed):
+ * 1 = some plane system hit an exact zero pivot (numpy raises
+ * LinAlgError -> "zero-area triangle").  Reads points/disparities/simplices
+ * of *tri, writes through planes_out / transform_out. */
+int st_tri_tables(const st_tri* tri, double* planes_out, double* transform_out, int32_t* flags,
+                  void* stream);
+
 /* prior.py:276-310 TriangulationPrior.disparity_map -- the containing
  * triangle's plane at every pixel centre, choosing the triangle exactly as
  * scipy's find_simplex walk does for a raster-order batch -- then the

@@ -517,6 +517,164 @@ MuLayout mu_layout(int W, int H, int n_tri) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// per-triangle LAPACK tables (see st_tri_tables in the header)
+
+namespace st {
+
+__global__ void k_tri_tables(const double* __restrict__ pts, const double* __restrict__ disp,
+                             const int32_t* __restrict__ simp, int n_tri,
+                             double* __restrict__ planes, double* __restrict__ transform,
+                             int32_t* __restrict__ flags) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tri) return;
+  int vtx[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) vtx[i] = simp[3 * t + i];
+  // planes: dgesv on A = [u v 1] (rows = vertices), b = d
+  double A[3][3], b[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    A[i][0] = pts[2 * vtx[i]];
+    A[i][1] = pts[2 * vtx[i] + 1];
+    A[i][2] = 1.0;
+    b[i] = disp[vtx[i]];
+  }
+  int piv[3];
+  bool zero_pivot = false;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+#pragma unroll
+    for (int i = 0; i < j; ++i) {  // earlier row interchanges on column j
+      if (piv[i] != i) {
+        const double x = A[i][j];
+        A[i][j] = A[piv[i]][j];
+        A[piv[i]][j] = x;
+      }
+    }
+#pragma unroll
+    for (int i = 1; i < j; ++i) {  // U part: b[i] -= dot(L[i, :i], b[:i])
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) acc = __fma_rn(A[i][k], A[k][j], acc);
+      A[i][j] = dsub(A[i][j], acc);
+    }
+    if (j > 0) {
+#pragma unroll
+      for (int i = j; i < 3; ++i) {  // gemv tail rows: dot, then subtract
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < j; ++k) acc = __fma_rn(A[i][k], A[k][j], acc);
+        A[i][j] = dsub(A[i][j], acc);
+      }
+    }
+    int p = j;  // idamax: first largest magnitude
+#pragma unroll
+    for (int i = j + 1; i < 3; ++i)
+      if (fabs(A[i][j]) > fabs(A[p][j])) p = i;
+    piv[j] = p;
+    if (p != j) {
+#pragma unroll
+      for (int k = 0; k <= j; ++k) {
+        const double x = A[j][k];
+        A[j][k] = A[p][k];
+        A[p][k] = x;
+      }
+    }
+    if (A[j][j] == 0.0) {
+      zero_pivot = true;
+    } else {
+      const double r = ddiv(1.0, A[j][j]);
+#pragma unroll
+      for (int i = j + 1; i < 3; ++i) A[i][j] = dmul(A[i][j], r);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    if (piv[i] != i) {
+      const double x = b[i];
+      b[i] = b[piv[i]];
+      b[piv[i]] = x;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)  // trsv, unit lower
+#pragma unroll
+    for (int k = i + 1; k < 3; ++k) b[k] = __fma_rn(-b[i], A[k][i], b[k]);
+#pragma unroll
+  for (int i = 2; i >= 0; --i) {  // trsv, upper: divide, then axpy
+    b[i] = ddiv(b[i], A[i][i]);
+#pragma unroll
+    for (int k = 0; k < i; ++k) b[k] = __fma_rn(-b[i], A[k][i], b[k]);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) planes[3 * t + i] = b[i];
+  if (zero_pivot) atomicOr(flags, 1);
+
+  // transform: M = T^T, M[j][i] = points[s[j]][i] - points[s[2]][i]
+  const double r0 = pts[2 * vtx[2]], r1 = pts[2 * vtx[2] + 1];
+  double m00 = dsub(pts[2 * vtx[0]], r0), m01 = dsub(pts[2 * vtx[0] + 1], r1);
+  double m10 = dsub(pts[2 * vtx[1]], r0), m11 = dsub(pts[2 * vtx[1] + 1], r1);
+  // integer coordinates: flat <=> exact determinant 0 (scipy: NaN rows)
+  const long long det = (long long)m00 * (long long)m11 - (long long)m10 * (long long)m01;
+  double* T = transform + 6 * t;
+  if (det == 0) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) T[i] = NAN;
+    return;
+  }
+  const bool sw = fabs(m10) > fabs(m00);
+  if (sw) {
+    double x = m00;
+    m00 = m10;
+    m10 = x;
+    x = m01;
+    m01 = m11;
+    m11 = x;
+  }
+  const double l = dmul(m10, ddiv(1.0, m00));
+  const double u11 = dsub(m11, dmul(l, m01));
+  const double iu00 = ddiv(1.0, m00), iu11 = ddiv(1.0, u11);
+  double X[2][2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    double y0 = c == 0 ? 1.0 : 0.0, y1 = c == 1 ? 1.0 : 0.0;
+    if (sw) {
+      const double x = y0;
+      y0 = y1;
+      y1 = x;
+    }
+    y1 = __fma_rn(-y0, l, y1);
+    y1 = dmul(y1, iu11);
+    y0 = __fma_rn(-y1, m01, y0);
+    y0 = dmul(y0, iu00);
+    X[0][c] = y0;
+    X[1][c] = y1;
+  }
+  T[0] = X[0][0];
+  T[1] = X[1][0];
+  T[2] = X[0][1];
+  T[3] = X[1][1];
+  T[4] = r0;
+  T[5] = r1;
+}
+
+}  // namespace st
+
+extern "C" int st_tri_tables(const st_tri* tri, double* planes_out, double* transform_out,
+                             int32_t* flags, void* stream) {
+  if (!tri || tri->n_tri < 0) {
+    sthost::set_error("st_tri_tables: bad triangulation");
+    return ST_EINVAL;
+  }
+  if (tri->n_tri == 0) return ST_OK;
+  st::k_tri_tables<<<(tri->n_tri + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+      tri->points, tri->disparities, tri->simplices, tri->n_tri, planes_out, transform_out,
+      flags);
+  ST_LAUNCH_CHECK("k_tri_tables");
+  return ST_OK;
+}
+
 extern "C" int64_t st_mu_raster_workspace(int32_t W, int32_t H, int32_t n_tri) {
   return (int64_t)mu_layout(W, H, n_tri).total;
 }

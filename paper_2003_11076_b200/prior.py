@@ -77,10 +77,21 @@ class _Staging:
 _STAGING = _Staging()
 
 
+def _integral_coords(points):
+    """Integer pixel coordinates below 2^24 (st_tri_tables' precondition)."""
+    pts = np.asarray(points)
+    return bool(pts.size == 0 or (np.all(np.floor(pts) == pts)
+                                  and np.abs(pts).max() < float(1 << 24)))
+
+
 class TriDevice:
-    """A TriangulationPrior on the device: vertices, planes, the Qhull walk
-    tables `st_mu_raster` replays, and the support list -- packed into one
-    pinned staging buffer and sent with a single asynchronous copy."""
+    """A TriangulationPrior on the device: vertices, the Qhull walk tables
+    `st_mu_raster` replays and the support list, packed into one pinned
+    staging buffer and sent with a single asynchronous copy.  The two LAPACK
+    tables -- planes (prior.py:351-357) and the barycentric transforms -- are
+    recomputed on the device by st_tri_tables with the host libraries'
+    operation order (host tables are only shipped for non-integer vertex
+    coordinates, outside st_tri_tables' exactness precondition)."""
 
     def __init__(self, tri):
         import torch
@@ -88,35 +99,54 @@ class TriDevice:
         dl = delaunay_of(tri)
         sp, sd = tri.support_points()
         sp = np.asarray(sp, dtype=np.float64).reshape(-1, 2)
+        points = np.asarray(tri.points, dtype=np.float64).reshape(-1, 2)
+        self.device_tables = _integral_coords(points)
+        n_tri = int(np.asarray(tri.triangles).shape[0])
         parts = [
-            ("points", np.asarray(tri.points, dtype=np.float64).reshape(-1, 2)),
+            ("points", points),
             ("disparities", np.asarray(tri.disparities, dtype=np.float64).reshape(-1)),
             ("triangles", np.asarray(tri.triangles, dtype=np.int32).reshape(-1, 3)),
-            ("planes", np.asarray(tri.planes, dtype=np.float64).reshape(-1, 3)),
             ("neighbors", np.asarray(dl.neighbors, dtype=np.int32).reshape(-1, 3)),
-            ("transform", np.asarray(dl.transform, dtype=np.float64).reshape(-1, 3, 2)),
             ("equations", np.asarray(dl.equations, dtype=np.float64).reshape(-1, 4)),
             ("sup_uv", sp),
             ("sup_d", np.asarray(sd, dtype=np.float64).reshape(-1)),
         ]
+        if not self.device_tables:
+            parts += [("planes", np.asarray(tri.planes, dtype=np.float64).reshape(-1, 3)),
+                      ("transform", np.asarray(dl.transform, dtype=np.float64).reshape(-1, 3, 2))]
         offs, total = [], 0
         for _, a in parts:
             offs.append(total)
             total += (a.nbytes + 255) & ~255
+        dev_total = total
+        if self.device_tables:  # device-only tail: planes, transform, flags
+            t_planes = dev_total
+            dev_total += (n_tri * 24 + 255) & ~255
+            t_transform = dev_total
+            dev_total += (n_tri * 48 + 255) & ~255
+            t_flags = dev_total
+            dev_total += 256
         i, stage = _STAGING.take(total)
         host = stage.numpy()
         for (_, a), o in zip(parts, offs):
             np.copyto(host[o:o + a.nbytes].view(a.dtype).reshape(a.shape), a)
-        self.buffer = torch.empty(max(total, 1), dtype=torch.uint8, device=dev())
+        self.buffer = torch.empty(max(dev_total, 1), dtype=torch.uint8, device=dev())
         self.buffer[:total].copy_(stage[:total], non_blocking=True)
         _STAGING.mark(i)
         tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32}
         for (name, a), o in zip(parts, offs):
             view = self.buffer[o:o + a.nbytes].view(tdt[a.dtype]).reshape(a.shape)
             setattr(self, name, view if a.size else None)
-        self.n_pts = parts[0][1].shape[0]
-        self.n_tri = parts[2][1].shape[0]
+        self.n_pts = points.shape[0]
+        self.n_tri = n_tri
         self.n_sup = int(sp.shape[0])
+        if self.device_tables:
+            self.planes = self.buffer[t_planes:t_planes + n_tri * 24].view(torch.float64)
+            self.transform = self.buffer[t_transform:t_transform + n_tri * 48].view(torch.float64)
+            self.flags = self.buffer[t_flags:t_flags + 4].view(torch.int32)
+            self.flags.zero_()
+        else:
+            self.flags = None
         s = N.StTri()
         s.points, s.disparities = self.points.data_ptr(), self.disparities.data_ptr()
         s.simplices, s.planes = self.triangles.data_ptr(), self.planes.data_ptr()
@@ -125,14 +155,23 @@ class TriDevice:
         s.n_pts, s.n_tri = self.n_pts, self.n_tri
         s.paraboloid_scale = float(dl.paraboloid_scale)
         s.paraboloid_shift = float(dl.paraboloid_shift)
-        for i in range(2):
-            s.min_bound[i] = float(dl.min_bound[i])
-            s.max_bound[i] = float(dl.max_bound[i])
+        for k in range(2):
+            s.min_bound[k] = float(dl.min_bound[k])
+            s.max_bound[k] = float(dl.max_bound[k])
         self.st = s
+        if self.device_tables:
+            N.invoke("st_tri_tables", s, self.planes, self.transform, self.flags)
+
+    def check(self):
+        """Raise the reference's triangulate error if a plane system was
+        singular (numpy LinAlgError at prior.py:355-357).  Synchronises."""
+        if self.flags is not None and int(self.flags.item()) & 1:
+            raise ValueError("degenerate support set: zero-area triangle")
 
     @property
     def nbytes(self):
-        return self.n_pts * 24 + self.n_tri * (12 + 24 + 12 + 48 + 32) + self.n_sup * 24
+        return self.n_pts * 24 + self.n_tri * (12 + 12 + 32) + self.n_sup * 24 + (
+            0 if self.device_tables else self.n_tri * 72)
 
     def tensors(self):
         return [self.buffer]
@@ -199,11 +238,23 @@ def triangulate(points, width, height):
 
     Upstream stage, host side (scipy Qhull), kept API-compatible.
     """
-    from scipy.spatial import Delaunay, QhullError, cKDTree
     if not points:
         raise ValueError("degenerate support set: no support points")
-    coords = np.array([[p.u, p.v] for p in points], dtype=np.float64)
-    disps = np.array([p.d for p in points], dtype=np.float64)
+    return triangulate_arrays([p.u for p in points], [p.v for p in points],
+                              [p.d for p in points], width, height)
+
+
+def triangulate_arrays(u, v, d, width, height, planes=True):
+    """triangulate over (u, v, d) arrays (same arithmetic as prior.py:318-360).
+
+    planes=False skips the host plane solve (TriDevice recomputes the planes
+    on the device; .planes is then None and a zero-area triangle surfaces
+    through TriDevice.check)."""
+    from scipy.spatial import Delaunay, QhullError, cKDTree
+    if len(u) == 0:
+        raise ValueError("degenerate support set: no support points")
+    coords = np.stack([np.asarray(u, dtype=np.float64), np.asarray(v, dtype=np.float64)], axis=1)
+    disps = np.asarray(d, dtype=np.float64).copy()
     corners = np.array([[0.0, 0.0], [width - 1.0, 0.0], [0.0, height - 1.0],
                         [width - 1.0, height - 1.0]])
     taken = {(int(c[0]), int(c[1])) for c in coords}
@@ -219,6 +270,9 @@ def triangulate(points, width, height):
     except QhullError as exc:
         raise ValueError(f"degenerate support set: {exc}") from None
     tris = dl.simplices.astype(np.int32)
+    if not planes:
+        return TriangulationPrior(points=coords, disparities=disps, triangles=tris, planes=None,
+                                  num_anchors=n_anchor, _lookup=dl)
     verts = coords[tris]
     mats = np.concatenate([verts, np.ones((verts.shape[0], 3, 1))], axis=2)
     try:

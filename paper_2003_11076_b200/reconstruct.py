@@ -71,6 +71,7 @@ class FramePipeline:
     def load(self, images, priors):
         """Copy a frame into the input buffers (async DMA when the host side is pinned)."""
         t = self.t
+        self._desc_ready = False
         for dst, src, dt in ((self.images, images, np.uint8), (self.priors, priors, np.float32)):
             if isinstance(src, t.Tensor):
                 dst.copy_(src, non_blocking=True)
@@ -83,9 +84,49 @@ class FramePipeline:
 
     # -- the frame --------------------------------------------------------------------
 
+    def harvest(self, threshold=None, stride=None, min_texture=None):
+        """Descriptors + the device support harvest of the loaded frame
+        (st_harvest, prior.py:233-259 before deduplicate).  Enqueued on the
+        current stream; returns (u, v, d, src, count) device tensors."""
+        from .prior import MIN_TEXTURE, SUPPORT_STRIDE, _grid_len
+        t = self.t
+        K, H, W = self.K, self.H, self.W
+        thr = self.params.threshold if threshold is None else threshold
+        stride = SUPPORT_STRIDE if stride is None else int(stride)
+        mt = MIN_TEXTURE if min_texture is None else float(min_texture)
+        if getattr(self, "_hv_key", None) != stride:
+            lib = N.lib()
+            cap = max(int(lib.st_harvest_capacity(K, W, H, stride)), 1)
+            self.hv_ws = empty((max(int(lib.st_harvest_workspace(K, W, H, stride)), 1),),
+                               t.uint8)
+            self.hv_u = empty((cap,), t.int32)
+            self.hv_v = empty((cap,), t.int32)
+            self.hv_d = empty((cap,), t.float64)
+            self.hv_src = empty((cap,), t.int32)
+            self.hv_n = empty((1,), t.int64)
+            self.cams = N.make_cams(self.rig_obj, W, H)
+            self._hv_key = stride
+        N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
+        self._desc_ready = True
+        N.invoke("st_harvest", self.desc, self.priors, self.cams, float(self.prior_params.d_max),
+                 _grid_len(self.prior_params.d_max), float(thr), stride, mt, self.hv_u,
+                 self.hv_v, self.hv_d, self.hv_src, self.hv_n, self.hv_ws, self.hv_ws.numel())
+        return self.hv_u, self.hv_v, self.hv_d, self.hv_src, self.hv_n
+
+    def harvest_host(self, **kw):
+        """harvest() + D2H + native dedup -> host (u, v, d, src) in the
+        reference's final support order (prior.py:183-212)."""
+        from .prior import deduplicate_arrays
+        u, v, d, s, n = self.harvest(**kw)
+        cnt = int(n.item())
+        u, v, d, s = (download(x[:cnt]) for x in (u, v, d, s))
+        keep = deduplicate_arrays(u, v, d, s, self.rig_obj.ref_index, self.W, self.H)
+        return u[keep], v[keep], d[keep], s[keep]
+
     def run(self, tri_dev, dynamic_only=False, forced_iters=0, median_radius=1, timing=False,
             reduce=None):
-        """Descriptors, mu, support lists, EM, refocus + median for the loaded frame."""
+        """Descriptors, mu, support lists, EM, refocus + median for the loaded frame
+        (descriptors are reused when harvest() already computed them)."""
         p = N.make_params(self.params, self.prior_params, forced_iters, timing)
         K, H, W = self.K, self.H, self.W
         t = self.t
@@ -107,7 +148,9 @@ class FramePipeline:
             N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max), self.mu,
                      self.mu_ws, self.mu_ws.numel())
             mu_done = self._event(timing=timing)
-        N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
+        if not getattr(self, "_desc_ready", False):
+            N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
+        self._desc_ready = False
         mark()
         need = int(N.lib().st_support_workspace(tri_dev.n_sup, W, H,
                                                 float(self.prior_params.neighborhood_radius)))
@@ -317,3 +360,44 @@ def reconstruct(frame, rig, tri, params=None, prior_params=None, dynamic_only=Fa
         segmentation=SegmentationState(static_bits=sbits.view(np.uint32),
                                        valid_bits=vbits.view(np.uint32)),
         stats=stats, image=img, provenance=prov, n_rays=nr)
+
+
+def reconstruct_frame(frame, rig, params=None, prior_params=None, dynamic_only=False,
+                      median_radius=1, forced_iters=0, timings=None):
+    """The reference pipeline's compute stages from a raw frame
+    (pipeline.py:233-261): collect_support (device harvest + native dedup),
+    triangulate (host Qhull, like the reference), em_solve + synthesize
+    (device).  Returns (Reconstruction, TriangulationPrior).  `timings`
+    (optional dict) receives host wall-clock seconds per stage."""
+    import time
+
+    from .prior import triangulate_arrays
+    t = require_cuda()
+    params = params or SolverParams()
+    prior_params = prior_params or PriorParams()
+    if frame.num_views != len(rig):
+        raise ValueError("frame view count does not match the rig")
+    h, w = frame.shape
+    pipe = _pipeline_for(rig, w, h, params, prior_params)
+    clock = time.perf_counter
+    t0 = clock()
+    pipe.load(frame.images, frame.priors)
+    u, v, d, _ = pipe.harvest_host()
+    t1 = clock()
+    tri = triangulate_arrays(u, v, d, w, h, planes=False)
+    t2 = clock()
+    td = TriDevice(tri)
+    stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
+                     median_radius=median_radius)
+    values, status, sbits, vbits, img, prov, nr = pipe.fetch()
+    td.check()  # the planes were solved on the device: surface numpy's error here
+    t3 = clock()
+    if timings is not None:
+        timings.update(support=t1 - t0, triangulate=t2 - t1, solve_refocus=t3 - t2)
+    del t
+    rec = Reconstruction(
+        disparity=DisparityMap(values=values, status=status),
+        segmentation=SegmentationState(static_bits=sbits.view(np.uint32),
+                                       valid_bits=vbits.view(np.uint32)),
+        stats=stats, image=img, provenance=prov, n_rays=nr)
+    return rec, tri
