@@ -269,6 +269,15 @@ int st_masked_variance(const double* desc, const uint8_t* mask, int64_t n, int32
 
 /* ---- the fused solve (solver.py:436-508) ------------------------------ */
 
+/* st_solve for a dense single-device solve (dynamic_only = 0, no active
+ * mask, no shard reduction, no timing) without any host synchronisation:
+ * the convergence test of solver.py:483-485 and the EM statistics run on
+ * the device, kernels of the iterations after convergence exit at once, and
+ * the statistics land in *stats_dev (device or pinned-mapped memory) when
+ * the stream reaches that point.  Same results as st_solve. */
+int st_solve_async(const st_frame* frame, const st_rig* rig, const st_params* params,
+                   float* values, uint8_t* status, uint32_t* static_bits, uint32_t* valid_bits,
+                   st_stats* stats_dev, void* workspace, int64_t workspace_bytes, void* stream);
 int64_t st_solve_workspace(int32_t W, int32_t H, int32_t K);
 
 /* Full EM: initial masks, M/E alternation with the reference's global

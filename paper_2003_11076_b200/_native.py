@@ -88,6 +88,8 @@ _SIGS = {
     "st_support_build": (C.c_int, [_P, _P, _I32, _I32, _I32, C.POINTER(StParams),
                                    C.POINTER(StFrame), _P, _I64, C.POINTER(C.c_int64), _P]),
     "st_support_workspace": (C.c_int64, [_I32, _I32, _I32, _D]),
+    "st_solve_async": (C.c_int, [C.POINTER(StFrame), C.POINTER(StRig), C.POINTER(StParams),
+                                 _P, _P, _P, _P, _P, _P, _I64, _P]),
     "st_tri_tables": (C.c_int, [C.POINTER(StTri), _P, _P, _P, _P]),
     "st_harvest": (C.c_int, [_P, _P, C.POINTER(StCams), _D, _I32, C.c_float, _I32, _D,
                              _P, _P, _P, _P, _P, _P, _I64, _P]),

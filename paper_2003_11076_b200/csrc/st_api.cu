@@ -438,7 +438,7 @@ static SolveLayout solve_layout(int W, int H) {
   L.mask_in = o;  o += align_up(sizeof(uint32_t) * npx);
   L.mlist = o;    o += align_up(sizeof(int32_t) * npx);
   L.elist = o;    o += align_up(sizeof(int32_t) * npx);
-  L.counts = o;   o += align_up(sizeof(uint32_t) * 2);
+  L.counts = o;   o += align_up(sizeof(uint32_t) * 4);  // 2 worklist counts + stop flag
   L.active = o;   o += align_up(sizeof(int64_t) * npx);
   L.flags = o;    o += align_up(sizeof(uint32_t) * (npx + 1));
   L.offs = o;     o += align_up(sizeof(uint32_t) * (npx + 1));
@@ -652,6 +652,109 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       ST_LAUNCH_CHECK("k_pack_outputs");
     }
   }
+  return ST_OK;
+}
+
+// st_solve for a dense solve on one device with no host synchronisation: the
+// convergence test (solver.py:483-485) and the statistics run on the device
+// (k_solve_control), and every kernel of the iterations after convergence
+// exits at once on the device stop flag.  Results are identical to st_solve.
+int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, float* values,
+                   uint8_t* status, uint32_t* static_bits, uint32_t* valid_bits,
+                   st_stats* stats_dev, void* workspace, int64_t workspace_bytes,
+                   void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  st::EmCtx c;
+  int rc = make_ctx(f, rig, p, c);
+  if (rc) return rc;
+  if ((rc = prepare_estep_kernels())) return rc;
+  const int W = c.W, H = c.H;
+  const int64_t npx = c.HW;
+  const SolveLayout L = solve_layout(W, H);
+  if ((int64_t)L.total > workspace_bytes) {
+    sthost::set_error("solve workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                      (long long)L.total);
+    return ST_ENOMEM;
+  }
+  if (!stats_dev) {
+    sthost::set_error("st_solve_async: stats_dev is required");
+    return ST_EINVAL;
+  }
+  char* ws = (char*)workspace;
+  double* d_act = (double*)(ws + L.d);
+  double* e_act = (double*)(ws + L.e);
+  double* pe_act = (double*)(ws + L.pe);
+  uint8_t* st_act = (uint8_t*)(ws + L.st_act);
+  uint8_t* chg = (uint8_t*)(ws + L.chg);
+  uint32_t* mask_in = (uint32_t*)(ws + L.mask_in);
+  int32_t* mlist = (int32_t*)(ws + L.mlist);
+  int32_t* elist = (int32_t*)(ws + L.elist);
+  uint32_t* counts = (uint32_t*)(ws + L.counts);
+  int* stop = (int*)(counts + 2);
+  st::Partial* work = (st::Partial*)(ws + L.work);
+  st::Partial* parts = (st::Partial*)(ws + L.parts);
+  st::Partial* reduced = (st::Partial*)(ws + L.reduced);
+
+  ST_CUDA_CHECK(cudaMemsetAsync(stats_dev, 0, sizeof(st_stats), s));
+  ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t) + sizeof(int), s));
+  st::k_stats_init<<<1, 32, 0, s>>>(stats_dev, npx);
+  ST_LAUNCH_CHECK("k_stats_init");
+  st::k_initial_masks<<<blocks_for(npx, 128), 128, 0, s>>>(c, nullptr, npx, static_bits,
+                                                           valid_bits);
+  ST_LAUNCH_CHECK("k_initial_masks");
+
+  const int iters = std::min(p->forced_iters > 0 ? p->forced_iters : p->max_iters, 64);
+  const int nblk = (int)blocks_for(npx, EM_BLOCK);
+  const int nwarps = nblk * (EM_BLOCK / 32);
+  const int sblk = (int)blocks_for(npx, STATS_BLOCK);
+  for (int it = 1; it <= iters; ++it) {
+    if (it > 1) {
+      st::k_flag_mstep<<<nblk, EM_BLOCK, 0, s>>>(nullptr, npx, static_bits, mask_in, e_act,
+                                                 pe_act, chg, mlist, counts, stop);
+      ST_LAUNCH_CHECK("k_flag_mstep");
+    }
+    st::MStepArgs a = {};
+    a.n = npx;
+    a.list = it > 1 ? mlist : nullptr;
+    a.list_count = counts;
+    a.static_all = static_bits;
+    a.first = it == 1;
+    a.d = d_act;
+    a.e = e_act;
+    a.status = st_act;
+    a.mask_in = mask_in;
+    a.pe = pe_act;
+    a.chg = chg;
+    a.elist = elist;
+    a.elist_count = counts + 1;
+    a.partials = work;
+    a.stop = stop;
+    st::k_m_step<<<nblk, EM_BLOCK, 0, s>>>(c, a);
+    ST_LAUNCH_CHECK("k_m_step");
+    st::EStepArgs e = {};
+    e.n = npx;
+    e.list = elist;
+    e.list_count = counts + 1;
+    e.d = d_act;
+    e.status = st_act;
+    e.static_out = static_bits;
+    e.valid_out = valid_bits;
+    e.scatter = 1;
+    e.stop = stop;
+    launch_e_step(rig->num_views, npx, s, c, e);
+    ST_LAUNCH_CHECK("k_e_step_at");
+    st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(npx, it > 1, e_act, pe_act, chg, work, nwarps,
+                                                parts, stop);
+    ST_LAUNCH_CHECK("k_em_stats");
+    st::k_reduce_partials<<<1, 256, 0, s>>>(parts, sblk, reduced + it, stop);
+    ST_LAUNCH_CHECK("k_reduce_partials");
+    st::k_solve_control<<<1, 32, 0, s>>>(it, reduced, counts, npx, p->forced_iters, stats_dev,
+                                         stop);
+    ST_LAUNCH_CHECK("k_solve_control");
+  }
+  st::k_pack_outputs<<<blocks_for(npx, 256), 256, 0, s>>>(f->mu, npx, nullptr, npx, d_act,
+                                                          st_act, values, status, 1);
+  ST_LAUNCH_CHECK("k_pack_outputs");
   return ST_OK;
 }
 

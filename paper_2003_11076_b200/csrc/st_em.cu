@@ -148,6 +148,7 @@ __device__ __forceinline__ void list_append(bool want, int32_t slot, int32_t* li
 // function of (pixel, d)).
 
 __global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
+  if (a.stop && *a.stop) return;  // converged (st_solve_async)
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
   const bool live = t < n_work;
@@ -247,7 +248,9 @@ __global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n,
                              const uint32_t* __restrict__ static_all,
                              const uint32_t* __restrict__ mask_in, const double* __restrict__ e,
                              double* __restrict__ pe, uint8_t* __restrict__ chg,
-                             int32_t* __restrict__ list, uint32_t* __restrict__ count) {
+                             int32_t* __restrict__ list, uint32_t* __restrict__ count,
+                             const int* stop) {
+  if (stop && *stop) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool want = false;
   if (i < n) {
@@ -267,7 +270,8 @@ __global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n,
 __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ e,
                            const double* __restrict__ pe, const uint8_t* __restrict__ chg,
                            const Partial* __restrict__ work, int n_work_parts,
-                           Partial* __restrict__ parts) {
+                           Partial* __restrict__ parts, const int* stop) {
+  if (stop && *stop) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double se = 0.0, spe = 0.0;
   long long nf = 0, npf = 0, nch = 0;
@@ -657,6 +661,7 @@ __device__ __forceinline__ void desc_word(const uint32_t* __restrict__ plane, in
 // rectified rig, vertical weight identically 0.
 template <int KT, bool RECT>
 __global__ void __launch_bounds__(ESTEP_TAPS_BLOCK) k_e_step_taps(EmCtx c, EStepArgs a) {
+  if (a.stop && *a.stop) return;  // converged (st_solve_async)
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
   if (t >= n_work) return;
@@ -711,6 +716,7 @@ template __global__ void k_e_step_taps<5, true>(EmCtx, EStepArgs);
 // enumerated one at a time (estep_generic).
 __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a) {
   extern __shared__ double sh_f[];
+  if (a.stop && *a.stop) return;  // converged (st_solve_async)
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
   if (t >= n_work) return;
@@ -916,8 +922,9 @@ __global__ void k_fill_mu(const double* __restrict__ mu, int64_t npx, float* __r
 
 // Fixed-order sum of the per-block partials into slot `it` of the stats.
 __global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
-                                  Partial* __restrict__ out) {
+                                  Partial* __restrict__ out, const int* stop) {
   __shared__ double sd[2][256];
+  if (stop && *stop) return;
   __shared__ long long si[5][256];
   double a = 0.0, b = 0.0;
   long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
@@ -970,6 +977,44 @@ __global__ void k_scatter_active(const uint32_t* __restrict__ flags,
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npx) return;
   if (flags[i]) active[offs[i]] = i;
+}
+
+__global__ void k_stats_init(st_stats* stats, int64_t n_act) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    stats->converged_after = -1;
+    stats->active_pixels = n_act;
+    stats->kernel_launches[2] = 1;  // k_initial_masks
+  }
+}
+
+__global__ void k_solve_control(int it, const Partial* __restrict__ reduced,
+                                uint32_t* __restrict__ counts, int64_t n_act, int forced_iters,
+                                st_stats* __restrict__ stats, int* __restrict__ stop) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || *stop) return;
+  const Partial r = reduced[it];
+  stats->iterations_run = it;
+  stats->msteps += it > 1 ? (int64_t)counts[0] : n_act;
+  stats->esteps += counts[1];
+  if (it > 1) stats->prev_evals += counts[0];
+  stats->kernel_launches[0] += 1;
+  stats->kernel_launches[1] += 1;
+  stats->kernel_launches[3] += it > 1 ? 3 : 2;
+  const double nf = (double)r.n_fin;
+  stats->mean_energy[it - 1] = nf > 0 ? r.sum_e / nf : NAN;
+  stats->candidates_total += r.n_cand;
+  stats->energy_evals += r.n_eval;
+  if (it > 1) {
+    const double npf = (double)r.n_pfin;
+    stats->prev_energy[it - 2] = npf > 0 ? r.sum_pe / npf : NAN;
+    const double changed = (double)r.n_changed / (double)n_act;
+    stats->changed_fraction[it - 2] = changed;
+    if (forced_iters <= 0 && changed < 1e-3) {  // solver.py:483-485
+      stats->converged_after = it - 1;
+      *stop = 1;
+    }
+  }
+  counts[0] = 0;  // next iteration's worklists
+  counts[1] = 0;
 }
 
 }  // namespace st

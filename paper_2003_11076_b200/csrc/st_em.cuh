@@ -61,6 +61,7 @@ struct MStepArgs {
   int32_t* elist;              // nullable: E-step worklist (append)
   uint32_t* elist_count;
   Partial* partials;           // nullable: per-warp work counters
+  const int* stop;             // nullable: device flag, set -> the launch does nothing
 };
 
 struct EStepArgs {
@@ -74,15 +75,16 @@ struct EStepArgs {
   uint32_t* valid_out;
   int scatter;               // 1: write at pixel index, 0: at row i
   int exhaustive;            // 1: score every mask in fp64 (no fp32 screen)
+  const int* stop;           // nullable: device flag, set -> the launch does nothing
 };
 
 __global__ void k_m_step(EmCtx c, MStepArgs a);
 __global__ void k_flag_mstep(const int64_t* active, int64_t n, const uint32_t* static_all,
                              const uint32_t* mask_in, const double* e, double* pe, uint8_t* chg,
-                             int32_t* list, uint32_t* count);
+                             int32_t* list, uint32_t* count, const int* stop = nullptr);
 __global__ void k_em_stats(int64_t n, int with_prev, const double* e, const double* pe,
                            const uint8_t* chg, const Partial* work, int n_work_parts,
-                           Partial* parts);
+                           Partial* parts, const int* stop = nullptr);
 template <int KT, bool RECT>
 __global__ void k_e_step_taps(EmCtx c, EStepArgs a);
 __global__ void k_e_step_at(EmCtx c, EStepArgs a);
@@ -100,7 +102,14 @@ __global__ void k_pack_outputs(const double* mu, int64_t npx, const int64_t* act
                                int64_t n_active, const double* d_act, const uint8_t* st_act,
                                float* values, uint8_t* status, int dense);
 __global__ void k_fill_mu(const double* mu, int64_t npx, float* values, uint8_t* status);
-__global__ void k_reduce_partials(const Partial* parts, int nparts, Partial* out);
+__global__ void k_reduce_partials(const Partial* parts, int nparts, Partial* out,
+                                  const int* stop = nullptr);
+// Device-side EM control for st_solve_async (solver.py:463-485): folds the
+// iteration's reduced partials and worklist counts into *stats, sets *stop
+// on convergence, and clears the worklist counts for the next iteration.
+__global__ void k_solve_control(int it, const Partial* reduced, uint32_t* counts, int64_t n_act,
+                                int forced_iters, st_stats* stats, int* stop);
+__global__ void k_stats_init(st_stats* stats, int64_t n_act);
 __global__ void k_flag_active(const float* ref_prior, const uint8_t* mask, int64_t npx,
                               double threshold, uint32_t* flags);
 __global__ void k_scatter_active(const uint32_t* flags, const uint32_t* offs, int64_t npx,

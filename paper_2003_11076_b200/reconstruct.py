@@ -19,6 +19,19 @@ from .solver import (DisparityMap, EMStats, SegmentationState, SolverParams, _ch
                      _stats_of)
 
 
+class AsyncStats:
+    """EM statistics still on the device (st_solve_async): resolved from the
+    raw st_stats bytes that FramePipeline.fetch_async brings back."""
+
+    def __init__(self, support_records):
+        self.support_records = support_records
+
+    def resolve(self, raw):
+        s = N.StStats.from_buffer_copy(raw.tobytes())
+        s.support_records = self.support_records
+        return _stats_of(s)
+
+
 @dataclass
 class Reconstruction:
     disparity: DisparityMap
@@ -59,6 +72,7 @@ class FramePipeline:
         self.n_rays = empty((H, W), t.uint8)
         self.scratch = empty((H, W, 3), t.uint8)
         self.copy = empty((H, W), t.uint8)
+        self.stats_dev = empty((N.C.sizeof(N.StStats),), t.uint8)
         self.frame = N.StFrame()
         self.frame.images = self.images.data_ptr()
         self.frame.priors = self.priors.data_ptr()
@@ -163,10 +177,18 @@ class FramePipeline:
         main.wait_event(mu_done)
         mark()
         stats = N.StStats()
-        cb = N.REDUCE_FN(reduce) if reduce is not None else N.REDUCE_FN()
-        N.invoke("st_solve", self.frame, self.rig, p, int(bool(dynamic_only)), None,
-                 self.values, self.status, self.sbits, self.vbits, stats, self.solve_ws,
-                 self.solve_ws.numel(), cb, None)
+        # no host round trip inside the solve unless a shard reduction, an
+        # active subset or per-stage timing needs one
+        run_async = not dynamic_only and reduce is None and not timing
+        if run_async:
+            N.invoke("st_solve_async", self.frame, self.rig, p, self.values, self.status,
+                     self.sbits, self.vbits, self.stats_dev, self.solve_ws,
+                     self.solve_ws.numel())
+        else:
+            cb = N.REDUCE_FN(reduce) if reduce is not None else N.REDUCE_FN()
+            N.invoke("st_solve", self.frame, self.rig, p, int(bool(dynamic_only)), None,
+                     self.values, self.status, self.sbits, self.vbits, stats, self.solve_ws,
+                     self.solve_ws.numel(), cb, None)
         mark()
         stats.support_records = rec.value
         copy = None
@@ -179,6 +201,8 @@ class FramePipeline:
                  int(self.params.min_static_rays), int(median_radius), copy, self.image,
                  self.prov, self.n_rays, self.scratch)
         mark()
+        if run_async:
+            return AsyncStats(rec.value)
         out = _stats_of(stats)
         if timing:
             marks[-1].synchronize()
@@ -210,7 +234,7 @@ class FramePipeline:
         outs = []
         with t.cuda.stream(stream):
             for d in (self.values, self.status, self.sbits, self.vbits, self.image, self.prov,
-                      self.n_rays):
+                      self.n_rays, self.stats_dev):
                 h = t.empty(d.shape, dtype=d.dtype, pin_memory=True)
                 h.copy_(d, non_blocking=True)
                 outs.append(h)
@@ -218,7 +242,9 @@ class FramePipeline:
 
 
 def _outputs_of(pipe, stats, host):
-    values, status, sbits, vbits, img, prov, nr = host
+    values, status, sbits, vbits, img, prov, nr, raw_stats = host
+    if isinstance(stats, AsyncStats):
+        stats = stats.resolve(raw_stats)
     return Reconstruction(
         disparity=DisparityMap(values=values, status=status),
         segmentation=SegmentationState(static_bits=sbits.view(np.uint32),
@@ -258,24 +284,39 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
 
     device = t.cuda.current_device()
 
+    import os
+    import time
+    prof = {} if os.environ.get("ST_STREAM_PROFILE") else None
+
+    def tick(key, t0):
+        if prof is not None:
+            prof[key] = prof.get(key, 0.0) + time.perf_counter() - t0
+        return time.perf_counter()
+
     def prep():
         t.cuda.set_device(device)
         try:
             for i, (frame, tri) in enumerate(_chain(first, it)):
+                t0 = time.perf_counter()
                 pipe = pipes[i % 2]
                 with free_lock:
                     while i >= 2 and free[i % 2] is None:
                         free_lock.wait()
                     ev = free[i % 2]
                     free[i % 2] = None
+                t0 = tick("prep_wait_free", t0)
                 with t.cuda.stream(copy_s):
                     if ev is not None:
                         copy_s.wait_event(ev)
                     pipe.load(frame.images, frame.priors)
+                    t0 = tick("prep_load", t0)
                     td = TriDevice(tri)
+                    t0 = tick("prep_tridevice", t0)
                     loaded = t.cuda.Event()
                     loaded.record(copy_s)
-                q.put((pipe, td, loaded))
+                # planes solved on the device only: numpy's singular-system
+                # error is checked when the frame's outputs arrive
+                q.put((pipe, td, loaded, tri.planes is None))
         except Exception as exc:  # noqa: BLE001 -- surfaced in the consumer
             error.append(exc)
         q.put(None)
@@ -285,36 +326,104 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
     pending = None
     i = 0
     while True:
+        t0 = time.perf_counter()
         item = q.get()
         if item is None:
             break
-        pipe, td, loaded = item
+        t0 = tick("main_wait_prep", t0)
+        pipe, td, loaded, check = item
         main.wait_event(loaded)
         for x in td.tensors():
             x.record_stream(main)
         stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
                          median_radius=median_radius)
+        t0 = tick("main_run", t0)
         done = t.cuda.Event()
         done.record(main)
         with t.cuda.stream(out_s):
             out_s.wait_event(done)
             host = pipe.fetch_async(out_s)
+            flags = None
+            if check and td.flags is not None:
+                flags = t.empty((1,), dtype=t.int32, pin_memory=True)
+                flags.copy_(td.flags, non_blocking=True)
             fetched = t.cuda.Event()
             fetched.record(out_s)
         with free_lock:
             free[i % 2] = fetched
             free_lock.notify_all()
+        t0 = tick("main_fetch_enqueue", t0)
         if pending is not None:
-            pending[2].synchronize()
-            yield _outputs_of(*pending[:2], pending[3])
-        pending = (pipe, stats, fetched, host)
+            out = _finish(pending)
+            t0 = tick("main_finish_prev", t0)
+            yield out
+            t0 = time.perf_counter()
+        pending = (pipe, stats, fetched, host, flags)
         i += 1
     worker.join()
+    if prof is not None:
+        print("reconstruct_stream profile (s, summed over frames):",
+              {k: round(v, 4) for k, v in sorted(prof.items())}, f"frames={i}", flush=True)
     if error:
         raise error[0]
     if pending is not None:
-        pending[2].synchronize()
-        yield _outputs_of(*pending[:2], pending[3])
+        yield _finish(pending)
+
+
+def _finish(pending):
+    pipe, stats, fetched, host, flags = pending
+    fetched.synchronize()
+    if flags is not None and int(flags[0]) & 1:
+        raise ValueError("degenerate support set: zero-area triangle")
+    return _outputs_of(pipe, stats, host)
+
+
+def reconstruct_frames(frames, rig, params=None, prior_params=None, dynamic_only=False,
+                       median_radius=1, forced_iters=0, workers=None, inflight=None):
+    """The reference pipeline's compute stages (pipeline.py:233-261) over a
+    stream of raw frames: device harvest + native dedup per frame on a side
+    stream, host Qhull in a process pool (several frames in flight), then
+    the pipelined device solve + refocus of reconstruct_stream.  Yields one
+    Reconstruction per frame, in order."""
+    from collections import deque
+
+    from .qhull_pool import delaunay_tables, make_pool, prior_of
+    t = require_cuda()
+    params = params or SolverParams()
+    prior_params = prior_params or PriorParams()
+
+    def triangulated():
+        it = iter(frames)
+        first = next(it, None)
+        if first is None:
+            return
+        h, w = first.shape
+        hp = FramePipeline(rig, w, h, params, prior_params)
+        hs = t.cuda.Stream()
+        pool, n = make_pool(workers)
+        depth = inflight or n + 2
+        q = deque()
+        try:
+            for frame in _chain(first, it):
+                if frame.num_views != len(rig):
+                    raise ValueError("frame view count does not match the rig")
+                with t.cuda.stream(hs):
+                    hp.load(frame.images, frame.priors)
+                    u, v, d, _ = hp.harvest_host()
+                q.append((frame, pool.submit(delaunay_tables, u, v, d, w, h)))
+                if len(q) >= depth:
+                    f0, fut = q.popleft()
+                    yield f0, prior_of(fut.result())
+            while q:
+                f0, fut = q.popleft()
+                yield f0, prior_of(fut.result())
+        finally:
+            for _, fut in q:
+                fut.cancel()
+
+    yield from reconstruct_stream(triangulated(), rig, params, prior_params,
+                                  dynamic_only=dynamic_only, median_radius=median_radius,
+                                  forced_iters=forced_iters)
 
 
 def _chain(first, rest):
@@ -354,12 +463,7 @@ def reconstruct(frame, rig, tri, params=None, prior_params=None, dynamic_only=Fa
     pipe.load(frame.images, frame.priors)
     stats = pipe.run(TriDevice(tri), dynamic_only=dynamic_only, forced_iters=forced_iters,
                      median_radius=median_radius)
-    values, status, sbits, vbits, img, prov, nr = pipe.fetch()
-    return Reconstruction(
-        disparity=DisparityMap(values=values, status=status),
-        segmentation=SegmentationState(static_bits=sbits.view(np.uint32),
-                                       valid_bits=vbits.view(np.uint32)),
-        stats=stats, image=img, provenance=prov, n_rays=nr)
+    return _outputs_of(pipe, stats, pipe.fetch())
 
 
 def reconstruct_frame(frame, rig, params=None, prior_params=None, dynamic_only=False,
@@ -389,15 +493,10 @@ def reconstruct_frame(frame, rig, params=None, prior_params=None, dynamic_only=F
     td = TriDevice(tri)
     stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
                      median_radius=median_radius)
-    values, status, sbits, vbits, img, prov, nr = pipe.fetch()
+    rec = _outputs_of(pipe, stats, pipe.fetch())
     td.check()  # the planes were solved on the device: surface numpy's error here
     t3 = clock()
     if timings is not None:
         timings.update(support=t1 - t0, triangulate=t2 - t1, solve_refocus=t3 - t2)
     del t
-    rec = Reconstruction(
-        disparity=DisparityMap(values=values, status=status),
-        segmentation=SegmentationState(static_bits=sbits.view(np.uint32),
-                                       valid_bits=vbits.view(np.uint32)),
-        stats=stats, image=img, provenance=prov, n_rays=nr)
     return rec, tri

@@ -104,3 +104,30 @@ def test_screened_em_equals_exhaustive(st, monkeypatch, cfg):
     assert np.array_equal(a.disparity.values, b.disparity.values)
     assert np.array_equal(a.image, b.image)
     assert list(a.stats.mean_energy) == list(b.stats.mean_energy)
+
+
+@pytest.mark.parametrize("forced", [0, 5])
+def test_async_solve_equals_sync(st, forced):
+    """st_solve_async (device-side convergence test and statistics, no host
+    round trip) == st_solve, outputs and EMStats."""
+    from paper_2003_11076_b200.prior import TriDevice
+    from paper_2003_11076_b200.reconstruct import AsyncStats, FramePipeline, _outputs_of
+    frame, rig, tri, sp, pp = _inputs("C2")
+    h, w = frame.shape
+    pipe = FramePipeline(rig, w, h, sp, pp)
+    td = TriDevice(tri)
+    res = []
+    for timing in (True, False):
+        pipe.load(frame.images, frame.priors)
+        stats = pipe.run(td, forced_iters=forced, timing=timing)
+        assert isinstance(stats, AsyncStats) == (not timing)
+        res.append(_outputs_of(pipe, stats, pipe.fetch()))
+    a, b = res
+    for x, y in ((a.disparity.values, b.disparity.values), (a.disparity.status, b.disparity.status),
+                 (a.segmentation.static_bits, b.segmentation.static_bits),
+                 (a.segmentation.valid_bits, b.segmentation.valid_bits), (a.image, b.image)):
+        assert np.array_equal(x, y)
+    for f in ("iterations_run", "converged_after", "mean_energy", "prev_energy",
+              "changed_fraction", "candidates_total", "energy_evals", "msteps", "esteps",
+              "prev_evals", "active_pixels", "support_records"):
+        assert getattr(a.stats, f) == getattr(b.stats, f), f

@@ -37,12 +37,28 @@ def main():
                 fn()
         torch.cuda.synchronize()
         print(f"{name:24s} {(time.perf_counter() - t0) / 10 * 1e3:.3f} ms")
+    os.environ["ST_STREAM_PROFILE"] = "1"
     for n in (10, 30):
         t0 = time.perf_counter()
         for _ in st.reconstruct_stream([(hf, tri)] * n, rig, sp, pp):
             pass
         torch.cuda.synchronize()
         print(f"stream x{n}: {(time.perf_counter() - t0) / n * 1e3:.3f} ms/frame")
+    del os.environ["ST_STREAM_PROFILE"]
+    # frame-in stream: harvest + dedup + pooled Qhull + solve per frame
+    ref = st.reconstruct(hf, rig, tri, sp, pp)
+    from paper_2003_11076_b200.qhull_pool import make_pool
+    t0 = time.perf_counter()
+    make_pool()
+    print(f"pool start + warm: {time.perf_counter() - t0:.2f} s")
+    for n in (8, 64):
+        t0 = time.perf_counter()
+        outs = list(st.reconstruct_frames([hf] * n, rig, sp, pp))
+        dt = (time.perf_counter() - t0) / n
+        ok = all(np.array_equal(o.disparity.values, ref.disparity.values)
+                 and np.array_equal(o.image, ref.image) for o in outs)
+        print(f"reconstruct_frames x{n}: {dt * 1e3:.2f} ms/frame ({1 / dt:.1f} fps), "
+              f"outputs == reconstruct(): {ok}")
 
 
 if __name__ == "__main__":
