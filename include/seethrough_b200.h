@@ -182,8 +182,10 @@ typedef struct {
 
 /* Build per-tile support candidate lists (solver.py:286-321 semantics).
  * support_uv (n,2) f64 pixel coords, support_d (n) f64.  Writes into
- * workspace; fills the sup_* pointers of *frame.  Returns records count via
- * *n_records. */
+ * workspace; fills the sup_* pointers of *frame.  With n_records non-NULL
+ * the record count is read back (one host synchronisation) and returned;
+ * with n_records NULL nothing waits on the device (the sort runs over the
+ * workspace's record bound with padding keys). */
 int st_support_build(const double* support_uv, const double* support_d, int32_t n,
                      int32_t W, int32_t H, const st_params* params, st_frame* frame,
                      void* workspace, int64_t workspace_bytes, int64_t* n_records,

@@ -70,10 +70,14 @@ __global__ void k_sup_emit(const double* __restrict__ uv, const double* __restri
 
 // After the sort: records with equal (tile, value) form one group.  heads[i]
 // flags the first record of each group.
+// n_dev (nullable): the record count on the device -- launches sized by an
+// upper bound then clear the flags of the padding records.
 __global__ void k_sup_heads(const unsigned long long* __restrict__ keys, int64_t n_rec,
-                            uint32_t* __restrict__ heads) {
+                            uint32_t* __restrict__ heads, const uint32_t* n_dev) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_rec) heads[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+  if (i >= n_rec) return;
+  const int64_t n = n_dev ? (int64_t)*n_dev : n_rec;
+  heads[i] = i < n && (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
 }
 
 // Each record ORs the pixels of its tile inside its disk (solver.py:290-308:
@@ -83,9 +87,9 @@ __global__ void k_sup_cover(const unsigned long long* __restrict__ keys,
                             const uint32_t* __restrict__ vals, const uint32_t* __restrict__ gid_incl,
                             int64_t n_rec, SupGeom g, double r2,
                             unsigned long long* __restrict__ gkey, float* __restrict__ gvalue,
-                            uint32_t* __restrict__ gmask) {
+                            uint32_t* __restrict__ gmask, const uint32_t* n_dev) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_rec) return;
+  if (i >= (n_dev ? (int64_t)*n_dev : n_rec)) return;
   const unsigned long long key = keys[i];
   const uint32_t grp = gid_incl[i] - 1;
   if (i == 0 || keys[i - 1] != key) {
@@ -240,10 +244,21 @@ extern "C" int st_support_build(const double* support_uv, const double* support_
     size_t tb = L.cub_bytes;
     ST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, counts, offs, n + 1, s));
     sthost::count_launch();
-    uint32_t host_total = 0;
-    ST_CUDA_CHECK(cudaMemcpyAsync(&host_total, offs + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    ST_CUDA_CHECK(cudaStreamSynchronize(s));
-    total = host_total;
+    // n_records == NULL: no host round trip -- every later launch is sized
+    // by the bound max_rec, padding keys (all ones) sort after the real
+    // records and the kernels read the real count offs[n] on the device.
+    const bool async = n_records == nullptr;
+    const uint32_t* total_dev = async ? offs + n : nullptr;
+    if (async) {
+      total = L.max_rec;
+      ST_CUDA_CHECK(cudaMemsetAsync(keys_in, 0xff, sizeof(unsigned long long) * (size_t)total, s));
+    } else {
+      uint32_t host_total = 0;
+      ST_CUDA_CHECK(cudaMemcpyAsync(&host_total, offs + n, sizeof(uint32_t),
+                                    cudaMemcpyDeviceToHost, s));
+      ST_CUDA_CHECK(cudaStreamSynchronize(s));
+      total = host_total;
+    }
     if (total > 0) {
       st::k_sup_emit<<<(n + 255) / 256, 256, 0, s>>>(support_uv, support_d, n, g, offs, keys_in,
                                                       vals_in);
@@ -256,7 +271,7 @@ extern "C" int st_support_build(const double* support_uv, const double* support_
       sthost::count_launch();
       // (tile, value) groups and their 32x8 pixel coverage masks
       const unsigned rb = (unsigned)((total + 255) / 256);
-      st::k_sup_heads<<<rb, 256, 0, s>>>(keys_out, total, heads);
+      st::k_sup_heads<<<rb, 256, 0, s>>>(keys_out, total, heads, total_dev);
       ST_LAUNCH_CHECK("k_sup_heads");
       tb = L.cub_bytes;
       ST_CUDA_CHECK(cub::DeviceScan::InclusiveSum(cub_tmp, tb, heads, gid, (int)total, s));
@@ -264,7 +279,7 @@ extern "C" int st_support_build(const double* support_uv, const double* support_
       ST_CUDA_CHECK(cudaMemsetAsync(gmask, 0, sizeof(uint32_t) * ST_TH * (size_t)total, s));
       const double r = p->neighborhood_radius;
       st::k_sup_cover<<<rb, 256, 0, s>>>(keys_out, vals_out, gid, total, g, r * r, gkey, gvalue,
-                                         gmask);
+                                         gmask, total_dev);
       ST_LAUNCH_CHECK("k_sup_cover");
     }
   }

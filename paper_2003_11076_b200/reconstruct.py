@@ -21,7 +21,9 @@ from .solver import (DisparityMap, EMStats, SegmentationState, SolverParams, _ch
 
 class AsyncStats:
     """EM statistics still on the device (st_solve_async): resolved from the
-    raw st_stats bytes that FramePipeline.fetch_async brings back."""
+    raw st_stats bytes that FramePipeline.fetch_async brings back
+    (support_records is -1: the asynchronous support build does not read
+    its record count back)."""
 
     def __init__(self, support_records):
         self.support_records = support_records
@@ -170,16 +172,15 @@ class FramePipeline:
                                                 float(self.prior_params.neighborhood_radius)))
         if self.sup_ws.numel() < need:
             self.sup_ws = empty((need,), t.uint8)
-        rec = N.C.c_int64(0)
+        # no host round trip unless a diagnostic path wants the record count
+        run_async = not dynamic_only and reduce is None and not timing
+        rec = N.C.c_int64(-1)
         N.invoke("st_support_build", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W, H, p,
-                 self.frame, self.sup_ws, self.sup_ws.numel(), rec)
+                 self.frame, self.sup_ws, self.sup_ws.numel(), None if run_async else rec)
         mark()
         main.wait_event(mu_done)
         mark()
         stats = N.StStats()
-        # no host round trip inside the solve unless a shard reduction, an
-        # active subset or per-stage timing needs one
-        run_async = not dynamic_only and reduce is None and not timing
         if run_async:
             N.invoke("st_solve_async", self.frame, self.rig, p, self.values, self.status,
                      self.sbits, self.vbits, self.stats_dev, self.solve_ws,

@@ -129,5 +129,5 @@ def test_async_solve_equals_sync(st, forced):
         assert np.array_equal(x, y)
     for f in ("iterations_run", "converged_after", "mean_energy", "prev_energy",
               "changed_fraction", "candidates_total", "energy_evals", "msteps", "esteps",
-              "prev_evals", "active_pixels", "support_records"):
+              "prev_evals", "active_pixels"):
         assert getattr(a.stats, f) == getattr(b.stats, f), f
