@@ -129,11 +129,12 @@ def lib():
     """Load the CUDA library (no fallback: raise if it is missing)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
+        path = os.environ.get("ST_LIB_PATH") or LIB  # experiment variants (build.py)
+        if not os.path.exists(path):
             raise ImportError(
-                f"seethrough_b200 native library not built ({LIB}); run "
+                f"seethrough_b200 native library not built ({path}); run "
                 "`python -m paper_2003_11076_b200.build` (needs nvcc, sm_100a)")
-        h = C.CDLL(LIB)
+        h = C.CDLL(path)
         for name, (res, args) in _SIGS.items():
             fn = getattr(h, name)
             fn.restype = res

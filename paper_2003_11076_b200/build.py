@@ -35,16 +35,20 @@ def up_to_date():
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
-def build(force=False, verbose=False, jobs=None):
-    """Compile every .cu for sm_100a and link one shared library."""
-    if not force and up_to_date():
+def build(force=False, verbose=False, jobs=None, defines=(), out=None):
+    """Compile every .cu for sm_100a and link one shared library.
+
+    defines / out: an experiment variant (-D flags) linked to another path
+    (load it with ST_LIB_PATH=<out>); the default library is untouched."""
+    lib = out or LIB
+    if not force and not defines and out is None and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(LIBDIR, "obj" if out is None else "obj_" + os.path.basename(out))
     os.makedirs(objdir, exist_ok=True)
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--extended-lambda",
                      "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-                     "-Xptxas", "-v"]
+                     "-Xptxas", "-v"] + ["-D" + d for d in defines]
     procs = []
     objs = []
     for src in SOURCES:
@@ -58,17 +62,17 @@ def build(force=False, verbose=False, jobs=None):
         logs.append(out.decode(errors="replace"))
         if pr.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{logs[-1]}")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout.decode(errors="replace"))
-    os.replace(tmp, LIB)
-    with open(os.path.join(LIBDIR, "ptxas.log"), "w") as fh:
+    os.replace(tmp, lib)
+    with open(lib + ".ptxas.log" if out else os.path.join(LIBDIR, "ptxas.log"), "w") as fh:
         fh.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -438,7 +438,7 @@ static SolveLayout solve_layout(int W, int H) {
   L.mask_in = o;  o += align_up(sizeof(uint32_t) * npx);
   L.mlist = o;    o += align_up(sizeof(int32_t) * npx);
   L.elist = o;    o += align_up(sizeof(int32_t) * npx);
-  L.counts = o;   o += align_up(sizeof(uint32_t) * 4);  // 2 worklist counts + stop flag
+  L.counts = o;   o += align_up(sizeof(uint32_t) * 4 + sizeof(double) * 4);  // worklist counts, stop flag, eps logs
   L.active = o;   o += align_up(sizeof(int64_t) * npx);
   L.flags = o;    o += align_up(sizeof(uint32_t) * (npx + 1));
   L.offs = o;     o += align_up(sizeof(uint32_t) * (npx + 1));
@@ -492,6 +492,9 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
   memset(stats, 0, sizeof(*stats));
   stats->converged_after = -1;
   EventSet ev(p->timing != 0);
+  double* eps_logs = (double*)(counts + 4);
+  st::k_eps_logs<<<1, 32, 0, s>>>(p->epsilon_prior, eps_logs);
+  ST_LAUNCH_CHECK("k_eps_logs");
 
   // initial masks for every pixel at the surface disparity (solver.py:455)
   ev.record(4, s);
@@ -586,6 +589,7 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       e.static_out = static_bits;
       e.valid_out = valid_bits;
       e.scatter = 1;
+      e.eps_logs = eps_logs;
       launch_e_step(rig->num_views, n_act, s, c, e);
       ST_LAUNCH_CHECK("k_e_step_at");
       ev.record(2, s);
@@ -699,6 +703,9 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
   ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t) + sizeof(int), s));
   st::k_stats_init<<<1, 32, 0, s>>>(stats_dev, npx);
   ST_LAUNCH_CHECK("k_stats_init");
+  double* eps_logs = (double*)(counts + 4);
+  st::k_eps_logs<<<1, 32, 0, s>>>(p->epsilon_prior, eps_logs);
+  ST_LAUNCH_CHECK("k_eps_logs");
   st::k_initial_masks<<<blocks_for(npx, 128), 128, 0, s>>>(c, nullptr, npx, static_bits,
                                                            valid_bits);
   ST_LAUNCH_CHECK("k_initial_masks");
@@ -740,6 +747,7 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     e.static_out = static_bits;
     e.valid_out = valid_bits;
     e.scatter = 1;
+    e.eps_logs = eps_logs;
     e.stop = stop;
     launch_e_step(rig->num_views, npx, s, c, e);
     ST_LAUNCH_CHECK("k_e_step_at");

@@ -147,7 +147,7 @@ __device__ __forceinline__ void list_append(bool want, int32_t slot, int32_t* li
 // themselves to the E-step worklist when their d changed (e_step_at is a pure
 // function of (pixel, d)).
 
-__global__ void __launch_bounds__(EM_BLOCK) k_m_step(EmCtx c, MStepArgs a) {
+__global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
   if (a.stop && *a.stop) return;  // converged (st_solve_async)
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
@@ -344,6 +344,33 @@ __device__ __forceinline__ void clamp_logs(double q, double eps, double& l1, dou
   const double qc = fmin(fmax(q, eps), dsub(1.0, eps));  // np.clip(q, eps, 1 - eps)
   l1 = log(qc);
   l0 = log(dsub(1.0, qc));
+}
+
+// Same values; rays clamped to eps or 1 - eps take the precomputed logs
+// (eps_logs = log(eps), log(1 - eps), log(1 - (1 - eps))).
+__device__ __forceinline__ void clamp_logs(double q, double eps, const double* eps_logs,
+                                           double& l1, double& l0) {
+  const double hi = dsub(1.0, eps);
+  const double qc = fmin(fmax(q, eps), hi);
+  if (eps_logs && qc == eps) {
+    l1 = __ldg(eps_logs);
+    l0 = __ldg(eps_logs + 1);
+  } else if (eps_logs && qc == hi) {
+    l1 = __ldg(eps_logs + 1);
+    l0 = __ldg(eps_logs + 2);
+  } else {
+    l1 = log(qc);
+    l0 = log(dsub(1.0, qc));
+  }
+}
+
+__global__ void k_eps_logs(double eps, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const double hi = dsub(1.0, eps);
+    out[0] = log(eps);
+    out[1] = log(hi);
+    out[2] = log(dsub(1.0, hi));
+  }
 }
 
 // Mask preference (solver.py:110-112, 156): higher score, then larger
@@ -689,7 +716,7 @@ __global__ void __launch_bounds__(ESTEP_TAPS_BLOCK) k_e_step_taps(EmCtx c, EStep
       q = sample_prior(c.priors + (size_t)k * c.HW, c.W, tp);
       vb |= 1u << k;
     }
-    clamp_logs(q, c.p.epsilon_prior, l1[k], l0[k]);
+    clamp_logs(q, c.p.epsilon_prior, a.eps_logs, l1[k], l0[k]);
   }
   const int su = c.W > 1 ? 1 : 0, sv = c.H > 1 ? c.W : 0;  // taps_of's steps
   const uint32_t* desc = reinterpret_cast<const uint32_t*>(c.desc);
@@ -744,7 +771,7 @@ __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a)
 #pragma unroll
       for (int ch = 0; ch < 16; ++ch) f[(k * 16 + ch) * stride] = 0.0;
     }
-    clamp_logs(q, c.p.epsilon_prior, l1[k], l0[k]);
+    clamp_logs(q, c.p.epsilon_prior, a.eps_logs, l1[k], l0[k]);
   }
   const uint32_t m = estep_generic(K, f, stride, l1, l0, vb, c.p);
   const int64_t o = a.scatter ? pix : i;

@@ -6,6 +6,11 @@
 #include "st_common.cuh"
 
 #define EM_BLOCK 128
+// 4 resident blocks per SM (<= 128 registers): measured fastest on B200
+#ifndef MSTEP_MIN_BLOCKS
+#define MSTEP_MIN_BLOCKS 4
+#endif
+#define MSTEP_BOUNDS __launch_bounds__(EM_BLOCK, MSTEP_MIN_BLOCKS)
 #define STATS_BLOCK 256
 #define ESTEP_BLOCK 64
 #define ESTEP_TAPS_BLOCK 128
@@ -76,6 +81,7 @@ struct EStepArgs {
   int scatter;               // 1: write at pixel index, 0: at row i
   int exhaustive;            // 1: score every mask in fp64 (no fp32 screen)
   const int* stop;           // nullable: device flag, set -> the launch does nothing
+  const double* eps_logs;    // nullable: k_eps_logs output (clamped-prior logs)
 };
 
 __global__ void k_m_step(EmCtx c, MStepArgs a);
@@ -110,6 +116,9 @@ __global__ void k_reduce_partials(const Partial* parts, int nparts, Partial* out
 __global__ void k_solve_control(int it, const Partial* reduced, uint32_t* counts, int64_t n_act,
                                 int forced_iters, st_stats* stats, int* stop);
 __global__ void k_stats_init(st_stats* stats, int64_t n_act);
+// log(eps), log(1 - eps), log(1 - (1 - eps)) with the device log: the E-step
+// reuses them for rays whose prior is clamped (identical values).
+__global__ void k_eps_logs(double eps, double* out);
 __global__ void k_flag_active(const float* ref_prior, const uint8_t* mask, int64_t npx,
                               double threshold, uint32_t* flags);
 __global__ void k_scatter_active(const uint32_t* flags, const uint32_t* offs, int64_t npx,

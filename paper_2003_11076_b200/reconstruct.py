@@ -81,6 +81,7 @@ class FramePipeline:
         self.frame.desc = self.desc.data_ptr()
         self.frame.mu = self.mu.data_ptr()
         self.side = t.cuda.Stream()
+        self.side2 = t.cuda.Stream()
 
     # -- inputs ---------------------------------------------------------------------
 
@@ -164,19 +165,24 @@ class FramePipeline:
             N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max), self.mu,
                      self.mu_ws, self.mu_ws.numel())
             mu_done = self._event(timing=timing)
-        if not getattr(self, "_desc_ready", False):
-            N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
-        self._desc_ready = False
-        mark()
+        # the support candidate groups depend only on the support list: a
+        # second side stream builds them concurrently with the descriptors
         need = int(N.lib().st_support_workspace(tri_dev.n_sup, W, H,
                                                 float(self.prior_params.neighborhood_radius)))
         if self.sup_ws.numel() < need:
             self.sup_ws = empty((need,), t.uint8)
-        # no host round trip unless a diagnostic path wants the record count
         run_async = not dynamic_only and reduce is None and not timing
         rec = N.C.c_int64(-1)
-        N.invoke("st_support_build", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W, H, p,
-                 self.frame, self.sup_ws, self.sup_ws.numel(), None if run_async else rec)
+        with t.cuda.stream(self.side2):
+            self.side2.wait_event(ready)
+            N.invoke("st_support_build", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W, H, p,
+                     self.frame, self.sup_ws, self.sup_ws.numel(), None if run_async else rec)
+            sup_done = self._event(timing=False)
+        if not getattr(self, "_desc_ready", False):
+            N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
+        self._desc_ready = False
+        mark()
+        main.wait_event(sup_done)
         mark()
         main.wait_event(mu_done)
         mark()
