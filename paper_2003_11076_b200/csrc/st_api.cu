@@ -714,9 +714,12 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
   const int nblk = (int)blocks_for(npx, EM_BLOCK);
   const int nwarps = nblk * (EM_BLOCK / 32);
   const int sblk = (int)blocks_for(npx, STATS_BLOCK);
+  // iterations >= 2 work on device-counted worklists (a fraction of the
+  // pixels) and do nothing once converged: one wave of grid-stride blocks
+  const int wave = std::min(nblk, 148 * 8);
   for (int it = 1; it <= iters; ++it) {
     if (it > 1) {
-      st::k_flag_mstep<<<nblk, EM_BLOCK, 0, s>>>(nullptr, npx, static_bits, mask_in, e_act,
+      st::k_flag_mstep<<<wave, EM_BLOCK, 0, s>>>(nullptr, npx, static_bits, mask_in, e_act,
                                                  pe_act, chg, mlist, counts, stop);
       ST_LAUNCH_CHECK("k_flag_mstep");
     }
@@ -736,7 +739,7 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     a.elist_count = counts + 1;
     a.partials = work;
     a.stop = stop;
-    st::k_m_step<<<nblk, EM_BLOCK, 0, s>>>(c, a);
+    st::k_m_step<<<it > 1 ? wave : nblk, EM_BLOCK, 0, s>>>(c, a);
     ST_LAUNCH_CHECK("k_m_step");
     st::EStepArgs e = {};
     e.n = npx;
@@ -749,9 +752,10 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     e.scatter = 1;
     e.eps_logs = eps_logs;
     e.stop = stop;
-    launch_e_step(rig->num_views, npx, s, c, e);
+    launch_e_step(rig->num_views, it > 1 ? std::min<int64_t>(npx, 148 * 8 * 128) : npx, s, c, e);
     ST_LAUNCH_CHECK("k_e_step_at");
-    st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(npx, it > 1, e_act, pe_act, chg, work, nwarps,
+    st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(npx, it > 1, e_act, pe_act, chg, work,
+                                                (it > 1 ? wave : nblk) * (EM_BLOCK / 32),
                                                 parts, stop);
     ST_LAUNCH_CHECK("k_em_stats");
     st::k_reduce_partials<<<1, 256, 0, s>>>(parts, sblk, reduced + it, stop);

@@ -149,12 +149,14 @@ __device__ __forceinline__ void list_append(bool want, int32_t slot, int32_t* li
 
 __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
   if (a.stop && *a.stop) return;  // converged (st_solve_async)
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
+  long long n_cand = 0, n_eval = 0;
+  // block-uniform grid-stride loop: one wave of blocks can cover a worklist
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_work;
+       base += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t t = base + threadIdx.x;
   const bool live = t < n_work;
   const int64_t i = live ? (a.list ? (int64_t)a.list[t] : t) : 0;
-
-  long long n_cand = 0, n_eval = 0;
   bool want_e = false;
 
   if (live) {
@@ -230,6 +232,7 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
     if (a.mask_in) a.mask_in[i] = bits;
   }
   if (a.elist) list_append(want_e, (int32_t)i, a.elist, a.elist_count);
+  }
   if (a.partials) {
     const long long c_cand = warp_sum(n_cand);
     const long long c_eval = warp_sum(n_eval);
@@ -251,17 +254,20 @@ __global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n,
                              int32_t* __restrict__ list, uint32_t* __restrict__ count,
                              const int* stop) {
   if (stop && *stop) return;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool want = false;
-  if (i < n) {
-    const int64_t pix = active ? active[i] : i;
-    want = static_all[pix] != mask_in[i];
-    if (!want) {
-      pe[i] = e[i];
-      chg[i] = 0;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool want = false;
+    if (i < n) {
+      const int64_t pix = active ? active[i] : i;
+      want = static_all[pix] != mask_in[i];
+      if (!want) {
+        pe[i] = e[i];
+        chg[i] = 0;
+      }
     }
+    list_append(want, (int32_t)i, list, count);
   }
-  list_append(want, (int32_t)i, list, count);
 }
 
 // Per-iteration statistics over every active slot, as fixed-order per-warp
@@ -687,13 +693,13 @@ __device__ __forceinline__ void desc_word(const uint32_t* __restrict__ plane, in
 // words (L1-resident), so occupancy is bounded by registers alone.  RECT:
 // rectified rig, vertical weight identically 0.
 template <int KT, bool RECT>
-__global__ void __launch_bounds__(ESTEP_TAPS_BLOCK) k_e_step_taps(EmCtx c, EStepArgs a) {
+__global__ void __launch_bounds__(ESTEP_TAPS_BLOCK, ESTEP_MIN_BLOCKS) k_e_step_taps(EmCtx c, EStepArgs a) {
   if (a.stop && *a.stop) return;  // converged (st_solve_async)
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
-  if (t >= n_work) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_work;
+       t += (int64_t)gridDim.x * blockDim.x) {
   const int64_t i = a.list ? (int64_t)a.list[t] : t;
-  if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) return;  // solver.py:476-478
+  if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) continue;  // solver.py:476-478
   const int64_t pix = a.pix ? a.pix[i] : i;
   const double u = (double)(pix % c.W), v = (double)(pix / c.W);
   const double d = a.d[i];
@@ -728,6 +734,7 @@ __global__ void __launch_bounds__(ESTEP_TAPS_BLOCK) k_e_step_taps(EmCtx c, EStep
   const int64_t o = a.scatter ? pix : i;
   a.static_out[o] = m;
   a.valid_out[o] = vb;
+  }
 }
 
 template __global__ void k_e_step_taps<2, false>(EmCtx, EStepArgs);
@@ -744,11 +751,11 @@ template __global__ void k_e_step_taps<5, true>(EmCtx, EStepArgs);
 __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a) {
   extern __shared__ double sh_f[];
   if (a.stop && *a.stop) return;  // converged (st_solve_async)
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
-  if (t >= n_work) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_work;
+       t += (int64_t)gridDim.x * blockDim.x) {
   const int64_t i = a.list ? (int64_t)a.list[t] : t;
-  if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) return;  // solver.py:476-478
+  if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) continue;  // solver.py:476-478
   const int64_t pix = a.pix ? a.pix[i] : i;
   const double u = (double)(pix % c.W), v = (double)(pix / c.W);
   const double d = a.d[i];
@@ -777,6 +784,7 @@ __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a)
   const int64_t o = a.scatter ? pix : i;
   a.static_out[o] = m;
   a.valid_out[o] = vb;
+  }
 }
 
 // initial_masks (solver.py:421-432): valid & q >= threshold at mu.
@@ -973,17 +981,26 @@ __global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
   si[3][threadIdx.x] = c3;
   si[4][threadIdx.x] = c4;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    Partial r = {};
-    for (int t = 0; t < (int)blockDim.x; ++t) {
-      r.sum_e += sd[0][t];
-      r.sum_pe += sd[1][t];
-      r.n_fin += si[0][t];
-      r.n_pfin += si[1][t];
-      r.n_changed += si[2][t];
-      r.n_cand += si[3][t];
-      r.n_eval += si[4][t];
+  // fixed-order pairwise tree over the 256 thread sums (deterministic)
+  for (int h = 128; h > 0; h >>= 1) {
+    const int t = threadIdx.x;
+    if (t < h) {
+      sd[0][t] += sd[0][t + h];
+      sd[1][t] += sd[1][t + h];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) si[k][t] += si[k][t + h];
     }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    Partial r;
+    r.sum_e = sd[0][0];
+    r.sum_pe = sd[1][0];
+    r.n_fin = si[0][0];
+    r.n_pfin = si[1][0];
+    r.n_changed = si[2][0];
+    r.n_cand = si[3][0];
+    r.n_eval = si[4][0];
     *out = r;
   }
 }

@@ -14,6 +14,9 @@
 #define STATS_BLOCK 256
 #define ESTEP_BLOCK 64
 #define ESTEP_TAPS_BLOCK 128
+#ifndef ESTEP_MIN_BLOCKS
+#define ESTEP_MIN_BLOCKS 4  // <= 128 registers
+#endif
 #define ST_MAX_BAND 64
 
 namespace st {

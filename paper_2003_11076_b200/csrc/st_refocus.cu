@@ -146,6 +146,31 @@ __global__ void k_median_small(const uint8_t* __restrict__ src, int H, int W, in
   const int ylo = max(y - radius, 0), yhi = min(y + radius, H - 1);
   const int xlo = max(x - radius, 0), xhi = min(x + radius, W - 1);
   const int cnt = (yhi - ylo + 1) * (xhi - xlo + 1);
+  if (radius == 1 && cnt == 9) {
+    // full 3x3 window: v[(9-1)//2] == v[9//2], so 0.5*(v+v) and rint give
+    // the middle value itself -- a fixed 19-exchange median-of-9 network
+    // in registers (no data-dependent sort)
+    for (int ch = 0; ch < C; ++ch) {
+      int v[9];
+#pragma unroll
+      for (int j = 0; j < 9; ++j)
+        v[j] = __ldg(src + ((size_t)(y - 1 + j / 3) * W + (x - 1 + j % 3)) * C + ch);
+      auto cx = [&](int a, int b) {
+        const int lo = min(v[a], v[b]), hi = max(v[a], v[b]);
+        v[a] = lo;
+        v[b] = hi;
+      };
+      cx(1, 2); cx(4, 5); cx(7, 8);
+      cx(0, 1); cx(3, 4); cx(6, 7);
+      cx(1, 2); cx(4, 5); cx(7, 8);
+      cx(0, 3); cx(5, 8); cx(4, 7);
+      cx(3, 6); cx(1, 4); cx(2, 5);
+      cx(4, 7); cx(4, 2); cx(6, 4);
+      cx(4, 2);
+      out[(size_t)p * C + ch] = (uint8_t)v[4];
+    }
+    return;
+  }
   for (int ch = 0; ch < C; ++ch) {
     int v0, v1;
     if (radius == 1) {

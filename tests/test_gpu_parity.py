@@ -288,6 +288,12 @@ def test_reconstruct_end_to_end(st, name):
         assert (r.disparity.values == g[f"{tag}_values"]).mean() >= AGREE
         assert (r.image == g[f"{tag}_synth1_img"]).all(axis=2).mean() >= AGREE
         assert (r.provenance == g[f"{tag}_synth1_prov"]).mean() >= AGREE
+        ref = g[f"{tag}_stats"]  # dense solves take the host-sync-free path
+        assert r.stats.iterations_run == ref["iterations_run"]
+        assert r.stats.converged_after == ref["converged_after"]
+        assert np.allclose(r.stats.mean_energy, ref["mean_energy"], rtol=1e-9)
+        assert np.allclose(r.stats.prev_energy, ref["prev_energy"], rtol=1e-9)
+        assert np.allclose(r.stats.changed_fraction, ref["changed_fraction"], atol=2e-4)
 
 
 def test_solver_errors(st):
