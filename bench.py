@@ -82,20 +82,61 @@ def params_for(cfg):
 # -- clocks ---------------------------------------------------------------------------
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled during the timed region: NVML
+    polled every 2 ms from a thread (plus one synchronous sample when the
+    region opens and one when it closes); nvidia-smi -lms as the fallback."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, index):
         self.index = index
+        self.samples = []          # (sm_mhz, max_mhz, reason bits)
+        self.nvml = None
+        self.stop = threading.Event()
         self.proc = None
         self.lines = []
 
+    def _handle(self, nv):
+        try:
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            return nv.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:  # noqa: BLE001
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _sample(self):
+        nv, h = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        self.samples.append((float(sm), float(mx), int(get(h))))
+
+    def _poll(self):
+        while not self.stop.wait(0.002):
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                return
+
     def __enter__(self):
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = (nv, self._handle(nv))
+            self._sample()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:  # noqa: BLE001
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.index)],
+                ["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "50", "-i", str(self.index)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -105,10 +146,23 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            parts = [x.strip() for x in line.split(",")]
+            try:
+                bits = sum(b for (_, b), v in zip(self.REASONS, parts[2:6])
+                           if v.lower() == "active")
+                self.samples.append((float(parts[0]), float(parts[1]), bits))
+            except (ValueError, IndexError):
+                continue
 
     def __exit__(self, *exc):
-        if self.proc is not None:
+        if self.nvml is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                pass
+        elif self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -117,24 +171,15 @@ class ClockSampler:
             self.thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [x[0] for x in self.samples]
+        bits = 0
+        for x in self.samples:
+            bits |= x[2]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.samples[-1][1],
+                "reasons": sorted(n for n, b in self.REASONS if bits & b),
+                "samples": len(sm), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # -- CPU oracle sample ------------------------------------------------------------------
@@ -334,7 +379,7 @@ def run_ours(args):
     for d, s in zip(pin_pris, frame.priors):
         d[...] = s
     host_frame = st.LightFieldFrame(images=pin_imgs, priors=pin_pris)
-    e2e_steps = max(3, args.steps)
+    e2e_steps = max(3, args.e2e_frames)
 
     def e2e_single():
         # one synchronous reconstruct() call per frame
@@ -491,6 +536,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="value loop only (profiling)")
+    ap.add_argument("--e2e-frames", type=int, default=60,
+                    help="frames per timed e2e stream (steady-state throughput)")
     ap.add_argument("--budget", type=float, default=150.0,
                     help="reference arm: seconds for the whole run")
     args = ap.parse_args()

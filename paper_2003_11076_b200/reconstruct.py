@@ -141,9 +141,16 @@ class FramePipeline:
         return u[keep], v[keep], d[keep], s[keep]
 
     def run(self, tri_dev, dynamic_only=False, forced_iters=0, median_radius=1, timing=False,
-            reduce=None):
+            reduce=None, ready=None):
         """Descriptors, mu, support lists, EM, refocus + median for the loaded frame
-        (descriptors are reused when harvest() already computed them)."""
+        (descriptors are reused when harvest() already computed them).
+
+        The pre-solve stages run on two side streams -- the surface raster
+        (its Qhull-walk emulation is a long pointer chase) on one, the
+        descriptors and the support candidate groups on the other -- and
+        start at `ready` (default: now, on the current stream).  A caller
+        that passes the event its frame's inputs were loaded on (see
+        reconstruct_stream) lets them overlap the previous frame's EM."""
         p = N.make_params(self.params, self.prior_params, forced_iters, timing)
         K, H, W = self.K, self.H, self.W
         t = self.t
@@ -151,38 +158,36 @@ class FramePipeline:
         marks = []
         mark = (lambda: marks.append(self._event())) if timing else (lambda: None)
         mark()
-        # the surface raster runs on a side stream, overlapped with the
-        # descriptors and the support lists (its Qhull-walk emulation has a
-        # long single-thread chain at the image corner)
         need = int(N.lib().st_mu_raster_workspace(W, H, tri_dev.n_tri))
         if self.mu_ws.numel() < need:
             self.mu_ws = empty((need,), t.uint8)
-        ready = t.cuda.Event()
-        ready.record(main)
+        if ready is None:
+            ready = t.cuda.Event()
+            ready.record(main)
         with t.cuda.stream(self.side):
             self.side.wait_event(ready)
             mu_start = self._event() if timing else None
             N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max), self.mu,
                      self.mu_ws, self.mu_ws.numel())
             mu_done = self._event(timing=timing)
-        # the support candidate groups depend only on the support list: a
-        # second side stream builds them concurrently with the descriptors
         need = int(N.lib().st_support_workspace(tri_dev.n_sup, W, H,
                                                 float(self.prior_params.neighborhood_radius)))
         if self.sup_ws.numel() < need:
             self.sup_ws = empty((need,), t.uint8)
+        # no host round trip unless a diagnostic path wants the record count
         run_async = not dynamic_only and reduce is None and not timing
         rec = N.C.c_int64(-1)
         with t.cuda.stream(self.side2):
             self.side2.wait_event(ready)
+            if getattr(self, "_desc_ready", False):
+                self.side2.wait_stream(main)  # harvest() wrote them on the caller's stream
+            else:
+                N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
             N.invoke("st_support_build", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W, H, p,
                      self.frame, self.sup_ws, self.sup_ws.numel(), None if run_async else rec)
-            sup_done = self._event(timing=False)
-        if not getattr(self, "_desc_ready", False):
-            N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
+            pre_done = self._event(timing=False)
         self._desc_ready = False
-        mark()
-        main.wait_event(sup_done)
+        main.wait_event(pre_done)
         mark()
         main.wait_event(mu_done)
         mark()
@@ -213,7 +218,7 @@ class FramePipeline:
         out = _stats_of(stats)
         if timing:
             marks[-1].synchronize()
-            names = ("descriptors", "support_build", "mu_wait", "solve", "synthesize")
+            names = ("descriptors_support", "mu_wait", "solve", "synthesize")
             out.stage_ms = {n: marks[i].elapsed_time(marks[i + 1]) for i, n in enumerate(names)}
             out.stage_ms["mu_raster_side_stream"] = mu_start.elapsed_time(mu_done)
         return out
@@ -236,13 +241,23 @@ class FramePipeline:
         return host
 
     def fetch_async(self, stream):
-        """Enqueue the D2H copies on `stream`; the arrays are valid once it syncs."""
+        """Enqueue the D2H copies on `stream`; the arrays are valid once it syncs.
+
+        One pinned block per frame (torch's caching host allocator recycles
+        it once the caller drops the arrays), carved into the artefacts."""
         t = self.t
+        devs = (self.values, self.status, self.sbits, self.vbits, self.image, self.prov,
+                self.n_rays, self.stats_dev)
+        offs, total = [], 0
+        for d in devs:
+            offs.append(total)
+            total += (d.numel() * d.element_size() + 255) & ~255
+        block = t.empty((total,), dtype=t.uint8, pin_memory=True)
         outs = []
         with t.cuda.stream(stream):
-            for d in (self.values, self.status, self.sbits, self.vbits, self.image, self.prov,
-                      self.n_rays, self.stats_dev):
-                h = t.empty(d.shape, dtype=d.dtype, pin_memory=True)
+            for d, o in zip(devs, offs):
+                n = d.numel() * d.element_size()
+                h = block[o:o + n].view(d.dtype).view(d.shape)
                 h.copy_(d, non_blocking=True)
                 outs.append(h)
         return [h.numpy() for h in outs]
@@ -281,7 +296,7 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
     if first is None:
         return
     h, w = first[0].shape
-    pipes = [FramePipeline(rig, w, h, params, prior_params) for _ in range(2)]
+    pipes = _stream_pipes(rig, w, h, params, prior_params)
     main = t.cuda.current_stream()
     copy_s, out_s = t.cuda.Stream(), t.cuda.Stream()
     free = [None, None]          # event: pipe's inputs/outputs no longer in use
@@ -341,9 +356,12 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
         pipe, td, loaded, check = item
         main.wait_event(loaded)
         for x in td.tensors():
-            x.record_stream(main)
+            for st_ in (main, pipe.side, pipe.side2):
+                x.record_stream(st_)
+        # the frame's pre-solve stages start as soon as its inputs are on the
+        # device, overlapping the previous frame's EM on the main stream
         stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
-                         median_radius=median_radius)
+                         median_radius=median_radius, ready=loaded)
         t0 = tick("main_run", t0)
         done = t.cuda.Event()
         done.record(main)
@@ -368,6 +386,7 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
         pending = (pipe, stats, fetched, host, flags)
         i += 1
     worker.join()
+    pipes.busy = False
     if prof is not None:
         print("reconstruct_stream profile (s, summed over frames):",
               {k: round(v, 4) for k, v in sorted(prof.items())}, f"frames={i}", flush=True)
@@ -439,6 +458,26 @@ def _chain(first, rest):
 
 
 _PIPES = {}
+_STREAM_PIPES = {}
+
+
+class _PipePair(list):
+    busy = False
+
+
+def _stream_pipes(rig, w, h, params, prior_params):
+    """The two alternating pipelines of reconstruct_stream, kept across calls;
+    a pair in use by a running stream is never handed out twice."""
+    key = (id(rig), w, h, repr(params), repr(prior_params))
+    p = _STREAM_PIPES.get(key)
+    if p is None or p.busy:
+        p = _PipePair(FramePipeline(rig, w, h, params, prior_params) for _ in range(2))
+        if key not in _STREAM_PIPES or not _STREAM_PIPES[key].busy:
+            if len(_STREAM_PIPES) > 4:
+                _STREAM_PIPES.clear()
+            _STREAM_PIPES[key] = p
+    p.busy = True
+    return p
 
 
 def _pipeline_for(rig, w, h, params, prior_params):
