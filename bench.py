@@ -421,6 +421,40 @@ def run_ours(args):
     h2d = sum(a.nbytes for a in pin_imgs) + sum(a.nbytes for a in pin_pris) + tdv.nbytes
     d2h = pipe.output_bytes()
 
+    # -- pipelined device-resident throughput: two resident frame slots alternate,
+    # each frame's pre-solve stages (side streams) overlapping the previous
+    # frame's EM; the two slots' working set (~300 MB) exceeds the 126 MB L2 -----
+    pipe2 = FramePipeline(rig, w, h, sp, pp)
+    pipe2.load(frame.images, frame.priors)
+    tdev2 = TriDevice(tri)
+    slots = [(pipe, tdev), (pipe2, tdev2)]
+    done_ev = [None, None]
+
+    def pipelined(n):
+        for j in range(n):
+            pp_, td_ = slots[j % 2]
+            ready = torch.cuda.Event()
+            if done_ev[j % 2] is not None:
+                ready = done_ev[j % 2]      # slot free once its previous frame finished
+            else:
+                ready.record(stream)
+            pp_.run(td_, forced_iters=args.forced_iters, ready=ready)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            done_ev[j % 2] = ev
+
+    pipelined(4)
+    barrier()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    n_pipe = max(args.steps, 20)
+    p0.record(stream)
+    pipelined(n_pipe)
+    p1.record(stream)
+    barrier()
+    pipe_ms = max_ranks(p0.elapsed_time(p1))
+    pipelined_fps = world * n_pipe / (pipe_ms / 1e3)
+
     # -- forced-5 (non-reference bench mode): exactly max_iters EM iterations -----------
     forced = None
     if not args.forced_iters and args.forced_steps > 0:
@@ -518,6 +552,11 @@ def run_ours(args):
                             for n in stats[0].stage_ms}},
         "gpix_plane_per_s": w * h * dmax * fps / 1e9,
         "forced_iters_mode": forced,
+        "pipelined_resident": {"value": pipelined_fps, "unit": "frames/s",
+                               "ms_per_frame": pipe_ms / n_pipe, "frames": n_pipe,
+                               "note": "two resident frame slots, frame i+1's descriptors / "
+                                       "support groups / mu raster overlap frame i's EM; "
+                                       "no L2 flush (working set > L2)"},
     }
     print(json.dumps(out), flush=True)
     if dist is not None:
