@@ -222,7 +222,10 @@ typedef struct st_cams {
 int st_harvest(const uint8_t* desc, const float* priors, const st_cams* cams, double d_max,
                int32_t n_d, float threshold, int32_t stride, double min_texture,
                int32_t* out_u, int32_t* out_v, double* out_d, int32_t* out_src,
-               int64_t* out_count, void* workspace, int64_t workspace_bytes, void* stream);
+               int64_t* out_count, int64_t* counters, void* workspace, int64_t workspace_bytes,
+               void* stream);
+/* counters (nullable, device int64[2]): candidates scanned, reverse scans run
+ * (each scan = n_d descriptor samples; the bench's roofline unit). */
 int64_t st_harvest_capacity(int32_t K, int32_t W, int32_t H, int32_t stride);
 int64_t st_harvest_workspace(int32_t K, int32_t W, int32_t H, int32_t stride);
 
@@ -316,6 +319,55 @@ int st_refocus_pixels(const uint8_t* images, const st_rig* rig, const int64_t* p
 /* refocus.py:68-106 median_filter on an (H,W,C) uint8 image. */
 int st_median(const uint8_t* image, int32_t H, int32_t W, int32_t C, int32_t radius,
               uint8_t* out, void* stream);
+
+/* ---- one frame, one call (the host runtime of reconstruct_stream) ------- */
+
+/* Everything a frame pipeline keeps across frames: the persistent device
+ * buffers, workspaces, streams and (after st_frame_plan_init) its events. */
+typedef struct st_frame_plan {
+  st_frame frame;              /* images, priors, desc, mu; sup_* filled per frame */
+  st_rig rig;
+  st_params params;            /* dense async solve: forced_iters, no timing */
+  int32_t median_radius;
+  int32_t descriptors_ready;   /* 1: desc already computed on the main stream */
+  float* values;
+  uint8_t* status;
+  uint32_t* static_bits;
+  uint32_t* valid_bits;
+  uint8_t* image;
+  uint8_t* prov;
+  uint8_t* n_rays;
+  uint8_t* scratch;            /* H*W*3 */
+  st_stats* stats_dev;
+  void* mu_ws;
+  int64_t mu_ws_bytes;
+  void* sup_ws;
+  int64_t sup_ws_bytes;
+  void* solve_ws;
+  int64_t solve_ws_bytes;
+  void* main_stream;           /* cudaStream_t handles */
+  void* side_stream;           /* mu raster */
+  void* side2_stream;          /* descriptors + support groups */
+  void* out_stream;            /* D2H of the artefacts (null = the default stream) */
+  void* events[4];             /* owned, created by st_frame_plan_init */
+} st_frame_plan;
+
+int st_frame_plan_init(st_frame_plan* plan);
+int st_frame_plan_destroy(st_frame_plan* plan);
+
+/* One frame of pipeline.py:247-261 (solve + synthesize) with no host
+ * synchronisation: the mu raster (side stream) and the descriptors + support
+ * candidate groups (side2) start at `ready` (a cudaEvent_t; nullable = now
+ * on the main stream), the dense asynchronous solve and the refocus run on
+ * the main stream, and when host_block (pinned, nullable) is given the
+ * artefacts -- values, status, static, valid, image, provenance, n_rays,
+ * st_stats, each 256-byte aligned in that order -- are copied into it on the
+ * out stream.  `done` (cudaEvent_t, nullable) is recorded after the copies
+ * (or after the refocus). */
+int st_frame_run(st_frame_plan* plan, const st_tri* tri, const double* support_uv,
+                 const double* support_d, int32_t n_support, void* ready, void* host_block,
+                 void* done);
+int64_t st_frame_host_bytes(int32_t W, int32_t H);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,20 @@ class StCams(C.Structure):
                 ("lr_scale", C.c_double * MAX_VIEWS)]
 
 
+class StFramePlan(C.Structure):
+    _fields_ = [("frame", StFrame), ("rig", StRig), ("params", StParams),
+                ("median_radius", C.c_int32), ("descriptors_ready", C.c_int32),
+                ("values", C.c_void_p), ("status", C.c_void_p), ("static_bits", C.c_void_p),
+                ("valid_bits", C.c_void_p), ("image", C.c_void_p), ("prov", C.c_void_p),
+                ("n_rays", C.c_void_p), ("scratch", C.c_void_p), ("stats_dev", C.c_void_p),
+                ("mu_ws", C.c_void_p), ("mu_ws_bytes", C.c_int64),
+                ("sup_ws", C.c_void_p), ("sup_ws_bytes", C.c_int64),
+                ("solve_ws", C.c_void_p), ("solve_ws_bytes", C.c_int64),
+                ("main_stream", C.c_void_p), ("side_stream", C.c_void_p),
+                ("side2_stream", C.c_void_p), ("out_stream", C.c_void_p),
+                ("events", C.c_void_p * 4)]
+
+
 REDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int32, C.c_void_p)
 
 _P = C.c_void_p
@@ -90,9 +104,14 @@ _SIGS = {
     "st_support_workspace": (C.c_int64, [_I32, _I32, _I32, _D]),
     "st_solve_async": (C.c_int, [C.POINTER(StFrame), C.POINTER(StRig), C.POINTER(StParams),
                                  _P, _P, _P, _P, _P, _P, _I64, _P]),
+    "st_frame_plan_init": (C.c_int, [C.POINTER(StFramePlan)]),
+    "st_frame_plan_destroy": (C.c_int, [C.POINTER(StFramePlan)]),
+    "st_frame_run": (C.c_int, [C.POINTER(StFramePlan), C.POINTER(StTri), _P, _P, _I32, _P, _P,
+                               _P]),
+    "st_frame_host_bytes": (C.c_int64, [_I32, _I32]),
     "st_tri_tables": (C.c_int, [C.POINTER(StTri), _P, _P, _P, _P]),
     "st_harvest": (C.c_int, [_P, _P, C.POINTER(StCams), _D, _I32, C.c_float, _I32, _D,
-                             _P, _P, _P, _P, _P, _P, _I64, _P]),
+                             _P, _P, _P, _P, _P, _P, _P, _I64, _P]),
     "st_harvest_capacity": (C.c_int64, [_I32, _I32, _I32, _I32]),
     "st_harvest_workspace": (C.c_int64, [_I32, _I32, _I32, _I32]),
     "st_support_dedup": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P]),

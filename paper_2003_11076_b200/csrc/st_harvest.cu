@@ -151,6 +151,7 @@ struct HvArgs {
   int32_t* pv;
   double* pd;
   uint8_t* flag;
+  int64_t* counters;          // nullable: [candidates, reverse scans]
 };
 
 __global__ void __launch_bounds__(HV_BLOCK) k_hv_match(st_cams cam, HvArgs a) {
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(HV_BLOCK) k_hv_match(st_cams cam, HvArgs a) {
       // reverse match from the rounded landing pixel (prior.py:120-133)
       const WarpOut w = warp_ab(cam.fw_a[s], cam.fw_b[s], u, v, best);
       const double ru = rint(w.pu), rv = rint(w.pv);
+      if (a.counters && lane == 0) atomicAdd((unsigned long long*)(a.counters + 1), 1ull);
       const double rb = warp_scan(pd, ps, a.W, a.H, cam.bw_a[s], cam.bw_b[s], ru, rv, a.nd);
       keep = !isnan(rb) && fabs(dsub(dmul(rb, cam.lr_scale[s]), best)) <= 1.0;
       if (keep && s == cam.ref_index) {
@@ -314,7 +316,8 @@ int64_t st_harvest_workspace(int32_t K, int32_t W, int32_t H, int32_t stride) {
 int st_harvest(const uint8_t* desc, const float* priors, const st_cams* cams, double d_max,
                int32_t n_d, float threshold, int32_t stride, double min_texture,
                int32_t* out_u, int32_t* out_v, double* out_d, int32_t* out_src,
-               int64_t* out_count, void* workspace, int64_t workspace_bytes, void* stream) {
+               int64_t* out_count, int64_t* counters, void* workspace, int64_t workspace_bytes,
+               void* stream) {
   if (!cams || cams->num_views < 2 || cams->num_views > ST_MAX_VIEWS) {
     sthost::set_error("st_harvest: view count must be in [2, %d]", ST_MAX_VIEWS);
     return ST_EINVAL;
@@ -369,6 +372,11 @@ int st_harvest(const uint8_t* desc, const float* priors, const st_cams* cams, do
   a.pv = w.pv;
   a.pd = w.pd;
   a.flag = w.pflag;
+  a.counters = counters;
+  if (counters) {
+    ST_CUDA_CHECK(cudaMemcpyAsync(counters, w.n_cand, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    ST_CUDA_CHECK(cudaMemsetAsync(counters + 1, 0, sizeof(int64_t), s));
+  }
   // one warp per candidate (grid-stride; the count stays on the device)
   ST_CUDA_CHECK(cudaMemsetAsync(w.pflag, 0, (size_t)sites, s));
   const int64_t warps = std::max<int64_t>(sites, 1);

@@ -322,7 +322,7 @@ def harvest_device(frame, rig, params=None, threshold=0.7, stride=SUPPORT_STRIDE
     osrc = empty((cap,), t.int32)
     cnt = empty((1,), t.int64)
     N.invoke("st_harvest", d.desc, d.priors, cams, float(params.d_max), _grid_len(params.d_max),
-             float(threshold), int(stride), float(min_texture), ou, ov, od, osrc, cnt, ws,
+             float(threshold), int(stride), float(min_texture), ou, ov, od, osrc, cnt, None, ws,
              ws.numel())
     n = int(cnt.item())
     return download(ou[:n]), download(ov[:n]), download(od[:n]), download(osrc[:n])

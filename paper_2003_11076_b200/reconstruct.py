@@ -101,10 +101,11 @@ class FramePipeline:
 
     # -- the frame --------------------------------------------------------------------
 
-    def harvest(self, threshold=None, stride=None, min_texture=None):
+    def harvest(self, threshold=None, stride=None, min_texture=None, counters=None):
         """Descriptors + the device support harvest of the loaded frame
         (st_harvest, prior.py:233-259 before deduplicate).  Enqueued on the
-        current stream; returns (u, v, d, src, count) device tensors."""
+        current stream; returns (u, v, d, src, count) device tensors.
+        counters: optional device int64[2] (candidates, reverse scans)."""
         from .prior import MIN_TEXTURE, SUPPORT_STRIDE, _grid_len
         t = self.t
         K, H, W = self.K, self.H, self.W
@@ -127,7 +128,8 @@ class FramePipeline:
         self._desc_ready = True
         N.invoke("st_harvest", self.desc, self.priors, self.cams, float(self.prior_params.d_max),
                  _grid_len(self.prior_params.d_max), float(thr), stride, mt, self.hv_u,
-                 self.hv_v, self.hv_d, self.hv_src, self.hv_n, self.hv_ws, self.hv_ws.numel())
+                 self.hv_v, self.hv_d, self.hv_src, self.hv_n, counters, self.hv_ws,
+                 self.hv_ws.numel())
         return self.hv_u, self.hv_v, self.hv_d, self.hv_src, self.hv_n
 
     def harvest_host(self, **kw):
@@ -222,6 +224,86 @@ class FramePipeline:
             out.stage_ms = {n: marks[i].elapsed_time(marks[i + 1]) for i, n in enumerate(names)}
             out.stage_ms["mu_raster_side_stream"] = mu_start.elapsed_time(mu_done)
         return out
+
+    # -- native per-frame path (st_frame_run) -------------------------------------------
+
+    def _plan_for(self, tri_dev, forced_iters, median_radius):
+        t = self.t
+        W, H = self.W, self.H
+        lib = N.lib()
+        P = getattr(self, "_plan", None)
+        if P is None:
+            P = N.StFramePlan()
+            P.frame = self.frame
+            P.rig = self.rig
+            for name, x in (("values", self.values), ("status", self.status),
+                            ("static_bits", self.sbits), ("valid_bits", self.vbits),
+                            ("image", self.image), ("prov", self.prov), ("n_rays", self.n_rays),
+                            ("scratch", self.scratch), ("stats_dev", self.stats_dev),
+                            ("solve_ws", self.solve_ws)):
+                setattr(P, name, x.data_ptr())
+            P.solve_ws_bytes = self.solve_ws.numel()
+            P.side_stream = self.side.cuda_stream
+            P.side2_stream = self.side2.cuda_stream
+            N.check(lib.st_frame_plan_init(N.C.byref(P)))
+            self._plan = P
+        P.params = N.make_params(self.params, self.prior_params, forced_iters, False)
+        P.median_radius = int(median_radius)
+        need = int(lib.st_mu_raster_workspace(W, H, tri_dev.n_tri))
+        if self.mu_ws.numel() < need:
+            self.mu_ws = empty((need,), t.uint8)
+        need = int(lib.st_support_workspace(tri_dev.n_sup, W, H,
+                                            float(self.prior_params.neighborhood_radius)))
+        if self.sup_ws.numel() < need:
+            self.sup_ws = empty((need,), t.uint8)
+        P.mu_ws, P.mu_ws_bytes = self.mu_ws.data_ptr(), self.mu_ws.numel()
+        P.sup_ws, P.sup_ws_bytes = self.sup_ws.data_ptr(), self.sup_ws.numel()
+        P.main_stream = t.cuda.current_stream().cuda_stream
+        P.descriptors_ready = 1 if getattr(self, "_desc_ready", False) else 0
+        self._desc_ready = False
+        return P
+
+    def run_native(self, tri_dev, forced_iters=0, median_radius=1, ready=None, out_stream=None,
+                   done=None):
+        """run() + fetch_async() for the dense solve in one native call
+        (st_frame_run): no per-stage Python, no host synchronisation.
+        Returns (pinned host block or None, AsyncStats)."""
+        t = self.t
+        P = self._plan_for(tri_dev, forced_iters, median_radius)
+        block = None
+        if out_stream is not None:
+            block = t.empty((int(N.lib().st_frame_host_bytes(self.W, self.H)),), dtype=t.uint8,
+                            pin_memory=True)
+            P.out_stream = out_stream.cuda_stream
+        else:
+            P.out_stream = None
+        N.check(N.lib().st_frame_run(
+            N.C.byref(P), N.C.byref(tri_dev.st), N.ptr(tri_dev.sup_uv), N.ptr(tri_dev.sup_d),
+            int(tri_dev.n_sup), ready, None if block is None else N.C.c_void_p(block.data_ptr()),
+            done))
+        return block, AsyncStats(-1)
+
+    def host_views(self, block):
+        """The artefacts inside an st_frame_run host block (its layout)."""
+        H, W = self.H, self.W
+        specs = ((np.float32, (H, W)), (np.uint8, (H, W)), (np.uint32, (H, W)),
+                 (np.uint32, (H, W)), (np.uint8, (H, W, 3)), (np.uint8, (H, W)),
+                 (np.uint8, (H, W)), (np.uint8, (N.C.sizeof(N.StStats),)))
+        raw = block.numpy()
+        out, o = [], 0
+        for dt, shape in specs:
+            n = int(np.prod(shape)) * np.dtype(dt).itemsize
+            out.append(raw[o:o + n].view(dt).reshape(shape))
+            o += (n + 255) & ~255
+        return out
+
+    def __del__(self):
+        P = getattr(self, "_plan", None)
+        if P is not None:
+            try:
+                N.lib().st_frame_plan_destroy(N.C.byref(P))
+            except Exception:  # noqa: BLE001 -- interpreter shutdown
+                pass
 
     def _event(self, timing=True):
         e = self.t.cuda.Event(enable_timing=timing)
@@ -360,20 +442,37 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
                 x.record_stream(st_)
         # the frame's pre-solve stages start as soon as its inputs are on the
         # device, overlapping the previous frame's EM on the main stream
-        stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
-                         median_radius=median_radius, ready=loaded)
-        t0 = tick("main_run", t0)
-        done = t.cuda.Event()
-        done.record(main)
-        with t.cuda.stream(out_s):
-            out_s.wait_event(done)
-            host = pipe.fetch_async(out_s)
-            flags = None
-            if check and td.flags is not None:
-                flags = t.empty((1,), dtype=t.int32, pin_memory=True)
-                flags.copy_(td.flags, non_blocking=True)
+        if not dynamic_only:
+            # one native call enqueues the whole frame and its D2H (st_frame_run)
             fetched = t.cuda.Event()
-            fetched.record(out_s)
+            fetched.record(out_s)  # creates the event; st_frame_run re-records it
+            block, stats = pipe.run_native(td, forced_iters=forced_iters,
+                                           median_radius=median_radius, ready=loaded,
+                                           out_stream=out_s, done=fetched)
+            host = pipe.host_views(block)
+            t0 = tick("main_run", t0)
+            with t.cuda.stream(out_s):
+                flags = None
+                if check and td.flags is not None:
+                    flags = t.empty((1,), dtype=t.int32, pin_memory=True)
+                    flags.copy_(td.flags, non_blocking=True)
+                    fetched = t.cuda.Event()
+                    fetched.record(out_s)
+        else:
+            stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
+                             median_radius=median_radius, ready=loaded)
+            t0 = tick("main_run", t0)
+            done = t.cuda.Event()
+            done.record(main)
+            with t.cuda.stream(out_s):
+                out_s.wait_event(done)
+                host = pipe.fetch_async(out_s)
+                flags = None
+                if check and td.flags is not None:
+                    flags = t.empty((1,), dtype=t.int32, pin_memory=True)
+                    flags.copy_(td.flags, non_blocking=True)
+                fetched = t.cuda.Event()
+                fetched.record(out_s)
         with free_lock:
             free[i % 2] = fetched
             free_lock.notify_all()
@@ -507,7 +606,14 @@ def reconstruct(frame, rig, tri, params=None, prior_params=None, dynamic_only=Fa
     h, w = frame.shape
     pipe = _pipeline_for(rig, w, h, params, prior_params)
     pipe.load(frame.images, frame.priors)
-    stats = pipe.run(TriDevice(tri), dynamic_only=dynamic_only, forced_iters=forced_iters,
+    td = TriDevice(tri)
+    if not dynamic_only:
+        cur = pipe.t.cuda.current_stream()
+        block, stats = pipe.run_native(td, forced_iters=forced_iters, median_radius=median_radius,
+                                       out_stream=cur)
+        cur.synchronize()
+        return _outputs_of(pipe, stats, pipe.host_views(block))
+    stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
                      median_radius=median_radius)
     return _outputs_of(pipe, stats, pipe.fetch())
 
