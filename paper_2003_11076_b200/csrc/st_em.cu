@@ -67,6 +67,89 @@ struct Energy {
   bool real;
 };
 
+#ifdef ENERGY_TWO_PASS
+// Channels 4p..4p+3 and 8+4p..8+4p+3 of one descriptor sample (words p and
+// p + 2), with exactly sample_desc's arithmetic.
+__device__ __forceinline__ void sample_words(const uint4* __restrict__ plane, int W,
+                                             const Taps& t, int p, double (&f)[8]) {
+  const size_t base = (size_t)t.iv * W + t.iu;
+  const uint4 a = __ldg(plane + base), b = __ldg(plane + base + t.su);
+  const uint32_t aw[2] = {p ? a.y : a.x, p ? a.w : a.z};
+  const uint32_t bw[2] = {p ? b.y : b.x, p ? b.w : b.z};
+  if (t.fv == 0.0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double g[4];
+      lerp_word(aw[h], bw[h], t.fu, g);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) f[4 * h + j] = g[j];
+    }
+  } else {
+    const uint4 e = __ldg(plane + base + t.sv), g = __ldg(plane + base + t.sv + t.su);
+    const uint32_t ew[2] = {p ? e.y : e.x, p ? e.w : e.z};
+    const uint32_t gw[2] = {p ? g.y : g.x, p ? g.w : g.z};
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int sh = 8 * j;
+        const double top = lerp_u8((aw[h] >> sh) & 0xff, (bw[h] >> sh) & 0xff, t.fu);
+        const double bot = lerp_u8((ew[h] >> sh) & 0xff, (gw[h] >> sh) & 0xff, t.fu);
+        f[4 * h + j] = dadd(top, dmul(t.fv, dsub(bot, top)));
+      }
+  }
+}
+
+// Same result as the single-pass form below with half the live channel
+// sums: a cheap count of the static in-margin rays first (too few -> the
+// penalty energy without sampling), then numpy's reduction tree in two
+// passes -- words {0, 2} give r0..r3, words {1, 3} give r4..r7.
+__device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, double d,
+                                            uint32_t bits, double lp) {
+  int cnt = 0;
+  for (int k = 0; k < c.rig.num_views; ++k)
+    if (((bits >> k) & 1u) && in_margin(c.rig, k, warp_ctx(c, k, u, v, d))) ++cnt;
+  Energy out;
+  out.real = cnt >= c.p.min_static_rays;
+  if (!out.real) {
+    out.e = dsub(dmul(c.p.beta, variance_ceiling()), lp);
+    return out;
+  }
+  const double nn = (double)cnt;
+  const double rn = c.recip[cnt];
+  double half[2];
+#pragma unroll 1
+  for (int p = 0; p < 2; ++p) {
+    double s1[8], s2[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s1[i] = 0.0;
+      s2[i] = 0.0;
+    }
+    for (int k = 0; k < c.rig.num_views; ++k) {
+      if (!((bits >> k) & 1u)) continue;
+      const WarpOut w = warp_ctx(c, k, u, v, d);
+      if (!in_margin(c.rig, k, w)) continue;
+      double f[8];
+      sample_words(c.desc + (size_t)k * c.HW, c.W, taps_ctx(c, w), p, f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s1[i] = dadd(s1[i], f[i]);
+        s2[i] = dadd(s2[i], dmul(f[i], f[i]));
+      }
+    }
+    double r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      r[j] = dadd(dsub(s2[j], div_small(dmul(s1[j], s1[j]), nn, rn)),
+                  dsub(s2[4 + j], div_small(dmul(s1[4 + j], s1[4 + j]), nn, rn)));
+    half[p] = dadd(dadd(r[0], r[1]), dadd(r[2], r[3]));
+  }
+  const double var = fmax(div_small(dadd(half[0], half[1]), nn, rn), 0.0);
+  out.e = dsub(dmul(c.p.beta, var), lp);
+  return out;
+}
+#else
 __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, double d,
                                             uint32_t bits, double lp) {
   double s1[16], s2[16];
@@ -110,6 +193,7 @@ __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, 
   out.e = dsub(dmul(c.p.beta, var), lp);
   return out;
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // block-deterministic reductions
@@ -489,8 +573,9 @@ __device__ __forceinline__ double score_exact(uint32_t m, Load& load, const doub
 // only the masks in that window are re-scored exactly (score_exact) under
 // the reference's tie rules -- normally one.  `exhaustive` re-scores every
 // admissible mask (the cross-check behind ST_ESTEP_EXHAUSTIVE).
-template <int K, typename Load>
-__device__ __forceinline__ uint32_t estep_small(Load& load, const double* l1, const double* l0,
+template <int K, typename Load, typename Load32>
+__device__ __forceinline__ uint32_t estep_small(Load& load, Load32& load32, float eps32,
+                                                const double* l1, const double* l0,
                                                 uint32_t vbits, const st_params& p,
                                                 bool exhaustive) {
   constexpr int M = 1 << K;
@@ -506,21 +591,22 @@ __device__ __forceinline__ uint32_t estep_small(Load& load, const double* l1, co
   float s2u = 0.0f;
 #pragma unroll 1
   for (int w = 0; w < 4; ++w) {
-    double ref[4];
+    // fp32 samples straight from the taps (|error| <= eps32 each); the
+    // first valid view's error is a common shift the variance ignores
+    float ref[4];
 #pragma unroll
     for (int k = 0; k < K; ++k)  // compile-time view index keeps the taps in registers
-      if (k == k0) load(k, w, ref);
+      if (k == k0) load32(k, w, ref);
     float g[K][4];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      double x[4] = {0.0, 0.0, 0.0, 0.0};  // invalid rays hold 0
-      if ((vbits >> k) & 1) load(k, w, x);
+      float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // invalid rays hold 0
+      if ((vbits >> k) & 1) load32(k, w, x);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        g[k][j] = __double2float_rn(dsub(x[j], ref[j]));
+        g[k][j] = x[j] - ref[j];
         q[k] = fmaf(g[k][j], g[k][j], q[k]);
-        const float xf = __double2float_rn(x[j]);
-        s2u = fmaf(xf, xf, s2u);
+        s2u = fmaf(x[j], x[j], s2u);
       }
     }
 #pragma unroll
@@ -567,8 +653,12 @@ __device__ __forceinline__ uint32_t estep_small(Load& load, const double* l1, co
     sc[m] = pr - beta * v;
     if (!((uint32_t)m & ~vbits)) best32 = fmaxf(best32, sc[m]);
   }
+  // + sample perturbation: |d t_c| <= 2 eps sqrt(n t_c) + n eps^2, summed
+  // over 16 channels, n <= 5 (not divided by n: conservative)
   const float D = 2.0f * (fabsf(beta) * (64.0f * U * s2c + 2.0f * U * fmaxf(ceil32, s2c) +
-                                         7.1054274e-15f * s2u + 2.0f * U * ceil32) +
+                                         7.1054274e-15f * s2u + 2.0f * U * ceil32 +
+                                         2.0f * eps32 * sqrtf(80.0f * s2c) +
+                                         80.0f * eps32 * eps32) +
                           (2.0f * K + 6.0f) * U * lsum);
   const float thr = best32 - 2.0f * D;
   const bool all = exhaustive || !(thr > -INFINITY);  // non-finite bound: decide exhaustively
@@ -652,15 +742,27 @@ struct SmemRays {
   }
 };
 
+// fp32 view of the same rays: one rounding, |error| <= 2^-24 * 255 < 256u
+struct SmemRays32 {
+  const double* f;
+  int stride;
+  __device__ __forceinline__ void operator()(int k, int w, float (&x)[4]) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = __double2float_rn(f[(k * 16 + 4 * w + j) * stride]);
+  }
+};
+
 __device__ __forceinline__ uint32_t estep_dispatch(int K, const double* f, int stride,
                                                    const double* l1, const double* l0,
                                                    uint32_t vbits, const st_params& p) {
   SmemRays ld{f, stride};
+  SmemRays32 ld32{f, stride};
+  const float eps = 512.0f * 5.9604645e-08f;
   switch (K) {
-    case 2: return estep_small<2>(ld, l1, l0, vbits, p, false);
-    case 3: return estep_small<3>(ld, l1, l0, vbits, p, false);
-    case 4: return estep_small<4>(ld, l1, l0, vbits, p, false);
-    case 5: return estep_small<5>(ld, l1, l0, vbits, p, false);
+    case 2: return estep_small<2>(ld, ld32, eps, l1, l0, vbits, p, false);
+    case 3: return estep_small<3>(ld, ld32, eps, l1, l0, vbits, p, false);
+    case 4: return estep_small<4>(ld, ld32, eps, l1, l0, vbits, p, false);
+    case 5: return estep_small<5>(ld, ld32, eps, l1, l0, vbits, p, false);
     default: return estep_generic(K, f, stride, l1, l0, vbits, p);
   }
 }
@@ -684,6 +786,38 @@ __device__ __forceinline__ void desc_word(const uint32_t* __restrict__ plane, in
       const double bot = lerp_u8((e >> sh) & 0xff, (g >> sh) & 0xff, fu);
       f[j] = dadd(top, dmul(fv, dsub(bot, top)));
     }
+  }
+}
+
+// fp32 counterpart of desc_word for the screen: exact integer taps via the
+// 2^23 trick, one FFMA per lerp.  |f32 - f| <= 511u for one lerp (u = 2^-24,
+// taps <= 255), <= 2300u for the bilinear case.
+__device__ __forceinline__ void lerp_word32(uint32_t wa, uint32_t wb, float fu, float (&f)[4]) {
+  const uint32_t ea = wa & 0x00ff00ffu, eb = wb & 0x00ff00ffu;
+  const uint32_t oa = (wa >> 8) & 0x00ff00ffu, ob = (wb >> 8) & 0x00ff00ffu;
+  const uint32_t de = eb + 0x01000100u - ea;
+  const uint32_t dodd = ob + 0x01000100u - oa;
+  const uint32_t lanes[4] = {__byte_perm(de, 0u, 0x4410), __byte_perm(dodd, 0u, 0x4410),
+                             __byte_perm(de, 0u, 0x4432), __byte_perm(dodd, 0u, 0x4432)};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float g0 = __fsub_rn(__uint_as_float(__byte_perm(wa, 0x4b000000u, 0x7440 | j)),
+                               8388608.0f);  // 2^23 + byte, exact
+    const float df = __fsub_rn(__uint_as_float(0x4b000000u | lanes[j]), 8388864.0f);
+    f[j] = fmaf(fu, df, g0);
+  }
+}
+
+template <bool RECT>
+__device__ __forceinline__ void desc_word32(const uint32_t* __restrict__ plane, int idx, int su,
+                                            int sv, float fu, float fv, int w, float (&f)[4]) {
+  const uint32_t* p = plane + (size_t)idx * 4 + w;
+  lerp_word32(__ldg(p), __ldg(p + 4 * su), fu, f);
+  if (!RECT && fv != 0.0f) {
+    float bot[4];
+    lerp_word32(__ldg(p + 4 * (size_t)sv), __ldg(p + 4 * ((size_t)sv + su)), fu, bot);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) f[j] = fmaf(fv, bot[j] - f[j], f[j]);
   }
 }
 
@@ -730,7 +864,12 @@ __global__ void __launch_bounds__(ESTEP_TAPS_BLOCK, ESTEP_MIN_BLOCKS) k_e_step_t
     desc_word<RECT>(desc + (size_t)k * c.HW * 4, idx[k], su, sv, fu[k], RECT ? 0.0 : fv[k], w,
                     x);
   };
-  const uint32_t m = estep_small<KT>(load, l1, l0, vb, c.p, a.exhaustive != 0);
+  auto load32 = [&](int k, int w, float (&x)[4]) {
+    desc_word32<RECT>(desc + (size_t)k * c.HW * 4, idx[k], su, sv, (float)fu[k],
+                      RECT ? 0.0f : (float)fv[k], w, x);
+  };
+  const float eps = (RECT ? 1024.0f : 4096.0f) * 5.9604645e-08f;
+  const uint32_t m = estep_small<KT>(load, load32, eps, l1, l0, vb, c.p, a.exhaustive != 0);
   const int64_t o = a.scatter ? pix : i;
   a.static_out[o] = m;
   a.valid_out[o] = vb;

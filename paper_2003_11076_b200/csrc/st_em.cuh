@@ -6,9 +6,13 @@
 #include "st_common.cuh"
 
 #define EM_BLOCK 128
-// 4 resident blocks per SM (<= 128 registers): measured fastest on B200
+// M-step energies in two passes of 8 channel sums (energy_at), 5 resident
+// blocks per SM (<= 96 registers): measured fastest on B200
+#ifndef ENERGY_SINGLE_PASS
+#define ENERGY_TWO_PASS
+#endif
 #ifndef MSTEP_MIN_BLOCKS
-#define MSTEP_MIN_BLOCKS 4
+#define MSTEP_MIN_BLOCKS 5
 #endif
 #define MSTEP_BOUNDS __launch_bounds__(EM_BLOCK, MSTEP_MIN_BLOCKS)
 #define STATS_BLOCK 256
