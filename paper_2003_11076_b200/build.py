@@ -69,7 +69,7 @@ def build(force=False, verbose=False, jobs=None, defines=(), out=None):
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout.decode(errors="replace"))
     os.replace(tmp, lib)
-    with open(lib + ".ptxas.log" if out else os.path.join(LIBDIR, "ptxas.log"), "w") as fh:
+    with open(lib + ".ptxas.log", "w") as fh:  # ptxas -v: registers / spills per kernel
         fh.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))

@@ -254,12 +254,30 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
     double be = INFINITY, bd = INFINITY;
     bool br = false;
     double lim = INFINITY;  // pruning radius of the current incumbent
+    // Iterations >= 2: the previous disparity is one of this pixel's
+    // candidates (the set is fixed per solve) and its energy under the new
+    // mask is needed for the statistics anyway (solver.py:468-471).  The
+    // winner is the order-independent lexicographic (E, d) minimum, so
+    // evaluating it first only seeds the incumbent -- and the pruning.
+    double dp = NAN, pe = NAN;
+    if (!a.first) {
+      dp = a.d[i];  // previous disparity (in place)
+      if (!isnan(dp)) {
+        const Energy E = energy_at(c, u, v, dp, bits,
+                                   log_prior(dp, mu, c.p.sigma, c.p.gamma, c.inv_sigma));
+        pe = E.e;
+        be = E.e;
+        bd = dp;
+        br = E.real;
+        lim = prune_radius(be, c.sigma_f, c.gamma_f);
+      }
+    }
     auto offer = [&](double d) {
       ++n_cand;
       // -log prior bounds the energy from below (var >= 0): exact pruning
       // (solver.py:341-347).  Candidates beyond the incumbent's radius are
       // certainly pruned; the rest get the exact fp64 comparison.
-      if (fabs(d - mu) > lim) return;
+      if (fabs(d - mu) > lim || d == bd) return;  // (d == bd: same energy, no change)
       const double lp = log_prior(d, mu, c.p.sigma, c.p.gamma, c.inv_sigma);
       if (!(-lp <= be)) return;
       ++n_eval;
@@ -298,10 +316,6 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
       status = ST_STATUS_NO_STATIC_EVIDENCE;
     }
     if (!a.first) {
-      const double dp = a.d[i];  // previous disparity (in place)
-      double pe = NAN;
-      if (!isnan(dp))
-        pe = energy_at(c, u, v, dp, bits, log_prior(dp, mu, c.p.sigma, c.p.gamma, c.inv_sigma)).e;
       a.pe[i] = pe;
       // |d - d_prev| > 0.5 with NaN -> False (solver.py:472-475)
       a.chg[i] = fabs(bd - dp) > 0.5 ? 1 : 0;
