@@ -290,15 +290,9 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
       }
     };
 
-    // band mu + 0.5 j, nearest first (solver.py:187-191, 360-363)
-    for (int j = 0; j < c.n_band; ++j) {
-      const double d = dadd(mu, c.band[j]);
-      if (d > 0.0 && d <= dmax) offer(d);
-    }
-    // coarse sweep 1, 5, 9, ... (solver.py:192, 364-365)
-    for (int j = 0; j < c.n_coarse; ++j) offer(dadd(1.0, dmul(4.0, (double)j)));
     // support disparities within the radius (solver.py:286-321, 373-400)
-    if (c.sup_tile_start) {
+    auto support = [&]() {
+      if (!c.sup_tile_start) return;
       // one bit test per distinct support value of the pixel's tile
       const int tile = (y / ST_TH) * c.tiles_x + (x / ST_TW);
       const uint32_t g1 = __ldg(c.sup_tile_start + tile + 1);
@@ -306,7 +300,15 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
       for (uint32_t g = __ldg(c.sup_tile_start + tile); g < g1; ++g)
         if ((__ldg(c.sup_mask + (size_t)g * ST_TH + row) >> col) & 1u)
           offer((double)__ldg(c.sup_value + g));
+    };
+    // band mu + 0.5 j, nearest first (solver.py:187-191, 360-363)
+    for (int j = 0; j < c.n_band; ++j) {
+      const double d = dadd(mu, c.band[j]);
+      if (d > 0.0 && d <= dmax) offer(d);
     }
+    // coarse sweep 1, 5, 9, ... (solver.py:192, 364-365)
+    for (int j = 0; j < c.n_coarse; ++j) offer(dadd(1.0, dmul(4.0, (double)j)));
+    support();
 
     uint8_t status = ST_STATUS_VALID;
     if (!isfinite(be)) {
