@@ -577,8 +577,13 @@ def run_ours(args):
     s0 = stats[-1]
     ms_m = float(np.mean([s.kernel_ms[0] for s in stats]))
     n_m = s0.kernel_launches[0]
-    samples_m = s0.candidates_total + s0.prev_evals     # candidate energies the model charges
-    bytes_m = samples_m * k * 16                          # 16 B per (candidate, view)
+    # 16 B per (pixel, candidate, view) descriptor sample.  The
+    # kernel samples only the energies it evaluates exactly: the survivors of
+    # the exact -log prior pruning plus the previous-disparity energies
+    # (<= K static views each).  The SURVEY model charges every candidate.
+    samples_m = s0.energy_evals + s0.prev_evals
+    bytes_m = samples_m * k * 16
+    model_bytes_m = (s0.candidates_total + s0.prev_evals) * k * 16
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(peaks_path):
         peak = float(json.load(open(peaks_path))["hbm_gbs"])
@@ -586,6 +591,7 @@ def run_ours(args):
     else:
         peak, peak_src = 6650.0, "fallback"
     achieved = bytes_m / (ms_m / 1e3) / 1e9
+    model_achieved = model_bytes_m / (ms_m / 1e3) / 1e9
     npx = w * h
     c_bar = s0.candidates_total / max(1, s0.msteps)
     # SURVEY 8d model, charged for the pixel M/E-steps the incremental EM runs
@@ -625,8 +631,14 @@ def run_ours(args):
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "algorithmic_bytes_per_launch": bytes_m / max(1, n_m),
+                     "unit_note": "16 B per evaluated (pixel, candidate, static view) "
+                                  "descriptor sample (<= K views counted)",
                      "launch_ms": ms_m / max(1, n_m), "launches_per_step": n_m,
-                     "share_of_step": ms_m / step_ms_mean},
+                     "share_of_step": ms_m / step_ms_mean,
+                     "model": {"algorithmic_bytes_per_launch": model_bytes_m / max(1, n_m),
+                               "achieved": model_achieved, "frac": model_achieved / peak,
+                               "note": "SURVEY 8d charges every candidate; exact pruning "
+                                       "evaluates ~20 % of them, hence frac > 1"}},
         "frame_roofline": {"model_bytes": frame_bytes, "achieved_gbs":
                            frame_bytes / (step_ms_mean / 1e3) / 1e9,
                            "frac": frame_bytes / (step_ms_mean / 1e3) / 1e9 / peak,
