@@ -137,3 +137,51 @@ def test_device_harvest_full_size(st, cfg):
     assert np.array_equal(np.array([[p.u, p.v] for p in fin]), z["support_uv"])
     assert np.array_equal(np.array([p.d for p in fin]), z["support_d"])
     assert np.array_equal(np.array([p.source_view for p in fin]), z["support_src"])
+
+
+@pytest.mark.gpu
+def test_frame_in_path_matches_reference_inputs(st):
+    """reconstruct_frame (device harvest -> native dedup -> host Qhull ->
+    device planes/transforms -> solve -> refocus) reproduces the
+    triangulation built from the reference's own support list and the
+    outputs of reconstruct() on it; reconstruct_frames streams the same."""
+    import bench
+    frame, rig, tri_ref, exact = bench.load_inputs("C1")
+    assert exact
+    sp, pp = bench.params_for("C1")
+    rec, tri = st.reconstruct_frame(frame, rig, sp, pp)
+    assert np.array_equal(tri.points, tri_ref.points)
+    assert np.array_equal(tri.disparities, tri_ref.disparities)
+    assert np.array_equal(tri.triangles, tri_ref.triangles)
+    ref = st.reconstruct(frame, rig, tri_ref, sp, pp)
+    for a, b in ((rec.disparity.values, ref.disparity.values), (rec.image, ref.image),
+                 (rec.segmentation.static_bits, ref.segmentation.static_bits),
+                 (rec.provenance, ref.provenance), (rec.n_rays, ref.n_rays)):
+        assert np.array_equal(a, b)
+    assert rec.stats.mean_energy == ref.stats.mean_energy
+    outs = list(st.reconstruct_frames([frame] * 3, rig, sp, pp, workers=2))
+    assert len(outs) == 3
+    for o in outs:
+        assert np.array_equal(o.disparity.values, ref.disparity.values)
+        assert np.array_equal(o.image, ref.image)
+
+
+@pytest.mark.gpu
+def test_stream_equals_single_calls(st):
+    """reconstruct_stream (native st_frame_run path, and the Python path for
+    dynamic_only) == reconstruct() frame by frame."""
+    import bench
+    frame, rig, tri, _ = bench.load_inputs("C1")
+    sp, pp = bench.params_for("C1")
+    for dyn in (False, True):
+        ref = st.reconstruct(frame, rig, tri, sp, pp, dynamic_only=dyn)
+        outs = list(st.reconstruct_stream([(frame, tri)] * 4, rig, sp, pp, dynamic_only=dyn))
+        assert len(outs) == 4
+        for o in outs:
+            for a, b in ((o.disparity.values, ref.disparity.values), (o.image, ref.image),
+                         (o.segmentation.static_bits, ref.segmentation.static_bits),
+                         (o.segmentation.valid_bits, ref.segmentation.valid_bits),
+                         (o.provenance, ref.provenance)):
+                assert np.array_equal(a, b)
+            assert o.stats.iterations_run == ref.stats.iterations_run
+            assert o.stats.mean_energy == ref.stats.mean_energy
