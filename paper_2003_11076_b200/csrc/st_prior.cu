@@ -11,11 +11,11 @@
 namespace st {
 
 // ---------------------------------------------------------------------------
-// support candidate lists.  A record is (tile, fp32 disparity, packed u|v)
-// for every support point whose radius-r disk bbox touches the tile.  After
-// a radix sort on (tile, value) each tile's records are grouped by value, so
-// a pixel dedups candidates by walking value groups (solver.py:316-321 keeps
-// unique (pixel, value) pairs).
+// support candidate lists.  A record is (fp32 disparity, packed u|v) in the
+// bucket of every 32x8 tile its radius-r disk bbox touches.  Each bucket is
+// sorted by value in shared memory and its records grouped by value, so a
+// pixel dedups candidates by walking value groups (solver.py:316-321 keeps
+// unique (pixel, value) pairs) and tests one coverage bit per group.
 
 struct SupGeom {
   int W, H, tiles_x, tiles_y, ir;
@@ -40,102 +40,166 @@ __device__ __forceinline__ bool sup_range(const SupGeom& g, double su, double sv
   return true;
 }
 
-__global__ void k_sup_count(const double* __restrict__ uv, const double* __restrict__ d, int n,
-                            SupGeom g, uint32_t* __restrict__ counts) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int tx0, tx1, ty0, ty1, pu, pv;
-  float val;
-  counts[i] = sup_range(g, uv[2 * i], uv[2 * i + 1], d[i], tx0, tx1, ty0, ty1, val, pu, pv)
-                  ? (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1))
-                  : 0u;
+// One point's 32x8 coverage rows in tile (tx, ty): the pixels inside its
+// disk (solver.py:290-308: du^2 + dv^2 <= r^2, |du|, |dv| <= floor(r), in the
+// image), dx range compared in double like numpy.
+__device__ __forceinline__ uint32_t cover_row(const SupGeom& g, double r2, int tx, int ty,
+                                              int pu, int pv, int r) {
+  const int y = ty * ST_TH + r;
+  if (y >= g.H) return 0u;
+  const int dy = y - pv;
+  if (abs(dy) > g.ir) return 0u;
+  int dxm = (int)floor(sqrt(fmax(r2 - (double)(dy * dy), 0.0)));
+  while ((double)((dxm + 1) * (dxm + 1) + dy * dy) <= r2) ++dxm;
+  while (dxm >= 0 && (double)(dxm * dxm + dy * dy) > r2) --dxm;
+  if (dxm < 0) return 0u;
+  dxm = min(dxm, g.ir);
+  const int x0 = max(max(pu - dxm, tx * ST_TW), 0);
+  const int x1 = min(min(pu + dxm, tx * ST_TW + ST_TW - 1), g.W - 1);
+  if (x0 > x1) return 0u;
+  const int c0 = x0 - tx * ST_TW, nbits = x1 - x0 + 1;
+  return (nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u)) << c0;
 }
 
-__global__ void k_sup_emit(const double* __restrict__ uv, const double* __restrict__ d, int n,
-                           SupGeom g, const uint32_t* __restrict__ offs,
-                           unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+// Records per tile: every support point whose disk bbox touches the tile.
+__global__ void k_tile_count(const double* __restrict__ uv, const double* __restrict__ d, int n,
+                             SupGeom g, uint32_t* __restrict__ cnt) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int tx0, tx1, ty0, ty1, pu, pv;
   float val;
   if (!sup_range(g, uv[2 * i], uv[2 * i + 1], d[i], tx0, tx1, ty0, ty1, val, pu, pv)) return;
-  uint32_t o = offs[i];
-  const uint32_t packed = ((uint32_t)(uint16_t)(int16_t)pu) | ((uint32_t)(uint16_t)(int16_t)pv << 16);
   for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx, ++o) {
-      keys[o] = ((unsigned long long)(ty * g.tiles_x + tx) << 32) | __float_as_uint(val);
-      vals[o] = packed;
+    for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(cnt + ty * g.tiles_x + tx, 1u);
+}
+
+// Scatter the records into their tile's bucket (order inside a bucket is
+// irrelevant: the bucket is sorted by value next).
+__global__ void k_tile_fill(const double* __restrict__ uv, const double* __restrict__ d, int n,
+                            SupGeom g, const uint32_t* __restrict__ off,
+                            uint32_t* __restrict__ fill, unsigned long long* __restrict__ recs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int tx0, tx1, ty0, ty1, pu, pv;
+  float val;
+  if (!sup_range(g, uv[2 * i], uv[2 * i + 1], d[i], tx0, tx1, ty0, ty1, val, pu, pv)) return;
+  const uint32_t packed = ((uint32_t)(uint16_t)(int16_t)pu) | ((uint32_t)(uint16_t)(int16_t)pv << 16);
+  const unsigned long long rec = ((unsigned long long)__float_as_uint(val) << 32) | packed;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      const int t = ty * g.tiles_x + tx;
+      recs[off[t] + atomicAdd(fill + t, 1u)] = rec;
     }
 }
 
-// After the sort: records with equal (tile, value) form one group.  heads[i]
-// flags the first record of each group.
-// n_dev (nullable): the record count on the device -- launches sized by an
-// upper bound then clear the flags of the padding records.
-__global__ void k_sup_heads(const unsigned long long* __restrict__ keys, int64_t n_rec,
-                            uint32_t* __restrict__ heads, const uint32_t* n_dev) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_rec) return;
-  const int64_t n = n_dev ? (int64_t)*n_dev : n_rec;
-  heads[i] = i < n && (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+#define TILE_CAP 2048  // records sorted in shared memory (more: in place, global)
+
+// In-block bitonic sort of n keys (padded to a power of two with ~0).
+__device__ void block_sort(unsigned long long* k, int n) {
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  for (int i = n + threadIdx.x; i < p2; i += blockDim.x) k[i] = ~0ull;
+  __syncthreads();
+  for (int size = 2; size <= p2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const unsigned long long a = k[lo], b = k[hi];
+        if ((a > b) == up) {
+          k[lo] = b;
+          k[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
 }
 
-// Each record ORs the pixels of its tile inside its disk (solver.py:290-308:
-// du^2 + dv^2 <= r^2, |du|, |dv| <= floor(r), in the image) into its group's
-// 32x8 coverage mask; group heads also publish the group's key and value.
-__global__ void k_sup_cover(const unsigned long long* __restrict__ keys,
-                            const uint32_t* __restrict__ vals, const uint32_t* __restrict__ gid_incl,
-                            int64_t n_rec, SupGeom g, double r2,
-                            unsigned long long* __restrict__ gkey, float* __restrict__ gvalue,
-                            uint32_t* __restrict__ gmask, const uint32_t* n_dev) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (n_dev ? (int64_t)*n_dev : n_rec)) return;
-  const unsigned long long key = keys[i];
-  const uint32_t grp = gid_incl[i] - 1;
-  if (i == 0 || keys[i - 1] != key) {
-    gkey[grp] = key;
-    gvalue[grp] = __uint_as_float((uint32_t)(key & 0xffffffffull));
+// One block per tile: sort its records by (value, point), one group per
+// distinct value, each record ORs its disk rows into its group's mask.
+// Groups land at the tile's record offset (scratch); ngroups per tile.
+__global__ void k_tile_groups(SupGeom g, double r2, const uint32_t* __restrict__ cnt,
+                              const uint32_t* __restrict__ off, unsigned long long* recs,
+                              float* __restrict__ tvalue, uint32_t* __restrict__ tmask,
+                              uint32_t* __restrict__ ngroups) {
+  extern __shared__ unsigned long long sh[];
+  __shared__ uint32_t s_ng;
+  const int t = blockIdx.x;
+  const int n = (int)cnt[t];
+  const uint32_t base = off[t];
+  if (n == 0) {
+    if (threadIdx.x == 0) ngroups[t] = 0u;
+    return;
   }
-  const int tile = (int)(key >> 32);
-  const int tx = tile % g.tiles_x, ty = tile / g.tiles_x;
-  const uint32_t uv = vals[i];
-  const int pu = (int)(int16_t)(uv & 0xffffu), pv = (int)(int16_t)(uv >> 16);
-  for (int r = 0; r < ST_TH; ++r) {
-    const int y = ty * ST_TH + r;
-    if (y >= g.H) break;
-    const int dy = y - pv;
-    if (abs(dy) > g.ir) continue;
-    // largest |dx| with dx^2 + dy^2 <= r^2 (compared in double like numpy)
-    int dxm = (int)floor(sqrt(fmax(r2 - (double)(dy * dy), 0.0)));
-    while ((double)((dxm + 1) * (dxm + 1) + dy * dy) <= r2) ++dxm;
-    while (dxm >= 0 && (double)(dxm * dxm + dy * dy) > r2) --dxm;
-    if (dxm < 0) continue;
-    dxm = min(dxm, g.ir);
-    const int x0 = max(max(pu - dxm, tx * ST_TW), 0);
-    const int x1 = min(min(pu + dxm, tx * ST_TW + ST_TW - 1), g.W - 1);
-    if (x0 > x1) continue;
-    const int c0 = x0 - tx * ST_TW, nbits = x1 - x0 + 1;
-    const uint32_t bits = (nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u)) << c0;
-    atomicOr(gmask + (size_t)grp * ST_TH + r, bits);
+  const bool in_smem = n <= TILE_CAP;
+  unsigned long long* k = in_smem ? sh : recs + base;  // large buckets: sort in place
+  uint32_t* gid = reinterpret_cast<uint32_t*>(sh + TILE_CAP);
+  if (in_smem) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) k[i] = recs[base + i];
+    block_sort(k, n);
+  } else {
+    // odd-even transposition sort in place in global memory: buckets this
+    // large do not occur for de-duplicated support sets (at most one point
+    // per pixel); kept correct, not fast
+    for (int round = 0; round < n; ++round) {
+      for (int i = 2 * threadIdx.x + (round & 1); i + 1 < n; i += 2 * blockDim.x) {
+        const unsigned long long a = k[i], b = k[i + 1];
+        if (a > b) {
+          k[i] = b;
+          k[i + 1] = a;
+        }
+      }
+      __syncthreads();
+    }
   }
+  // group ids (value = high 32 bits): serial scan by thread 0 over heads is
+  // cheap at these sizes; masks accumulate in scratch (global) for large
+  // buckets, in shared memory otherwise
+  if (threadIdx.x == 0) {
+    uint32_t gcur = 0;
+    for (int i = 0; i < n; ++i) {
+      if (i > 0 && (k[i] >> 32) != (k[i - 1] >> 32)) ++gcur;
+      if (in_smem) gid[i] = gcur;
+    }
+    s_ng = gcur + 1;
+  }
+  __syncthreads();
+  const uint32_t ng = s_ng;
+  const int tx = t % g.tiles_x, ty = t / g.tiles_x;
+  // masks: tmask (scratch, at the tile's record offset) zeroed, then ORed
+  for (uint32_t i = threadIdx.x; i < ng * ST_TH; i += blockDim.x) tmask[(size_t)base * ST_TH + i] = 0u;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    uint32_t grp;
+    if (in_smem) {
+      grp = gid[i];
+    } else {  // first record of this value = number of distinct values before it
+      grp = 0;
+      for (int j = 1; j <= i; ++j) grp += (k[j] >> 32) != (k[j - 1] >> 32);
+    }
+    const uint32_t uv = (uint32_t)(k[i] & 0xffffffffull);
+    const int pu = (int)(int16_t)(uv & 0xffffu), pv = (int)(int16_t)(uv >> 16);
+    if (i == 0 || (k[i] >> 32) != (k[i - 1] >> 32))
+      tvalue[base + grp] = __uint_as_float((uint32_t)(k[i] >> 32));
+#pragma unroll
+    for (int r = 0; r < ST_TH; ++r) {
+      const uint32_t bits = cover_row(g, r2, tx, ty, pu, pv, r);
+      if (bits) atomicOr(tmask + ((size_t)base + grp) * ST_TH + r, bits);
+    }
+  }
+  if (threadIdx.x == 0) ngroups[t] = ng;
 }
 
-__global__ void k_sup_group_start(const unsigned long long* __restrict__ gkey,
-                                  const uint32_t* __restrict__ n_groups_ptr, int n_tiles,
-                                  uint32_t* __restrict__ tile_start) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > n_tiles) return;
-  // lower_bound of tile i in the sorted group keys
-  int64_t lo = 0, hi = n_groups_ptr ? (int64_t)*n_groups_ptr : 0;
-  const unsigned long long want = (unsigned long long)i << 32;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (gkey[mid] < want)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  tile_start[i] = (uint32_t)lo;
+// Compact every tile's groups to the scanned group offsets.
+__global__ void k_tile_compact(const uint32_t* __restrict__ off, const uint32_t* __restrict__ ngroups,
+                               const uint32_t* __restrict__ gstart, const float* __restrict__ tvalue,
+                               const uint32_t* __restrict__ tmask, float* __restrict__ gvalue,
+                               uint32_t* __restrict__ gmask) {
+  const int t = blockIdx.x;
+  const uint32_t ng = ngroups[t], src = off[t], dst = gstart[t];
+  for (uint32_t i = threadIdx.x; i < ng; i += blockDim.x) gvalue[dst + i] = tvalue[src + i];
+  for (uint32_t i = threadIdx.x; i < ng * ST_TH; i += blockDim.x)
+    gmask[(size_t)dst * ST_TH + i] = tmask[(size_t)src * ST_TH + i];
 }
 
 }  // namespace st
@@ -148,8 +212,7 @@ namespace {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct SupLayout {
-  size_t counts, offs, keys_in, keys_out, vals_in, vals_out, heads, gid, gkey, gvalue, gmask,
-      tile_start, cub, total;
+  size_t cnt, off, fill, ng, gstart, recs, tvalue, tmask, gvalue, gmask, cub, total;
   size_t cub_bytes;
   int64_t max_rec;
   int tiles_x, tiles_y;
@@ -167,30 +230,23 @@ SupLayout sup_layout(int n, int W, int H, double radius) {
   L.tiles_y = (H + ST_TH - 1) / ST_TH;
   const int n_tiles = L.tiles_x * L.tiles_y;
   L.max_rec = (int64_t)n * tiles_per_point_max(ir < 0 ? 0 : ir);
-  size_t scan_bytes = 0, sort_bytes = 0, incl_bytes = 0;
-  const int mr = (int)(L.max_rec > 0 ? L.max_rec : 1);
+  size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                n + 1);
-  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (unsigned long long*)nullptr,
-                                  (unsigned long long*)nullptr, (uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, mr);
-  cub::DeviceScan::InclusiveSum(nullptr, incl_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, mr);
-  L.cub_bytes = std::max(scan_bytes, std::max(sort_bytes, incl_bytes));
-  const size_t R = (size_t)L.max_rec + 1;
+                                n_tiles + 1);
+  L.cub_bytes = scan_bytes;
+  const size_t R = (size_t)L.max_rec + 1, T = (size_t)n_tiles + 1;
   size_t o = 0;
-  L.counts = o;     o += align_up(sizeof(uint32_t) * (n + 1));
-  L.offs = o;       o += align_up(sizeof(uint32_t) * (n + 1));
-  L.keys_in = o;    o += align_up(sizeof(unsigned long long) * R);
-  L.keys_out = o;   o += align_up(sizeof(unsigned long long) * R);
-  L.vals_in = o;    o += align_up(sizeof(uint32_t) * R);
-  L.vals_out = o;   o += align_up(sizeof(uint32_t) * R);
-  L.heads = o;      o += align_up(sizeof(uint32_t) * R);
-  L.gid = o;        o += align_up(sizeof(uint32_t) * R);
-  L.gkey = o;       o += align_up(sizeof(unsigned long long) * R);
-  L.gvalue = o;     o += align_up(sizeof(float) * R);
-  L.gmask = o;      o += align_up(sizeof(uint32_t) * ST_TH * R);
-  L.tile_start = o; o += align_up(sizeof(uint32_t) * (n_tiles + 1));
-  L.cub = o;        o += align_up(L.cub_bytes);
+  L.cnt = o;    o += align_up(sizeof(uint32_t) * T);
+  L.fill = o;   o += align_up(sizeof(uint32_t) * T);
+  L.off = o;    o += align_up(sizeof(uint32_t) * T);
+  L.ng = o;     o += align_up(sizeof(uint32_t) * T);
+  L.gstart = o; o += align_up(sizeof(uint32_t) * T);
+  L.recs = o;   o += align_up(sizeof(unsigned long long) * R);
+  L.tvalue = o; o += align_up(sizeof(float) * R);
+  L.tmask = o;  o += align_up(sizeof(uint32_t) * ST_TH * R);
+  L.gvalue = o; o += align_up(sizeof(float) * R);
+  L.gmask = o;  o += align_up(sizeof(uint32_t) * ST_TH * R);
+  L.cub = o;    o += align_up(L.cub_bytes);
   L.total = o;
   return L;
 }
@@ -213,19 +269,16 @@ extern "C" int st_support_build(const double* support_uv, const double* support_
     return ST_ENOMEM;
   }
   char* ws = (char*)workspace;
-  uint32_t* counts = (uint32_t*)(ws + L.counts);
-  uint32_t* offs = (uint32_t*)(ws + L.offs);
-  auto* keys_in = (unsigned long long*)(ws + L.keys_in);
-  auto* keys_out = (unsigned long long*)(ws + L.keys_out);
-  uint32_t* vals_in = (uint32_t*)(ws + L.vals_in);
-  uint32_t* vals_out = (uint32_t*)(ws + L.vals_out);
-  uint32_t* tile_start = (uint32_t*)(ws + L.tile_start);
-  uint32_t* heads = (uint32_t*)(ws + L.heads);
-  uint32_t* gid = (uint32_t*)(ws + L.gid);
-  auto* gkey = (unsigned long long*)(ws + L.gkey);
+  uint32_t* cnt = (uint32_t*)(ws + L.cnt);
+  uint32_t* fill = (uint32_t*)(ws + L.fill);
+  uint32_t* off = (uint32_t*)(ws + L.off);
+  uint32_t* ng = (uint32_t*)(ws + L.ng);
+  uint32_t* gstart = (uint32_t*)(ws + L.gstart);
+  auto* recs = (unsigned long long*)(ws + L.recs);
+  float* tvalue = (float*)(ws + L.tvalue);
+  uint32_t* tmask = (uint32_t*)(ws + L.tmask);
   float* gvalue = (float*)(ws + L.gvalue);
   uint32_t* gmask = (uint32_t*)(ws + L.gmask);
-  void* cub_tmp = ws + L.cub;
   const int n_tiles = L.tiles_x * L.tiles_y;
 
   st::SupGeom g;
@@ -235,61 +288,41 @@ extern "C" int st_support_build(const double* support_uv, const double* support_
   g.tiles_y = L.tiles_y;
   g.ir = (int)floor(p->neighborhood_radius);
   g.d_max = p->d_max;
+  const double r = p->neighborhood_radius;
 
-  int64_t total = 0;
+  // per-tile buckets: count, scan, fill -- no host round trip
+  ST_CUDA_CHECK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (n_tiles + 1), s));
+  ST_CUDA_CHECK(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * (n_tiles + 1), s));
   if (n > 0) {
-    ST_CUDA_CHECK(cudaMemsetAsync(counts + n, 0, sizeof(uint32_t), s));
-    st::k_sup_count<<<(n + 255) / 256, 256, 0, s>>>(support_uv, support_d, n, g, counts);
-    ST_LAUNCH_CHECK("k_sup_count");
-    size_t tb = L.cub_bytes;
-    ST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, counts, offs, n + 1, s));
-    sthost::count_launch();
-    // n_records == NULL: no host round trip -- every later launch is sized
-    // by the bound max_rec, padding keys (all ones) sort after the real
-    // records and the kernels read the real count offs[n] on the device.
-    const bool async = n_records == nullptr;
-    const uint32_t* total_dev = async ? offs + n : nullptr;
-    if (async) {
-      total = L.max_rec;
-      ST_CUDA_CHECK(cudaMemsetAsync(keys_in, 0xff, sizeof(unsigned long long) * (size_t)total, s));
-    } else {
-      uint32_t host_total = 0;
-      ST_CUDA_CHECK(cudaMemcpyAsync(&host_total, offs + n, sizeof(uint32_t),
-                                    cudaMemcpyDeviceToHost, s));
-      ST_CUDA_CHECK(cudaStreamSynchronize(s));
-      total = host_total;
-    }
-    if (total > 0) {
-      st::k_sup_emit<<<(n + 255) / 256, 256, 0, s>>>(support_uv, support_d, n, g, offs, keys_in,
-                                                      vals_in);
-      ST_LAUNCH_CHECK("k_sup_emit");
-      int tile_bits = 1;
-      while ((1ll << tile_bits) <= n_tiles) ++tile_bits;
-      tb = L.cub_bytes;
-      ST_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, keys_in, keys_out, vals_in,
-                                                    vals_out, (int)total, 0, 32 + tile_bits, s));
-      sthost::count_launch();
-      // (tile, value) groups and their 32x8 pixel coverage masks
-      const unsigned rb = (unsigned)((total + 255) / 256);
-      st::k_sup_heads<<<rb, 256, 0, s>>>(keys_out, total, heads, total_dev);
-      ST_LAUNCH_CHECK("k_sup_heads");
-      tb = L.cub_bytes;
-      ST_CUDA_CHECK(cub::DeviceScan::InclusiveSum(cub_tmp, tb, heads, gid, (int)total, s));
-      sthost::count_launch();
-      ST_CUDA_CHECK(cudaMemsetAsync(gmask, 0, sizeof(uint32_t) * ST_TH * (size_t)total, s));
-      const double r = p->neighborhood_radius;
-      st::k_sup_cover<<<rb, 256, 0, s>>>(keys_out, vals_out, gid, total, g, r * r, gkey, gvalue,
-                                         gmask, total_dev);
-      ST_LAUNCH_CHECK("k_sup_cover");
-    }
+    st::k_tile_count<<<(n + 255) / 256, 256, 0, s>>>(support_uv, support_d, n, g, cnt);
+    ST_LAUNCH_CHECK("k_tile_count");
   }
-  st::k_sup_group_start<<<(unsigned)((n_tiles + 1 + 255) / 256), 256, 0, s>>>(
-      gkey, total > 0 ? gid + total - 1 : nullptr, n_tiles, tile_start);
-  ST_LAUNCH_CHECK("k_sup_group_start");
-  frame->sup_tile_start = tile_start;
+  size_t tb = L.cub_bytes;
+  ST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws + L.cub, tb, cnt, off, n_tiles + 1, s));
+  sthost::count_launch();
+  if (n > 0) {
+    st::k_tile_fill<<<(n + 255) / 256, 256, 0, s>>>(support_uv, support_d, n, g, off, fill, recs);
+    ST_LAUNCH_CHECK("k_tile_fill");
+  }
+  // per tile: sort by value, one group per distinct value, coverage masks
+  const int smem = TILE_CAP * (int)(sizeof(unsigned long long) + sizeof(uint32_t));
+  st::k_tile_groups<<<n_tiles, 128, smem, s>>>(g, r * r, cnt, off, recs, tvalue, tmask, ng);
+  ST_LAUNCH_CHECK("k_tile_groups");
+  ST_CUDA_CHECK(cudaMemsetAsync(ng + n_tiles, 0, sizeof(uint32_t), s));
+  tb = L.cub_bytes;
+  ST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws + L.cub, tb, ng, gstart, n_tiles + 1, s));
+  sthost::count_launch();
+  st::k_tile_compact<<<n_tiles, 64, 0, s>>>(off, ng, gstart, tvalue, tmask, gvalue, gmask);
+  ST_LAUNCH_CHECK("k_tile_compact");
+  frame->sup_tile_start = gstart;
   frame->sup_value = gvalue;
   frame->sup_mask = gmask;
-  if (n_records) *n_records = total;
+  if (n_records) {  // diagnostics only: one host round trip
+    uint32_t total = 0;
+    ST_CUDA_CHECK(cudaMemcpyAsync(&total, off + n_tiles, sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, s));
+    ST_CUDA_CHECK(cudaStreamSynchronize(s));
+    *n_records = total;
+  }
   return ST_OK;
 }
-
