@@ -257,8 +257,10 @@ def triangulate_arrays(u, v, d, width, height, planes=True):
     disps = np.asarray(d, dtype=np.float64).copy()
     corners = np.array([[0.0, 0.0], [width - 1.0, 0.0], [0.0, height - 1.0],
                         [width - 1.0, height - 1.0]])
-    taken = {(int(c[0]), int(c[1])) for c in coords}
-    missing = [c for c in corners if (int(c[0]), int(c[1])) not in taken]
+    # prior.py:336-337 {(int(u), int(v))} membership, vectorised (int() truncates)
+    ci = np.trunc(coords)
+    missing = [c for c in corners
+               if not np.any((ci[:, 0] == np.trunc(c[0])) & (ci[:, 1] == np.trunc(c[1])))]
     n_anchor = 0
     if missing:
         _, nearest = cKDTree(coords).query(np.array(missing))
