@@ -93,7 +93,11 @@ class TriDevice:
     operation order (host tables are only shipped for non-integer vertex
     coordinates, outside st_tri_tables' exactness precondition)."""
 
-    def __init__(self, tri):
+    def __init__(self, tri, slot=None):
+        """slot (optional): an object with reusable `tri_stage` (pinned) and
+        `tri_buf` (device) tensors -- a FramePipeline slot whose previous
+        frame has finished -- instead of the shared staging ring and a fresh
+        device allocation."""
         import torch
         from .device import dev
         dl = delaunay_of(tri)
@@ -126,13 +130,32 @@ class TriDevice:
             dev_total += (n_tri * 48 + 255) & ~255
             t_flags = dev_total
             dev_total += 256
-        i, stage = _STAGING.take(total)
+        if slot is None:
+            i, stage = _STAGING.take(total)
+        else:
+            ev = getattr(slot, "tri_stage_event", None)
+            if ev is not None:
+                ev.synchronize()  # the slot's previous upload has left the staging buffer
+            if getattr(slot, "tri_stage", None) is None or slot.tri_stage.numel() < total:
+                slot.tri_stage = torch.empty(max(total, 1 << 20) * 5 // 4, dtype=torch.uint8,
+                                             pin_memory=True)
+            stage = slot.tri_stage
         host = stage.numpy()
         for (_, a), o in zip(parts, offs):
             np.copyto(host[o:o + a.nbytes].view(a.dtype).reshape(a.shape), a)
-        self.buffer = torch.empty(max(dev_total, 1), dtype=torch.uint8, device=dev())
+        if slot is None:
+            self.buffer = torch.empty(max(dev_total, 1), dtype=torch.uint8, device=dev())
+        else:
+            if getattr(slot, "tri_buf", None) is None or slot.tri_buf.numel() < dev_total:
+                slot.tri_buf = torch.empty(max(dev_total, 1 << 20) * 5 // 4, dtype=torch.uint8,
+                                           device=dev())
+            self.buffer = slot.tri_buf
         self.buffer[:total].copy_(stage[:total], non_blocking=True)
-        _STAGING.mark(i)
+        if slot is None:
+            _STAGING.mark(i)
+        else:
+            slot.tri_stage_event = torch.cuda.Event()
+            slot.tri_stage_event.record(torch.cuda.current_stream())
         tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32}
         for (name, a), o in zip(parts, offs):
             view = self.buffer[o:o + a.nbytes].view(tdt[a.dtype]).reshape(a.shape)

@@ -361,7 +361,7 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
     """Pipelined `reconstruct` over a sequence of (frame, tri) pairs.
 
     Yields one Reconstruction per frame, in order.  Two device pipelines
-    alternate: while frame i computes on the caller's stream, a host thread
+    rotate (STREAM_SLOTS): while frame i computes on the caller's stream, a host thread
     uploads frame i+1 (pinned frames copy by DMA) and its triangulation on a
     copy stream, and frame i-1's artefacts stream back to pinned host memory
     on a third stream.  Every frame gets the full per-frame work of
@@ -381,7 +381,8 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
     pipes = _stream_pipes(rig, w, h, params, prior_params)
     main = t.cuda.current_stream()
     copy_s, out_s = t.cuda.Stream(), t.cuda.Stream()
-    free = [None, None]          # event: pipe's inputs/outputs no longer in use
+    n_slots = len(pipes)
+    free = [None] * n_slots      # event: pipe's inputs/outputs no longer in use
     free_lock = threading.Condition()
     q = queue.Queue(maxsize=1)
     error = []
@@ -402,19 +403,19 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
         try:
             for i, (frame, tri) in enumerate(_chain(first, it)):
                 t0 = time.perf_counter()
-                pipe = pipes[i % 2]
+                pipe = pipes[i % n_slots]
                 with free_lock:
-                    while i >= 2 and free[i % 2] is None:
+                    while i >= n_slots and free[i % n_slots] is None:
                         free_lock.wait()
-                    ev = free[i % 2]
-                    free[i % 2] = None
+                    ev = free[i % n_slots]
+                    free[i % n_slots] = None
                 t0 = tick("prep_wait_free", t0)
                 with t.cuda.stream(copy_s):
                     if ev is not None:
                         copy_s.wait_event(ev)
                     pipe.load(frame.images, frame.priors)
                     t0 = tick("prep_load", t0)
-                    td = TriDevice(tri)
+                    td = TriDevice(tri, slot=pipe)  # the slot's own staging + device buffer
                     t0 = tick("prep_tridevice", t0)
                     loaded = t.cuda.Event()
                     loaded.record(copy_s)
@@ -474,7 +475,7 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
                 fetched = t.cuda.Event()
                 fetched.record(out_s)
         with free_lock:
-            free[i % 2] = fetched
+            free[i % n_slots] = fetched
             free_lock.notify_all()
         t0 = tick("main_fetch_enqueue", t0)
         if pending is not None:
@@ -564,13 +565,17 @@ class _PipePair(list):
     busy = False
 
 
+STREAM_SLOTS = 3  # frames in flight: H2D of i+1 never waits for the D2H of i-1
+
+
 def _stream_pipes(rig, w, h, params, prior_params):
-    """The two alternating pipelines of reconstruct_stream, kept across calls;
-    a pair in use by a running stream is never handed out twice."""
+    """The rotating pipelines of reconstruct_stream, kept across calls; a set
+    in use by a running stream is never handed out twice."""
     key = (id(rig), w, h, repr(params), repr(prior_params))
     p = _STREAM_PIPES.get(key)
     if p is None or p.busy:
-        p = _PipePair(FramePipeline(rig, w, h, params, prior_params) for _ in range(2))
+        p = _PipePair(FramePipeline(rig, w, h, params, prior_params)
+                      for _ in range(STREAM_SLOTS))
         if key not in _STREAM_PIPES or not _STREAM_PIPES[key].busy:
             if len(_STREAM_PIPES) > 4:
                 _STREAM_PIPES.clear()

@@ -12,7 +12,7 @@ for d, s in zip(pin_p, frame.priors): d[...] = s
 hf = st.LightFieldFrame(images=pin_i, priors=pin_p)
 for _ in st.reconstruct_stream([(hf, tri)] * 2, rig, sp, pp): pass
 os.environ["ST_STREAM_PROFILE"] = "1"
-for rep in range(6):
+for rep in range(10):
     torch.cuda.synchronize()
     t0 = time.perf_counter(); n = 0
     for _ in st.reconstruct_stream([(hf, tri)] * 60, rig, sp, pp): n += 1
