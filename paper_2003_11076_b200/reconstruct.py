@@ -384,7 +384,7 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
     n_slots = len(pipes)
     free = [None] * n_slots      # event: pipe's inputs/outputs no longer in use
     free_lock = threading.Condition()
-    q = queue.Queue(maxsize=1)
+    q = queue.Queue(maxsize=max(1, len(pipes) - 1))  # prepared frames ahead of the consumer
     error = []
 
     device = t.cuda.current_device()
