@@ -91,6 +91,9 @@ typedef struct {
    * [0] k_m_step, [1] k_e_step_at, [2] k_initial_masks, [3] the rest */
   double kernel_ms[4];
   int32_t kernel_launches[4];
+  int64_t hopeless_msteps;           /* pixel M-steps with fewer static views than min_static_rays */
+  int64_t energy_samples;            /* M-step descriptor samples: static in-margin rays of the real
+                                        candidates evaluated (incl. previous-disparity energies) */
 } st_stats;
 
 const char* st_last_error(void);

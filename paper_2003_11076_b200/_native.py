@@ -38,7 +38,8 @@ class StStats(C.Structure):
                 ("support_records", C.c_int64), ("candidates_total", C.c_int64),
                 ("energy_evals", C.c_int64), ("prev_evals", C.c_int64),
                 ("msteps", C.c_int64), ("esteps", C.c_int64),
-                ("kernel_ms", C.c_double * 4), ("kernel_launches", C.c_int32 * 4)]
+                ("kernel_ms", C.c_double * 4), ("kernel_launches", C.c_int32 * 4),
+                ("hopeless_msteps", C.c_int64), ("energy_samples", C.c_int64)]
 
 
 class StFrame(C.Structure):

@@ -105,6 +105,11 @@ int make_ctx(const st_frame* f, const st_rig* rig, const st_params* p, st::EmCtx
     if (!eye || b[1] != 0.0 || b[2] != 0.0 || !(fabs(b[0]) < 1e300)) c.rectified = 0;
   }
   for (int n = 0; n <= ST_MAX_VIEWS; ++n) c.recip[n] = n ? 1.0 / (double)n : 0.0;
+  // the M-step tap cache holds 32-bit descriptor indices
+  if ((double)rig->num_views * (double)c.HW >= 4294967295.0) c.rectified = 0;
+  c.view_bits = (uint32_t)((1u << rig->num_views) - 1u);
+  // cross-check: evaluate every candidate (no pruning; same winner)
+  c.exhaustive = getenv("ST_MSTEP_EXHAUSTIVE") != nullptr;
   return ST_OK;
 }
 
@@ -158,11 +163,36 @@ void launch_taps(unsigned blocks, cudaStream_t s, const st::EmCtx& c, const st::
     st::k_e_step_taps<K, false><<<blocks, ESTEP_TAPS_BLOCK, 0, s>>>(c, a);
 }
 
+template <int K>
+void launch_cert(unsigned blocks, cudaStream_t s, const st::EmCtx& c, const st::EStepArgs& a) {
+  if (c.rectified)
+    st::k_e_step_cert<K, true><<<blocks, ESTEP_CERT_BLOCK, 0, s>>>(c, a);
+  else
+    st::k_e_step_cert<K, false><<<blocks, ESTEP_CERT_BLOCK, 0, s>>>(c, a);
+}
+
+// With a fallback list (args.flist, K <= 5): the certificate pass
+// (k_e_step_cert) decides most rows without any fp64 score; the rows it
+// cannot certify go through the screened kernel, one grid-stride wave.
 void launch_e_step(int K, int64_t n, cudaStream_t s, const st::EmCtx& c,
                    const st::EStepArgs& args) {
   const bool exhaustive = getenv("ST_ESTEP_EXHAUSTIVE") != nullptr;  // cross-check
   st::EStepArgs a = args;
   a.exhaustive = exhaustive ? 1 : 0;
+  if (K <= 5 && a.flist && !exhaustive) {
+    cudaMemsetAsync(a.flist_count, 0, sizeof(uint32_t), s);
+    const unsigned bc = blocks_for(n, ESTEP_CERT_BLOCK);
+    switch (K) {
+      case 2: launch_cert<2>(bc, s, c, a); break;
+      case 3: launch_cert<3>(bc, s, c, a); break;
+      case 4: launch_cert<4>(bc, s, c, a); break;
+      default: launch_cert<5>(bc, s, c, a); break;
+    }
+    sthost::count_launch();
+    a.list = a.flist;
+    a.list_count = a.flist_count;
+    n = std::min<int64_t>(n, 148 * ESTEP_MIN_BLOCKS * ESTEP_TAPS_BLOCK);
+  }
   const unsigned bt = blocks_for(n, ESTEP_TAPS_BLOCK);
   switch (K) {
     case 2: launch_taps<2>(bt, s, c, a); break;
@@ -415,8 +445,8 @@ int st_masked_variance(const double* desc, const uint8_t* mask, int64_t n, int32
 // fused solve
 
 struct SolveLayout {
-  size_t d, e, pe, st_act, chg, mask_in, mlist, elist, counts, active, flags, offs, work,
-      parts, reduced, cub, total;
+  size_t d, e, pe, st_act, chg, mask_in, mlist, elist, counts, flist, active, flags, offs,
+      work, parts, reduced, cub, total;
   size_t cub_bytes;
   int max_warps;
 };
@@ -438,7 +468,8 @@ static SolveLayout solve_layout(int W, int H) {
   L.mask_in = o;  o += align_up(sizeof(uint32_t) * npx);
   L.mlist = o;    o += align_up(sizeof(int32_t) * npx);
   L.elist = o;    o += align_up(sizeof(int32_t) * npx);
-  L.counts = o;   o += align_up(sizeof(uint32_t) * 4 + sizeof(double) * 4);  // worklist counts, stop flag, eps logs
+  L.counts = o;   o += align_up(sizeof(uint32_t) * 4 + sizeof(double) * 4 + 16);  // worklist counts, stop flag, eps logs, fallback count
+  L.flist = o;    o += align_up(sizeof(int32_t) * npx);
   L.active = o;   o += align_up(sizeof(int64_t) * npx);
   L.flags = o;    o += align_up(sizeof(uint32_t) * (npx + 1));
   L.offs = o;     o += align_up(sizeof(uint32_t) * (npx + 1));
@@ -590,6 +621,8 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       e.valid_out = valid_bits;
       e.scatter = 1;
       e.eps_logs = eps_logs;
+      e.flist = (int32_t*)(ws + L.flist);
+      e.flist_count = (uint32_t*)(eps_logs + 4);
       launch_e_step(rig->num_views, n_act, s, c, e);
       ST_LAUNCH_CHECK("k_e_step_at");
       ev.record(2, s);
@@ -631,6 +664,8 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
     stats->mean_energy[it - 1] = v[1] > 0 ? v[0] / v[1] : NAN;
     stats->candidates_total += (int64_t)v[5];
     stats->energy_evals += (int64_t)v[6];
+    stats->hopeless_msteps += r.n_hopeless;  // (diagnostics, this rank only)
+    stats->energy_samples += r.n_samples;
     if (it > 1) {
       stats->prev_energy[it - 2] = v[3] > 0 ? v[2] / v[3] : NAN;
       const double changed = v[4] / n_act_global;
@@ -751,6 +786,8 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     e.valid_out = valid_bits;
     e.scatter = 1;
     e.eps_logs = eps_logs;
+    e.flist = (int32_t*)(ws + L.flist);
+    e.flist_count = (uint32_t*)(eps_logs + 4);
     e.stop = stop;
     launch_e_step(rig->num_views, it > 1 ? std::min<int64_t>(npx, 148 * 8 * 128) : npx, s, c, e);
     ST_LAUNCH_CHECK("k_e_step_at");

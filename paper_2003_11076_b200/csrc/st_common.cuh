@@ -134,7 +134,9 @@ __device__ __forceinline__ double prune_radius(double best, float sigma_f, float
   if (!(best < 1e30)) return INFINITY;
   const float x = expf(-(float)best) - gamma_f;
   if (!(x >= 1e-3f)) return INFINITY;  // nothing prunable (best near -log gamma)
-  if (x >= 1.0f) return 0.0;           // best below every bound
+  // best at (or, by fp32 rounding, apparently below) the smallest bound:
+  // only candidates within the absolute margin of mu can still tie
+  if (x >= 1.0f) return 0.01;
   const float r = sigma_f * sqrtf(-2.0f * logf(x));
   return (double)r * (1.0 + 1e-4) + 0.01;
 }

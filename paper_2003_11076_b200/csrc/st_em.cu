@@ -65,6 +65,7 @@ __device__ __forceinline__ Taps taps_ctx(const EmCtx& c, const WarpOut& w) {
 struct Energy {
   double e;
   bool real;
+  int n;  // descriptor samples taken (static in-margin rays of a real candidate)
 };
 
 #ifdef ENERGY_TWO_PASS
@@ -111,6 +112,7 @@ __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, 
     if (((bits >> k) & 1u) && in_margin(c.rig, k, warp_ctx(c, k, u, v, d))) ++cnt;
   Energy out;
   out.real = cnt >= c.p.min_static_rays;
+  out.n = out.real ? cnt : 0;
   if (!out.real) {
     out.e = dsub(dmul(c.p.beta, variance_ceiling()), lp);
     return out;
@@ -172,6 +174,7 @@ __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, 
   }
   Energy out;
   out.real = cnt >= c.p.min_static_rays;
+  out.n = cnt;
   double var;
   if (out.real) {
     const double nn = (double)cnt;
@@ -194,6 +197,79 @@ __device__ __forceinline__ Energy energy_at(const EmCtx& c, double u, double v, 
   return out;
 }
 #endif
+
+// ---------------------------------------------------------------------------
+// Rectified rigs: cached taps (k_m_step).
+//
+// On a rectified rig a ray's bilinear taps are one descriptor index and a
+// horizontal weight.  The count pass that decides `real` (solver.py:244-250)
+// stores them per thread in shared memory (column `threadIdx.x`, stride
+// EM_BLOCK), so the two channel passes of the energy do not re-warp.
+
+struct TapCol {
+  uint32_t* off;  // k * HW + row * W + floor(pu), static in-margin views in view order
+  double* f64;    // fu = pu - floor(pu)
+};
+
+__device__ __forceinline__ int rect_taps(const EmCtx& c, double u, double v, double d,
+                                         uint32_t bits, const TapCol& t) {
+  int cnt = 0;
+  const uint32_t row = (uint32_t)v * (uint32_t)c.W;
+  for (int k = 0; k < c.rig.num_views; ++k) {
+    if (!((bits >> k) & 1u)) continue;
+    const WarpOut w = warp_ctx(c, k, u, v, d);
+    if (!in_margin(c.rig, k, w)) continue;
+    const double fl = floor(w.pu);
+    const double fu = dsub(w.pu, fl);
+    t.off[cnt * EM_BLOCK] = (uint32_t)k * (uint32_t)c.HW + row + (uint32_t)(int)fl;
+    t.f64[cnt * EM_BLOCK] = fu;
+    ++cnt;
+  }
+  return cnt;
+}
+
+// Exact energy of a real candidate from the cached taps: the arithmetic of
+// energy_at (two passes along numpy's reduction tree) on the same samples.
+__device__ __forceinline__ double rect_energy(const EmCtx& c, int cnt, const TapCol& t,
+                                              double lp) {
+  const double nn = (double)cnt;
+  const double rn = c.recip[cnt];
+  double half[2];
+#pragma unroll 1
+  for (int p = 0; p < 2; ++p) {
+    double s1[8], s2[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s1[i] = 0.0;
+      s2[i] = 0.0;
+    }
+    for (int j = 0; j < cnt; ++j) {
+      const uint4* pl = c.desc + t.off[j * EM_BLOCK];
+      const uint4 a = __ldg(pl), b = __ldg(pl + 1);
+      const double fu = t.f64[j * EM_BLOCK];
+      const uint32_t aw[2] = {p ? a.y : a.x, p ? a.w : a.z};
+      const uint32_t bw[2] = {p ? b.y : b.x, p ? b.w : b.z};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double g[4];
+        lerp_word(aw[h], bw[h], fu, g);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          s1[4 * h + q] = dadd(s1[4 * h + q], g[q]);
+          s2[4 * h + q] = dadd(s2[4 * h + q], dmul(g[q], g[q]));
+        }
+      }
+    }
+    double r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      r[j] = dadd(dsub(s2[j], div_small(dmul(s1[j], s1[j]), nn, rn)),
+                  dsub(s2[4 + j], div_small(dmul(s1[4 + j], s1[4 + j]), nn, rn)));
+    half[p] = dadd(dadd(r[0], r[1]), dadd(r[2], r[3]));
+  }
+  const double var = fmax(div_small(dadd(half[0], half[1]), nn, rn), 0.0);
+  return dsub(dmul(c.p.beta, var), lp);
+}
 
 // ---------------------------------------------------------------------------
 // block-deterministic reductions
@@ -234,7 +310,31 @@ __device__ __forceinline__ void list_append(bool want, int32_t slot, int32_t* li
 __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
   if (a.stop && *a.stop) return;  // converged (st_solve_async)
   const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
-  long long n_cand = 0, n_eval = 0;
+  long long n_cand = 0, n_eval = 0, n_hopeless = 0, n_samples = 0;
+  __shared__ uint32_t s_off[ST_MAX_VIEWS * EM_BLOCK];
+  __shared__ double s_f64[ST_MAX_VIEWS * EM_BLOCK];
+  const TapCol tc = {s_off + threadIdx.x, s_f64 + threadIdx.x};
+  // penalty energy term beta * VARIANCE_CEILING (solver.py:44, 252-256)
+  const double pen = dmul(c.p.beta, variance_ceiling());
+  // Exact energy (and `real`) of one candidate.  A pixel whose static mask
+  // has fewer than min_static_rays views (`hopeless`) can have no real
+  // candidate: every energy is the penalty minus the log prior, no sampling.
+  auto energy = [&](double u, double v, double d, uint32_t bits, bool hopeless, double lp,
+                    Energy& E) {
+    if (hopeless) {
+      E.real = false;
+      E.n = 0;
+      E.e = dsub(pen, lp);
+    } else if (!c.rectified) {
+      E = energy_at(c, u, v, d, bits, lp);
+    } else {
+      const int cnt = rect_taps(c, u, v, d, bits, tc);
+      E.real = cnt >= c.p.min_static_rays;
+      E.n = E.real ? cnt : 0;
+      E.e = E.real ? rect_energy(c, cnt, tc, lp) : dsub(pen, lp);
+    }
+    n_samples += E.n;
+  };
   // block-uniform grid-stride loop: one wave of blocks can cover a worklist
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_work;
        base += (int64_t)gridDim.x * blockDim.x) {
@@ -250,6 +350,19 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
     const double mu = c.mu[pix];
     const uint32_t bits = a.static_all[pix];
     const double dmax = c.p.d_max;
+    const bool hopeless = __popc(bits & c.view_bits) < c.p.min_static_rays;
+    n_hopeless += hopeless;
+    // Pruning radius of an incumbent energy.  Real candidates: E >= -lp
+    // (var >= 0, solver.py:341-347).  Hopeless pixels: E = fl(pen - lp), and
+    // fl is monotone, so a candidate can only tie the incumbent when
+    // -lp <= (be - pen) + one rounding of pen (the slack), i.e. only
+    // candidates within a hair of the best prior survive.
+    auto radius = [&](double best) -> double {
+      if (c.exhaustive) return INFINITY;
+      if (!hopeless) return prune_radius(best, c.sigma_f, c.gamma_f);
+      return prune_radius(dadd(dsub(best, pen), 1e-12 * (1.0 + fabs(pen))), c.sigma_f,
+                          c.gamma_f);
+    };
 
     double be = INFINITY, bd = INFINITY;
     bool br = false;
@@ -263,13 +376,14 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
     if (!a.first) {
       dp = a.d[i];  // previous disparity (in place)
       if (!isnan(dp)) {
-        const Energy E = energy_at(c, u, v, dp, bits,
-                                   log_prior(dp, mu, c.p.sigma, c.p.gamma, c.inv_sigma));
+        Energy E;
+        energy(u, v, dp, bits, hopeless, log_prior(dp, mu, c.p.sigma, c.p.gamma, c.inv_sigma),
+               E);
         pe = E.e;
         be = E.e;
         bd = dp;
         br = E.real;
-        lim = prune_radius(be, c.sigma_f, c.gamma_f);
+        lim = radius(be);
       }
     }
     auto offer = [&](double d) {
@@ -279,14 +393,15 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
       // certainly pruned; the rest get the exact fp64 comparison.
       if (fabs(d - mu) > lim || d == bd) return;  // (d == bd: same energy, no change)
       const double lp = log_prior(d, mu, c.p.sigma, c.p.gamma, c.inv_sigma);
-      if (!(-lp <= be)) return;
+      if (!(-lp <= be) && !c.exhaustive) return;
       ++n_eval;
-      const Energy E = energy_at(c, u, v, d, bits, lp);
+      Energy E;
+      energy(u, v, d, bits, hopeless, lp, E);
       if (E.e < be || (E.e == be && d < bd)) {
         be = E.e;
         bd = d;
         br = E.real;
-        lim = prune_radius(be, c.sigma_f, c.gamma_f);
+        lim = radius(be);
       }
     };
 
@@ -336,10 +451,14 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
   if (a.partials) {
     const long long c_cand = warp_sum(n_cand);
     const long long c_eval = warp_sum(n_eval);
+    const long long c_hopeless = warp_sum(n_hopeless);
+    const long long c_samples = warp_sum(n_samples);
     if ((threadIdx.x & 31) == 0) {
       Partial& P = a.partials[(blockIdx.x * blockDim.x + threadIdx.x) >> 5];
       P.n_cand = c_cand;
       P.n_eval = c_eval;
+      P.n_hopeless = c_hopeless;
+      P.n_samples = c_samples;
     }
   }
 }
@@ -416,6 +535,8 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ 
     if (w < n_work_parts) {
       P.n_cand = work[w].n_cand;
       P.n_eval = work[w].n_eval;
+      P.n_hopeless = work[w].n_hopeless;
+      P.n_samples = work[w].n_samples;
     }
     sp[wid] = P;
   }
@@ -430,6 +551,8 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ 
       B.n_changed += sp[j].n_changed;
       B.n_cand += sp[j].n_cand;
       B.n_eval += sp[j].n_eval;
+      B.n_hopeless += sp[j].n_hopeless;
+      B.n_samples += sp[j].n_samples;
     }
     parts[blockIdx.x] = B;
   }
@@ -901,6 +1024,170 @@ template __global__ void k_e_step_taps<3, true>(EmCtx, EStepArgs);
 template __global__ void k_e_step_taps<4, true>(EmCtx, EStepArgs);
 template __global__ void k_e_step_taps<5, true>(EmCtx, EStepArgs);
 
+// E-step certificate pass for K <= 5 views (prior dominance, exact).
+//
+// score(m) = fl(P(m) - fl(beta v(m))) <= P(m) - [pop(m) < min_static_rays]
+// beta * ceiling, P(m) the prior sum (v >= 0, fl monotone).  Those bounds
+// need no descriptor samples.  The admissible mask m1 with the largest
+// bound is scored in fp32 with the screen's error bound D (estep_small);
+// if the lower end of that score beats every other mask's bound, m1 is the
+// reference's argmax -- uniquely, so its tie rules cannot intervene.  Rows
+// without such a certificate go to a fallback list for k_e_step_taps.
+//
+// Everything here is fp32 except the warp (validity is an output and must
+// be exact).  The priors' log factors are fp32 too; against the fp64
+// recipe (sample_prior, clamp_logs) each log differs by at most
+//   E_l = (6u + 2u) / eps * 1.01 + 2 ulp32(max(|log eps|, 1)),
+// (q lerp in fp32 <= 6u, clip bound and 1 - q roundings 2u, |d log q| <=
+// |dq| / eps, logf <= 2 ulp), so every P(m) moves by <= K E_l.
+template <int KT, bool RECT>
+__global__ void __launch_bounds__(ESTEP_CERT_BLOCK, ESTEP_CERT_MIN_BLOCKS)
+    k_e_step_cert(EmCtx c, EStepArgs a) {
+  if (a.stop && *a.stop) return;  // converged (st_solve_async)
+  constexpr int M = 1 << KT;
+  constexpr float U = 5.9604645e-08f;  // 2^-24
+  const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
+  const float eps = (float)c.p.epsilon_prior;
+  const float hi = (float)dsub(1.0, c.p.epsilon_prior);
+  const float lmax = fmaxf(fabsf(logf(eps)), 1.0f);
+  const float e_l = (8.0f * U) / eps * 1.01f + 4.0f * U * 2.0f * lmax;
+  const float beta = (float)c.p.beta;
+  const float ceil32 = (float)variance_ceiling();
+  const float pen = beta * ceil32;
+  const float eps32 = (RECT ? 1024.0f : 4096.0f) * U;  // descriptor sample error (desc_word32)
+  const uint32_t* desc = reinterpret_cast<const uint32_t*>(c.desc);
+  const int su = c.W > 1 ? 1 : 0, sv = c.H > 1 ? c.W : 0;  // taps_of's steps
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_work;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = base + threadIdx.x;
+    bool fail = false;
+    int64_t i = 0;
+    if (t < n_work) {
+      i = a.list ? (int64_t)a.list[t] : t;
+      if (!(a.status && a.status[i] == ST_STATUS_LOW_TEXTURE)) {  // solver.py:476-478
+        const int64_t pix = a.pix ? a.pix[i] : i;
+        const double u = (double)(pix % c.W), v = (double)(pix / c.W);
+        const double d = a.d[i];
+        int idx[KT];
+        float fu[KT], fv[KT], l1[KT], l0[KT];
+        uint32_t vb = 0;
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+          const WarpOut w = warp_ctx(c, k, u, v, d);
+          float q = 0.5f;  // invalid rays (solver.py:206-227)
+          idx[k] = 0;
+          fu[k] = 0.0f;
+          fv[k] = 0.0f;
+          if (in_margin(c.rig, k, w)) {
+            const Taps tp = taps_ctx(c, w);
+            idx[k] = tp.iv * c.W + tp.iu;
+            fu[k] = (float)tp.fu;
+            if (!RECT) fv[k] = (float)tp.fv;
+            const float* pl = c.priors + (size_t)k * c.HW + idx[k];
+            const float p0 = __ldg(pl), p1 = __ldg(pl + tp.su);
+            q = fmaf(fu[k], __fsub_rn(p1, p0), p0);
+            if (!RECT && tp.fv != 0.0) {
+              const float p2 = __ldg(pl + tp.sv), p3 = __ldg(pl + tp.sv + tp.su);
+              const float bot = fmaf(fu[k], __fsub_rn(p3, p2), p2);
+              q = fmaf(fv[k], bot - q, q);
+            }
+            vb |= 1u << k;
+          }
+          const float qc = fminf(fmaxf(q, eps), hi);
+          l1[k] = logf(qc);
+          l0[k] = logf(1.0f - qc);
+        }
+        uint32_t m1 = 0;
+        if (vb) {
+          float l0t = 0.0f, lsum = 0.0f, dl[KT];
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            dl[k] = l1[k] - l0[k];
+            l0t += l0[k];
+            lsum += fabsf(l1[k]) + fabsf(l0[k]);
+          }
+          float ub1 = -INFINITY, ub2 = -INFINITY;
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            if ((uint32_t)m & ~vb) continue;
+            float ub = l0t;
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+              if ((m >> k) & 1) ub += dl[k];
+            if (__popc(m) < c.p.min_static_rays) ub -= pen;
+            if (ub > ub1) {
+              ub2 = ub1;
+              ub1 = ub;
+              m1 = (uint32_t)m;
+            } else {
+              ub2 = fmaxf(ub2, ub);
+            }
+          }
+          // |bound32 - bound64| <= K E_l + fp32 sums and penalty roundings
+          const float errp = 2.0f * (KT * e_l + (2.0f * KT + 8.0f) * U * (lsum + pen));
+          if (__popc(m1) < c.p.min_static_rays) {
+            fail = !(ub1 - errp > ub2 + errp);
+          } else {
+            const int k0 = __ffs(vb) - 1;
+            float qs = 0.0f, ac = 0.0f, s2u = 0.0f;
+#pragma unroll 1
+            for (int w = 0; w < 4; ++w) {
+              float ref[4];
+#pragma unroll
+              for (int k = 0; k < KT; ++k)
+                if (k == k0)
+                  desc_word32<RECT>(desc + (size_t)k * c.HW * 4, idx[k], su, sv, fu[k], fv[k], w,
+                                    ref);
+              float b1[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+              for (int k = 0; k < KT; ++k) {
+                if (!((m1 >> k) & 1)) continue;
+                float x[4];
+                desc_word32<RECT>(desc + (size_t)k * c.HW * 4, idx[k], su, sv, fu[k], fv[k], w,
+                                  x);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float g = x[j] - ref[j];
+                  b1[j] += g;
+                  qs = fmaf(g, g, qs);
+                  s2u = fmaf(x[j], x[j], s2u);
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) ac = fmaf(b1[j], b1[j], ac);
+            }
+            const float rn = 1.0f / (float)__popc(m1);
+            const float var = fmaxf((qs - ac * rn) * rn, 0.0f);
+            const float s32 = ub1 - beta * var;
+            // estep_small's D on the in-mask sums
+            const float D = 2.0f * (fabsf(beta) * (64.0f * U * qs + 2.0f * U * fmaxf(ceil32, qs) +
+                                                   7.1054274e-15f * s2u + 2.0f * U * ceil32 +
+                                                   2.0f * eps32 * sqrtf(80.0f * qs) +
+                                                   80.0f * eps32 * eps32) +
+                                    (2.0f * KT + 6.0f) * U * lsum);
+            fail = !(s32 - D - errp > ub2 + errp);
+          }
+        }
+        if (!fail) {
+          const int64_t o = a.scatter ? pix : i;
+          a.static_out[o] = m1;
+          a.valid_out[o] = vb;
+        }
+      }
+    }
+    list_append(fail, (int32_t)i, a.flist, a.flist_count);
+  }
+}
+
+template __global__ void k_e_step_cert<2, false>(EmCtx, EStepArgs);
+template __global__ void k_e_step_cert<3, false>(EmCtx, EStepArgs);
+template __global__ void k_e_step_cert<4, false>(EmCtx, EStepArgs);
+template __global__ void k_e_step_cert<5, false>(EmCtx, EStepArgs);
+template __global__ void k_e_step_cert<2, true>(EmCtx, EStepArgs);
+template __global__ void k_e_step_cert<3, true>(EmCtx, EStepArgs);
+template __global__ void k_e_step_cert<4, true>(EmCtx, EStepArgs);
+template __global__ void k_e_step_cert<5, true>(EmCtx, EStepArgs);
+
 // E-step for 6 <= K <= 12 views: rays staged in shared memory, masks
 // enumerated one at a time (estep_generic).
 __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a) {
@@ -1115,9 +1402,9 @@ __global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
                                   Partial* __restrict__ out, const int* stop) {
   __shared__ double sd[2][256];
   if (stop && *stop) return;
-  __shared__ long long si[5][256];
+  __shared__ long long si[7][256];
   double a = 0.0, b = 0.0;
-  long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+  long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0;
   // thread t sums parts t, t+256, ... in order
   for (int j = threadIdx.x; j < nparts; j += blockDim.x) {
     a += parts[j].sum_e;
@@ -1127,6 +1414,8 @@ __global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
     c2 += parts[j].n_changed;
     c3 += parts[j].n_cand;
     c4 += parts[j].n_eval;
+    c5 += parts[j].n_hopeless;
+    c6 += parts[j].n_samples;
   }
   sd[0][threadIdx.x] = a;
   sd[1][threadIdx.x] = b;
@@ -1135,6 +1424,8 @@ __global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
   si[2][threadIdx.x] = c2;
   si[3][threadIdx.x] = c3;
   si[4][threadIdx.x] = c4;
+  si[5][threadIdx.x] = c5;
+  si[6][threadIdx.x] = c6;
   __syncthreads();
   // fixed-order pairwise tree over the 256 thread sums (deterministic)
   for (int h = 128; h > 0; h >>= 1) {
@@ -1143,7 +1434,7 @@ __global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
       sd[0][t] += sd[0][t + h];
       sd[1][t] += sd[1][t + h];
 #pragma unroll
-      for (int k = 0; k < 5; ++k) si[k][t] += si[k][t + h];
+      for (int k = 0; k < 7; ++k) si[k][t] += si[k][t + h];
     }
     __syncthreads();
   }
@@ -1156,6 +1447,8 @@ __global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
     r.n_changed = si[2][0];
     r.n_cand = si[3][0];
     r.n_eval = si[4][0];
+    r.n_hopeless = si[5][0];
+    r.n_samples = si[6][0];
     *out = r;
   }
 }
@@ -1202,6 +1495,8 @@ __global__ void k_solve_control(int it, const Partial* __restrict__ reduced,
   stats->mean_energy[it - 1] = nf > 0 ? r.sum_e / nf : NAN;
   stats->candidates_total += r.n_cand;
   stats->energy_evals += r.n_eval;
+  stats->hopeless_msteps += r.n_hopeless;
+  stats->energy_samples += r.n_samples;
   if (it > 1) {
     const double npf = (double)r.n_pfin;
     stats->prev_energy[it - 2] = npf > 0 ? r.sum_pe / npf : NAN;

@@ -18,6 +18,10 @@
 #define STATS_BLOCK 256
 #define ESTEP_BLOCK 64
 #define ESTEP_TAPS_BLOCK 128
+#define ESTEP_CERT_BLOCK 128
+#ifndef ESTEP_CERT_MIN_BLOCKS
+#define ESTEP_CERT_MIN_BLOCKS 6  // <= 80 registers
+#endif
 #ifndef ESTEP_MIN_BLOCKS
 #define ESTEP_MIN_BLOCKS 4  // <= 128 registers
 #endif
@@ -48,11 +52,15 @@ struct EmCtx {
   float gamma_f;
   int rectified;        // every view: A = I, b = (bx, 0, 0) -> 1-D horizontal warp
   double recip[ST_MAX_VIEWS + 1];  // RN(1/n), n = 1..12, for div_small
+  uint32_t view_bits;   // (1 << K) - 1
+  int exhaustive;       // M-step: no pruning, every candidate evaluated (cross-check)
 };
 
 struct Partial {
   double sum_e, sum_pe;
   long long n_fin, n_pfin, n_changed, n_cand, n_eval;
+  long long n_hopeless;  // M-step pixels with fewer static views than min_static_rays
+  long long n_samples;   // M-step descriptor samples (static in-margin rays of real candidates)
 };
 
 // Slots are the rows of the active set (slot i -> pixel active[i], or i when
@@ -89,6 +97,8 @@ struct EStepArgs {
   int exhaustive;            // 1: score every mask in fp64 (no fp32 screen)
   const int* stop;           // nullable: device flag, set -> the launch does nothing
   const double* eps_logs;    // nullable: k_eps_logs output (clamped-prior logs)
+  int32_t* flist;            // k_e_step_cert: rows it could not certify (append) ...
+  uint32_t* flist_count;     // ... and their count (zeroed by the launcher)
 };
 
 __global__ void k_m_step(EmCtx c, MStepArgs a);
@@ -101,6 +111,8 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* e, const doub
 template <int KT, bool RECT>
 __global__ void k_e_step_taps(EmCtx c, EStepArgs a);
 __global__ void k_e_step_at(EmCtx c, EStepArgs a);
+template <int KT, bool RECT>
+__global__ void k_e_step_cert(EmCtx c, EStepArgs a);
 __global__ void k_initial_masks(EmCtx c, const int64_t* pix, int64_t n, uint32_t* static_out,
                                 uint32_t* valid_out);
 __global__ void k_gather_rays(EmCtx c, const int64_t* pix, const double* d, int64_t n,

@@ -282,6 +282,8 @@ def _stats_of(s):
     st.active_pixels = int(s.active_pixels)
     st.candidates_total = int(s.candidates_total)
     st.energy_evals = int(s.energy_evals)
+    st.hopeless_msteps = int(s.hopeless_msteps)
+    st.energy_samples = int(s.energy_samples)
     st.prev_evals = int(s.prev_evals)
     st.msteps = int(s.msteps)
     st.esteps = int(s.esteps)

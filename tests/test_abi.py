@@ -46,7 +46,7 @@ def test_struct_layouts_match_the_header():
     # st_rig: 4 ints + 12*9 + 12*3 doubles + 2*12 ints
     assert ctypes.sizeof(N.StRig) == 16 + 12 * 12 * 8 + 2 * 12 * 4
     assert ctypes.sizeof(N.StParams) == 8 * 2 + 4 * 2 + 8 * 5 + 4 * 2
-    assert ctypes.sizeof(N.StStats) == 8 + 3 * 64 * 8 + 7 * 8 + 4 * 8 + 4 * 4
+    assert ctypes.sizeof(N.StStats) == 8 + 3 * 64 * 8 + 7 * 8 + 4 * 8 + 4 * 4 + 2 * 8
 
 
 def test_version_and_error_calls_need_no_gpu(lib):

@@ -91,9 +91,10 @@ def test_c2_properties(st):
 
 @pytest.mark.parametrize("cfg", ["C2", "C3"])
 def test_screened_em_equals_exhaustive(st, monkeypatch, cfg):
-    """The fp32-screened E-step and M-step decide exactly what evaluating
-    every mask / surviving candidate in fp64 decides (st_em.cu estep_small,
-    screen_energy), whole frame."""
+    """The fp32-screened E-step and the pruned M-step decide exactly what
+    evaluating every mask / every candidate in fp64 decides (st_em.cu
+    estep_small; k_m_step's prior-bound and hopeless-pixel radii), whole
+    frame."""
     frame, rig, tri, sp, pp = _inputs(cfg)
     a = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=5)
     monkeypatch.setenv("ST_ESTEP_EXHAUSTIVE", "1")
