@@ -5,6 +5,7 @@
 // memory, then every thread writes its descriptor as a single 16-byte store.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "st_common.cuh"
 
@@ -30,6 +31,27 @@ __device__ __forceinline__ uint8_t sobel_code(int raw) {
   // features.py:56-57: clip(rint(128 + raw / 4), 0, 255), half to even
   const double r = rint(dadd(128.0, dmul((double)raw, 0.25)));
   return (uint8_t)fmin(fmax(r, 0.0), 255.0);
+}
+
+// The same two codes in integer arithmetic (exact):
+// * gray: the fp64 sum is N/1000 + O(1e-13) with N = 299 R + 587 G + 114 B,
+//   so rint agrees with rounding N/1000 unless N/1000 is exactly a half
+//   (N mod 1000 == 500), where the fp64 roundings decide: recompute those.
+// * Sobel: 128 + raw/4 = t/4 with t = 512 + raw exactly; rint half to even.
+__device__ __forceinline__ int gray_int(int r, int g, int b) {
+  const int n = 299 * r + 587 * g + 114 * b;
+  const int k = n / 1000, rem = n - 1000 * k;
+  if (rem != 500) return k + (rem > 500 ? 1 : 0);
+  const double v = dadd(dadd(dmul((double)r, 0.299), dmul((double)g, 0.587)),
+                        dmul((double)b, 0.114));
+  return (int)rint(v);
+}
+
+__device__ __forceinline__ uint8_t sobel_code_int(int raw) {
+  const int t = 512 + raw;
+  const int q = t >> 2, rem = t & 3;  // t = 4q + rem, rem in [0, 3]
+  const int v = q + (rem > 2 || (rem == 2 && (q & 1)) ? 1 : 0);
+  return (uint8_t)min(max(v, 0), 255);
 }
 
 __global__ void __launch_bounds__(DT_W* DT_H) k_descriptors(const uint8_t* __restrict__ images,
@@ -89,6 +111,92 @@ __global__ void __launch_bounds__(DT_W* DT_H) k_descriptors(const uint8_t* __res
   }
 }
 
+// Wide-tile variant for RGB views (the production path): one CTA owns a
+// 128x16 output tile.  The edge-clamped RGB rows of the tile (+3 px halo)
+// are staged as raw bytes with 32-bit loads (many independent loads in
+// flight per thread), then gray, Sobel and the ring are computed from
+// shared memory exactly as in k_descriptors; each thread writes 8
+// descriptors, a warp 32 consecutive ones per store.
+#define DW_W 128
+#define DW_H 16
+#define DW_ROWB 416  // >= 3 * (DW_W + 6) + 6 bytes of one staged row
+
+__global__ void __launch_bounds__(256) k_descriptors_wide(const uint8_t* __restrict__ images,
+                                                          int H, int W, size_t total_bytes,
+                                                          uint4* __restrict__ desc,
+                                                          uint8_t* __restrict__ gray_out,
+                                                          uint8_t* __restrict__ sobel_out) {
+  __shared__ __align__(16) uint8_t raw[DW_H + 6][DW_ROWB];
+  __shared__ int16_t g[DW_H + 6][DW_W + 6];
+  __shared__ uint16_t sxy[DW_H + 4][DW_W + 4];  // gx | gy << 8; 0x8080 off-image
+  __shared__ int roff[DW_H + 6];  // byte of pixel 0 of the row, relative to the staged start
+  const int k = blockIdx.z;
+  const size_t view = (size_t)k * H * W * 3;
+  const int x0 = blockIdx.x * DW_W, y0 = blockIdx.y * DW_H;
+  const int tid = threadIdx.x;
+  const int cl0 = max(x0 - 3, 0), cl1 = min(x0 + DW_W + 3, W);  // clamped column range
+  const uintptr_t buf0 = (uintptr_t)images, buf1 = buf0 + total_bytes;
+  // stage rows: 32-bit words covering bytes [3 cl0, 3 cl1) of each clamped row
+  const int words_per_row = (3 * (cl1 - cl0) + 6) / 4 + 1;
+  for (int i = tid; i < (DW_H + 6) * words_per_row; i += blockDim.x) {
+    const int r = i / words_per_row, j = i % words_per_row;
+    const int yy = min(max(y0 - 3 + r, 0), H - 1);
+    const uintptr_t a0 = buf0 + view + ((size_t)yy * W + cl0) * 3;
+    const uintptr_t w0 = a0 & ~(uintptr_t)3;
+    if (j == 0) roff[r] = (int)(a0 - w0) - 3 * cl0;
+    const uintptr_t wa = w0 + 4 * (uintptr_t)j;
+    if (wa + 4 <= buf1) {
+      *reinterpret_cast<uint32_t*>(&raw[r][4 * j]) = __ldg(reinterpret_cast<const uint32_t*>(wa));
+    } else {
+      for (int b = 0; b < 4; ++b)
+        raw[r][4 * j + b] = wa + b < buf1 ? __ldg(reinterpret_cast<const uint8_t*>(wa + b)) : 0;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < (DW_H + 6) * (DW_W + 6); i += blockDim.x) {
+    const int r = i / (DW_W + 6), c = i % (DW_W + 6);
+    const int xx = min(max(x0 - 3 + c, 0), W - 1);
+    const uint8_t* px = &raw[r][roff[r] + 3 * xx];
+    g[r][c] = (int16_t)gray_int(px[0], px[1], px[2]);  // features.py:34-36
+  }
+  __syncthreads();
+  for (int i = tid; i < (DW_H + 4) * (DW_W + 4); i += blockDim.x) {
+    const int r = i / (DW_W + 4), c = i % (DW_W + 4);
+    const int gr = r + 1, gc = c + 1;
+    const int colR = g[gr - 1][gc + 1] + 2 * g[gr][gc + 1] + g[gr + 1][gc + 1];
+    const int colL = g[gr - 1][gc - 1] + 2 * g[gr][gc - 1] + g[gr + 1][gc - 1];
+    const int rowD = g[gr + 1][gc - 1] + 2 * g[gr + 1][gc] + g[gr + 1][gc + 1];
+    const int rowU = g[gr - 1][gc - 1] + 2 * g[gr - 1][gc] + g[gr - 1][gc + 1];
+    const int xx = x0 - 2 + c, yy = y0 - 2 + r;
+    // off-image ring samples read the bias (features.py:95-101)
+    sxy[r][c] = (xx >= 0 && xx < W && yy >= 0 && yy < H)
+                    ? (uint16_t)(sobel_code_int(colR - colL) | (sobel_code_int(rowD - rowU) << 8))
+                    : (uint16_t)0x8080;
+  }
+  __syncthreads();
+  // pixel e * 256 + tid of the tile: a warp writes 32 consecutive descriptors
+#pragma unroll 2
+  for (int e = 0; e < 8; ++e) {
+    const int ty = e * 2 + (tid >> 7), tx = tid & 127;
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= W || y >= H) continue;
+    // descriptor bytes 2i, 2i+1 = (gx, gy) at ring offset i: halfword i
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      w[h] = (uint32_t)sxy[ty + 2 + c_ring_dv[2 * h]][tx + 2 + c_ring_du[2 * h]] |
+             ((uint32_t)sxy[ty + 2 + c_ring_dv[2 * h + 1]][tx + 2 + c_ring_du[2 * h + 1]] << 16);
+    const size_t o = (size_t)k * H * W + (size_t)y * W + x;
+    desc[o] = make_uint4(w[0], w[1], w[2], w[3]);
+    if (gray_out) gray_out[o] = (uint8_t)g[ty + 3][tx + 3];
+    if (sobel_out) {
+      const uint16_t c = sxy[ty + 2][tx + 2];
+      sobel_out[2 * o] = (uint8_t)(c & 0xff);
+      sobel_out[2 * o + 1] = (uint8_t)(c >> 8);
+    }
+  }
+}
+
 }  // namespace st
 
 extern "C" int st_descriptors(const uint8_t* images, int32_t K, int32_t H, int32_t W,
@@ -101,6 +209,14 @@ extern "C" int st_descriptors(const uint8_t* images, int32_t K, int32_t H, int32
   if (channels != 1 && channels != 3) {
     sthost::set_error("descriptors need 1 or 3 channels, got %d", channels);
     return ST_EINVAL;
+  }
+  if (channels == 3 && ((uintptr_t)images & 3) == 0 && getenv("ST_DESC_NARROW") == nullptr) {
+    dim3 grid((W + DW_W - 1) / DW_W, (H + DW_H - 1) / DW_H, K);
+    st::k_descriptors_wide<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        images, H, W, (size_t)K * H * W * 3, reinterpret_cast<uint4*>(desc_out), gray_out,
+        sobel_out);
+    ST_LAUNCH_CHECK("k_descriptors_wide");
+    return ST_OK;
   }
   dim3 block(DT_W, DT_H);
   dim3 grid((W + DT_W - 1) / DT_W, (H + DT_H - 1) / DT_H, K);

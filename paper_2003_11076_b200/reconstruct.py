@@ -10,6 +10,8 @@ so a frame costs its H2D copy, the kernels and the D2H of the artefacts.
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _native as N
@@ -80,7 +82,11 @@ class FramePipeline:
         self.frame.priors = self.priors.data_ptr()
         self.frame.desc = self.desc.data_ptr()
         self.frame.mu = self.mu.data_ptr()
-        self.side = t.cuda.Stream()
+        # the surface raster is a latency-bound pointer chase on the pre-solve
+        # critical path: its stream gets the higher priority, so its blocks are
+        # scheduled ahead of the descriptor / support-group kernels
+        prio = int(os.environ.get("ST_SIDE_PRIORITY", "-1"))
+        self.side = t.cuda.Stream(priority=prio)
         self.side2 = t.cuda.Stream()
 
     # -- inputs ---------------------------------------------------------------------
