@@ -1,0 +1,297 @@
+"""Frame directories in, artefact sets out.
+
+Drop-in for the reference's `pipeline.run_reconstruct` (pipeline.py:
+233-287) and the frame-directory loader it uses (pipeline.py:154-184),
+with the same file names, config keys, error texts and artefact bytes:
+
+    disparity.pgm (16-bit, fixed point x256), disparity_scale.txt,
+    refocused.ppm, provenance.pgm, status.pgm, n_rays.pgm, seg_XX.pgm,
+    valid_XX.pgm, config_used.txt, em_stats.txt, timings.txt
+
+The compute stages run on the device (`reconstruct_frame`: device harvest
++ native dedup, host Qhull, device solve + refocus); only parsing, file
+I/O and PNM framing stay on the host.  `run_reconstruct_sequence` streams
+many frame directories through `reconstruct_frames` (pinned H2D, Qhull
+process pool, pipelined device solve) with the artefact writes on a
+thread pool, for sequence throughput (BASELINE C5).
+"""
+
+import os
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from . import pnm
+from .frame import LightFieldFrame
+from .geometry import CalibrationError, load_calibration
+from .prior import PriorParams
+from .refocus import PROV_COPIED, PROV_FALLBACK, PROV_REFOCUSED  # noqa: F401
+from .solver import STATUS_VALID, SolverParams
+
+DISPARITY_SCALE = 256.0
+
+
+class PipelineError(Exception):
+    """Input or artefact problem; maps to process exit code 2 (pipeline.py:44-47)."""
+
+    exit_code = 2
+
+
+# -- configuration (pipeline.py:52-113) --------------------------------------------
+
+def _boolean(text):
+    word = text.strip().lower()
+    if word in ("1", "true", "yes", "on"):
+        return True
+    if word in ("0", "false", "no", "off"):
+        return False
+    raise ValueError(f"not a boolean: {text!r}")
+
+
+_OPTIONS = {
+    "beta": float, "sigma": float, "gamma": float, "d_max": float, "threshold": float,
+    "max_iters": int, "min_static_rays": int, "epsilon_prior": float,
+    "median_radius": int, "dynamic_only": _boolean,
+}
+_SOLVER_KEYS = ("beta", "threshold", "max_iters", "min_static_rays", "epsilon_prior")
+_PRIOR_KEYS = ("sigma", "gamma", "d_max")
+
+
+def parse_config(path):
+    """`key = value` lines with '#' comments -> dict of typed overrides."""
+    out = {}
+    with open(path, "r") as fh:
+        for n, raw in enumerate(fh, start=1):
+            text = raw.split("#", 1)[0].strip()
+            if not text:
+                continue
+            if "=" not in text:
+                raise PipelineError(f"{path}:{n}: expected key = value")
+            key, _, value = (s.strip() for s in text.partition("="))
+            if key not in _OPTIONS:
+                raise PipelineError(f"{path}:{n}: unknown option {key!r}")
+            try:
+                out[key] = _OPTIONS[key](value)
+            except ValueError:
+                raise PipelineError(f"{path}:{n}: bad value for {key}: {value!r}")
+    return out
+
+
+def resolve_params(overrides=None):
+    """overrides -> (SolverParams, PriorParams, median_radius, dynamic_only)."""
+    rest = dict(overrides or {})
+    solver, prior = SolverParams(), PriorParams()
+    for key in _SOLVER_KEYS:
+        if key in rest:
+            setattr(solver, key, rest.pop(key))
+    for key in _PRIOR_KEYS:
+        if key in rest:
+            setattr(prior, key, rest.pop(key))
+    median_radius = int(rest.pop("median_radius", 1))
+    dynamic_only = bool(rest.pop("dynamic_only", False))
+    if rest:
+        raise PipelineError(f"unknown options: {sorted(rest)}")
+    if median_radius < 0:
+        raise PipelineError("median_radius must be >= 0")
+    return solver, prior, median_radius, dynamic_only
+
+
+# -- frame directories (pipeline.py:151-184) ----------------------------------------
+
+def view_name(stem, k, ext):
+    return f"{stem}_{k:02d}.{ext}"
+
+
+def load_frame_dir(rig, frames_dir, priors_dir=None):
+    """view_XX.ppm + prior_XX.pgm for every camera of the rig -> LightFieldFrame."""
+    priors_dir = priors_dir or frames_dir
+    images, priors = [], []
+    for k in range(len(rig)):
+        vpath = os.path.join(frames_dir, view_name("view", k, "ppm"))
+        ppath = os.path.join(priors_dir, view_name("prior", k, "pgm"))
+        for what, path in (("image", vpath), ("prior", ppath)):
+            if not os.path.exists(path):
+                raise PipelineError(f"view {k}: missing {what} {path}")
+        img = pnm.read_pnm(vpath)
+        if img.ndim != 3:
+            raise PipelineError(f"view {k}: {vpath} is not a color image")
+        intr = rig.intrinsics(k)
+        if img.shape[:2] != (intr.height, intr.width):
+            raise PipelineError(f"view {k}: image is {img.shape[1]}x{img.shape[0]}, "
+                                f"calibration says {intr.width}x{intr.height}")
+        pri = pnm.read_pnm(ppath)
+        if pri.ndim != 2:
+            raise PipelineError(f"view {k}: {ppath} is not grayscale")
+        if pri.shape != img.shape[:2]:
+            raise PipelineError(f"view {k}: prior is {pri.shape[1]}x{pri.shape[0]}, "
+                                f"image is {img.shape[1]}x{img.shape[0]}")
+        full = 65535.0 if pri.dtype == np.uint16 else 255.0
+        images.append(img)
+        priors.append(pri.astype(np.float32) / full)
+    return LightFieldFrame(images=images, priors=priors)
+
+
+def write_frame_dir(out_dir, frame, rig):
+    """The input half of the reference's run_synth writes (pipeline.py:338-345):
+    calib.txt, view_XX.ppm and the 8-bit coded prior_XX.pgm."""
+    from .geometry import save_calibration
+    os.makedirs(out_dir, exist_ok=True)
+    save_calibration(rig, os.path.join(out_dir, "calib.txt"))
+    for k in range(frame.num_views):
+        pnm.write_ppm(os.path.join(out_dir, view_name("view", k, "ppm")), frame.images[k])
+        code = np.clip(np.rint(np.asarray(frame.priors[k]) * 255.0), 0, 255).astype(np.uint8)
+        pnm.write_pgm(os.path.join(out_dir, view_name("prior", k, "pgm")), code)
+
+
+# -- artefacts (pipeline.py:187-193, 247-305) -------------------------------------
+
+def disparity_code(disparity):
+    """16-bit fixed point x256, 0 where the status is not VALID."""
+    code = np.zeros(disparity.values.shape, dtype=np.uint16)
+    ok = disparity.status == STATUS_VALID
+    code[ok] = np.clip(np.rint(disparity.values[ok] * DISPARITY_SCALE), 0, 65535).astype(np.uint16)
+    return code
+
+
+def _config_text(solver, prior, median_radius, dynamic_only):
+    rows = [("beta", repr(solver.beta)), ("sigma", repr(prior.sigma)),
+            ("gamma", repr(prior.gamma)), ("d_max", repr(prior.d_max)),
+            ("threshold", repr(solver.threshold)), ("max_iters", str(solver.max_iters)),
+            ("min_static_rays", str(solver.min_static_rays)),
+            ("epsilon_prior", repr(solver.epsilon_prior)),
+            ("median_radius", str(median_radius)), ("dynamic_only", str(int(dynamic_only)))]
+    return "".join(f"{k} = {v}\n" for k, v in rows)
+
+
+def _stats_text(stats):
+    def row(values):
+        return ",".join(repr(float(v)) for v in values)
+    conv = "none" if stats.converged_after is None else str(stats.converged_after)
+    return (f"iterations_run = {stats.iterations_run}\n"
+            f"converged_after = {conv}\n"
+            f"mean_energy = {row(stats.mean_energy)}\n"
+            f"prev_energy = {row(stats.prev_energy)}\n"
+            f"changed_fraction = {row(stats.changed_fraction)}\n")
+
+
+def artefact_files(rec, num_views, solver, prior, median_radius, dynamic_only):
+    """{file name: bytes} of one run's artefact set, timings.txt excluded."""
+    files = {
+        "disparity.pgm": pnm.encode_pgm(disparity_code(rec.disparity)),
+        "disparity_scale.txt": f"{int(DISPARITY_SCALE)}\n".encode(),
+        "refocused.ppm": pnm.encode_ppm(rec.image),
+        "provenance.pgm": pnm.encode_pgm(rec.provenance),
+        "status.pgm": pnm.encode_pgm(rec.disparity.status),
+        "n_rays.pgm": pnm.encode_pgm(rec.n_rays),
+    }
+    sb = rec.segmentation.static_bits.astype(np.uint32)
+    vb = rec.segmentation.valid_bits.astype(np.uint32)
+    for k in range(num_views):
+        files[view_name("seg", k, "pgm")] = pnm.encode_pgm(
+            (((sb >> np.uint32(k)) & np.uint32(1)) * 255).astype(np.uint8))
+        files[view_name("valid", k, "pgm")] = pnm.encode_pgm(
+            (((vb >> np.uint32(k)) & np.uint32(1)) * 255).astype(np.uint8))
+    files["config_used.txt"] = _config_text(solver, prior, median_radius, dynamic_only).encode()
+    files["em_stats.txt"] = _stats_text(rec.stats).encode()
+    return files
+
+
+def _write_files(out_dir, files):
+    os.makedirs(out_dir, exist_ok=True)
+    for name, data in files.items():
+        with open(os.path.join(out_dir, name), "wb") as fh:
+            fh.write(data)
+
+
+def _write_timings(out_dir, timings, threads):
+    text = "" if threads is None else f"# threads_hint = {threads}\n"
+    text += "".join(f"{name} {sec:.3f}\n" for name, sec in timings)
+    text += f"total {sum(s for _, s in timings):.3f}\n"
+    with open(os.path.join(out_dir, "timings.txt"), "w") as fh:
+        fh.write(text)
+
+
+def _setup(calib_path, config, ref_index, dynamic_only):
+    overrides = parse_config(config) if isinstance(config, str) else dict(config or {})
+    solver, prior, median_radius, cfg_dynamic = resolve_params(overrides)
+    if dynamic_only is not None:
+        cfg_dynamic = bool(dynamic_only)
+    try:
+        rig = load_calibration(calib_path, ref_index=ref_index)
+    except (CalibrationError, OSError) as exc:
+        raise PipelineError(f"calibration: {exc}")
+    return rig, solver, prior, median_radius, cfg_dynamic
+
+
+def _load(rig, frames_dir, priors_dir):
+    try:
+        return load_frame_dir(rig, frames_dir, priors_dir)
+    except PipelineError:
+        raise
+    except (ValueError, OSError) as exc:
+        raise PipelineError(str(exc))
+
+
+def run_reconstruct(calib_path, frames_dir, out_dir, priors_dir=None, config=None,
+                    ref_index=None, dynamic_only=None, threads=None):
+    """pipeline.py:233-287: solve one frame directory and write its artefacts.
+
+    `threads` is a hint only, as in the reference: no output depends on it.
+    Returns {"out_dir", "stats", "timings", "total_seconds"}."""
+    from .reconstruct import reconstruct_frame
+    rig, solver, prior, median_radius, dyn = _setup(calib_path, config, ref_index, dynamic_only)
+    frame = _load(rig, frames_dir, priors_dir)
+    os.makedirs(out_dir, exist_ok=True)
+    stage = {}
+    try:
+        rec, _ = reconstruct_frame(frame, rig, solver, prior, dynamic_only=dyn,
+                                   median_radius=median_radius, timings=stage)
+    except ValueError as exc:  # e.g. a degenerate support set (prior.py:330-349)
+        raise PipelineError(str(exc))
+    t0 = time.perf_counter()
+    _write_files(out_dir, artefact_files(rec, frame.num_views, solver, prior, median_radius, dyn))
+    timings = [("support", stage["support"]), ("triangulate", stage["triangulate"]),
+               ("solve_refocus", stage["solve_refocus"]), ("write", time.perf_counter() - t0)]
+    _write_timings(out_dir, timings, threads)
+    return {"out_dir": out_dir, "stats": rec.stats, "timings": dict(timings),
+            "total_seconds": sum(s for _, s in timings)}
+
+
+def run_reconstruct_sequence(calib_path, frame_dirs, out_dirs, priors_dirs=None, config=None,
+                             ref_index=None, dynamic_only=None, threads=None, workers=None):
+    """run_reconstruct over a sequence of frame directories, streamed: frames
+    are read ahead on a thread pool, reconstructed by `reconstruct_frames`
+    (device harvest, Qhull process pool, pipelined device solve) and their
+    artefacts written on the same pool.  Every directory's artefacts equal
+    those of run_reconstruct on it alone.  Returns the per-frame EMStats."""
+    from .reconstruct import reconstruct_frames
+    frame_dirs, out_dirs = list(frame_dirs), list(out_dirs)
+    if len(frame_dirs) != len(out_dirs):
+        raise PipelineError("frame_dirs and out_dirs differ in length")
+    priors_dirs = list(priors_dirs) if priors_dirs is not None else [None] * len(frame_dirs)
+    rig, solver, prior, median_radius, dyn = _setup(calib_path, config, ref_index, dynamic_only)
+    io = ThreadPoolExecutor(max_workers=max(2, min(8, os.cpu_count() or 2)))
+    try:
+        reads = [io.submit(_load, rig, f, p) for f, p in zip(frame_dirs, priors_dirs)]
+        frames = (r.result() for r in reads)
+        writes, stats = [], []
+        t_start = time.perf_counter()
+        for out_dir, rec in zip(out_dirs, reconstruct_frames(
+                frames, rig, solver, prior, dynamic_only=dyn, median_radius=median_radius,
+                workers=workers)):
+            files = artefact_files(rec, len(rig), solver, prior, median_radius, dyn)
+            writes.append(io.submit(_write_files, out_dir, files))
+            stats.append(rec.stats)
+        for w in writes:
+            w.result()
+        total = time.perf_counter() - t_start
+        for out_dir in out_dirs:
+            _write_timings(out_dir, [("sequence_total", total)], threads)
+    except ValueError as exc:
+        if isinstance(exc, PipelineError):
+            raise
+        raise PipelineError(str(exc))
+    finally:
+        io.shutdown(wait=True)
+    return stats
