@@ -188,7 +188,8 @@ def next_rows(frame, rig, cfg, pipe, host_frame, peak, cpu_leg=True):
     """SURVEY 8(f) rows widened this round, measured like the hot path:
     (f)1 the device support harvest (st_harvest + native dedup) with its
     roofline and a CPU-port baseline, (f)2 host Qhull + device planes /
-    transforms, and the frame-in stream (reconstruct_frames)."""
+    transforms, the frame-in stream (reconstruct_frames) and (f)3 frame
+    directories -> artefact directories (run_reconstruct_sequence)."""
     import torch
     import paper_2003_11076_b200 as st
     from paper_2003_11076_b200 import _native as N
@@ -236,6 +237,30 @@ def next_rows(frame, rig, cfg, pipe, host_frame, peak, cpu_leg=True):
         pass
     torch.cuda.synchronize()
     fi_fps = n_fi / (time.perf_counter() - t0)
+    # (f)3 frame directories on disk -> artefact sets on disk (run_reconstruct_sequence)
+    import shutil
+    import tempfile
+    from paper_2003_11076_b200 import pipeline as PL
+    base = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    io_dir = tempfile.mkdtemp(prefix="st_bench_io_", dir=base)
+    try:
+        fdir = os.path.join(io_dir, "frames")
+        PL.write_frame_dir(fdir, host_frame, rig)
+        calib = os.path.join(fdir, "calib.txt")
+        PL.run_reconstruct_sequence(calib, [fdir] * 2, [os.path.join(io_dir, f"w{i}")
+                                                         for i in range(2)])
+        n_io = 24
+        outs = [os.path.join(io_dir, f"o{i}") for i in range(n_io)]
+        t0 = time.perf_counter()
+        PL.run_reconstruct_sequence(calib, [fdir] * n_io, outs)
+        io_fps = n_io / (time.perf_counter() - t0)
+        art = sum(os.path.getsize(os.path.join(outs[0], f)) for f in os.listdir(outs[0]))
+        inp = sum(os.path.getsize(os.path.join(fdir, f)) for f in os.listdir(fdir))
+        t0 = time.perf_counter()
+        res = PL.run_reconstruct(calib, fdir, os.path.join(io_dir, "single"))
+        single_s = time.perf_counter() - t0
+    finally:
+        shutil.rmtree(io_dir, ignore_errors=True)
     out = {
         "harvest": {"device_ms": hv_ms, "includes": "descriptors + st_harvest",
                     "candidates": n_cand, "reverse_scans": n_rev, "grid": nd,
@@ -251,6 +276,13 @@ def next_rows(frame, rig, cfg, pipe, host_frame, peak, cpu_leg=True):
         "frame_in_stream": {"value": fi_fps, "unit": "frames/s", "frames": n_fi,
                             "qhull_workers": n_workers,
                             "api": "reconstruct_frames (raw frames in, artefacts out)"},
+        "frame_io_stream": {"value": io_fps, "unit": "frames/s", "frames": n_io,
+                            "input_bytes_per_frame": inp, "artefact_bytes_per_frame": art,
+                            "storage": base or "tempdir",
+                            "api": "pipeline.run_reconstruct_sequence (frame directories "
+                                   "in, artefact directories out)",
+                            "single_run_reconstruct_s": single_s,
+                            "single_stage_s": res["timings"]},
     }
     if cpu_leg:
         import oracle

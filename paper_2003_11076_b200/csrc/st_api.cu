@@ -626,7 +626,7 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       launch_e_step(rig->num_views, n_act, s, c, e);
       ST_LAUNCH_CHECK("k_e_step_at");
       ev.record(2, s);
-      const int sblk = (int)blocks_for(n_act, STATS_BLOCK);
+      const int sblk = std::min((int)blocks_for(n_act, STATS_BLOCK), STATS_GRID);
       st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(n_act, it > 1, e_act, pe_act, chg, work, nwarps,
                                                   parts);
       ST_LAUNCH_CHECK("k_em_stats");
@@ -748,7 +748,7 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
   const int iters = std::min(p->forced_iters > 0 ? p->forced_iters : p->max_iters, 64);
   const int nblk = (int)blocks_for(npx, EM_BLOCK);
   const int nwarps = nblk * (EM_BLOCK / 32);
-  const int sblk = (int)blocks_for(npx, STATS_BLOCK);
+  const int sblk = std::min((int)blocks_for(npx, STATS_BLOCK), STATS_GRID);
   // iterations >= 2 work on device-counted worklists (a fraction of the
   // pixels) and do nothing once converged: one wave of grid-stride blocks
   const int wave = std::min(nblk, 148 * 8);

@@ -497,24 +497,38 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ 
                            const Partial* __restrict__ work, int n_work_parts,
                            Partial* __restrict__ parts, const int* stop) {
   if (stop && *stop) return;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // fixed grid (STATS_GRID), fixed per-thread order: deterministic sums
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   double se = 0.0, spe = 0.0;
   long long nf = 0, npf = 0, nch = 0;
-  if (i < n) {
+  for (int64_t i = t0; i < n; i += stride) {
     const double x = e[i];
     if (isfinite(x)) {
-      se = x;
-      nf = 1;
+      se += x;
+      nf += 1;
     }
     if (with_prev) {
       const double y = pe[i];
       if (isfinite(y)) {
-        spe = y;
-        npf = 1;
+        spe += y;
+        npf += 1;
       }
-      nch = chg[i];
+      nch += chg[i];
     }
   }
+  // the M-step's per-warp work counters (integers: any order is exact)
+  long long wc = 0, we = 0, wh = 0, ws = 0;
+  for (int64_t w = t0; w < n_work_parts; w += stride) {
+    wc += work[w].n_cand;
+    we += work[w].n_eval;
+    wh += work[w].n_hopeless;
+    ws += work[w].n_samples;
+  }
+  wc = warp_sum(wc);
+  we = warp_sum(we);
+  wh = warp_sum(wh);
+  ws = warp_sum(ws);
   se = warp_sum(se);
   spe = warp_sum(spe);
   nf = warp_sum(nf);
@@ -524,20 +538,16 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ 
   __shared__ Partial sp[STATS_BLOCK / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) {
-    const int64_t w = i >> 5;
     Partial P = {};
     P.sum_e = se;
     P.sum_pe = spe;
     P.n_fin = nf;
     P.n_pfin = npf;
     P.n_changed = nch;
-    // fold the M-step's work counters (warp w of that launch) in as well
-    if (w < n_work_parts) {
-      P.n_cand = work[w].n_cand;
-      P.n_eval = work[w].n_eval;
-      P.n_hopeless = work[w].n_hopeless;
-      P.n_samples = work[w].n_samples;
-    }
+    P.n_cand = wc;
+    P.n_eval = we;
+    P.n_hopeless = wh;
+    P.n_samples = ws;
     sp[wid] = P;
   }
   __syncthreads();

@@ -204,6 +204,11 @@ def _write_files(out_dir, files):
             fh.write(data)
 
 
+def _encode_and_write(out_dir, rec, num_views, solver, prior, median_radius, dynamic_only):
+    _write_files(out_dir, artefact_files(rec, num_views, solver, prior, median_radius,
+                                         dynamic_only))
+
+
 def _write_timings(out_dir, timings, threads):
     text = "" if threads is None else f"# threads_hint = {threads}\n"
     text += "".join(f"{name} {sec:.3f}\n" for name, sec in timings)
@@ -280,8 +285,8 @@ def run_reconstruct_sequence(calib_path, frame_dirs, out_dirs, priors_dirs=None,
         for out_dir, rec in zip(out_dirs, reconstruct_frames(
                 frames, rig, solver, prior, dynamic_only=dyn, median_radius=median_radius,
                 workers=workers)):
-            files = artefact_files(rec, len(rig), solver, prior, median_radius, dyn)
-            writes.append(io.submit(_write_files, out_dir, files))
+            writes.append(io.submit(_encode_and_write, out_dir, rec, len(rig), solver, prior,
+                                    median_radius, dyn))
             stats.append(rec.stats)
         for w in writes:
             w.result()
