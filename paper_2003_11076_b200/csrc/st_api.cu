@@ -750,8 +750,13 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
   const int nwarps = nblk * (EM_BLOCK / 32);
   const int sblk = std::min((int)blocks_for(npx, STATS_BLOCK), STATS_GRID);
   // iterations >= 2 work on device-counted worklists (a fraction of the
-  // pixels) and do nothing once converged: one wave of grid-stride blocks
-  const int wave = std::min(nblk, 148 * 8);
+  // pixels) and do nothing once converged: a fixed grid of grid-stride
+  // blocks (16 per SM measured best: the worklists' items are latency-bound)
+  static const int wave_env = [] {
+    const char* e = getenv("ST_WAVE_BLOCKS_PER_SM");
+    return e ? atoi(e) : 16;
+  }();
+  const int wave = std::min(nblk, 148 * wave_env);
   for (int it = 1; it <= iters; ++it) {
     if (it > 1) {
       st::k_flag_mstep<<<wave, EM_BLOCK, 0, s>>>(nullptr, npx, static_bits, mask_in, e_act,

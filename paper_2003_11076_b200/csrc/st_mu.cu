@@ -41,6 +41,7 @@ namespace st {
 
 struct TriDev {
   const double *pts, *disp, *planes, *transform, *equations;
+  const double* nb_eq;  // (n_tri, 3, 4): the neighbours' lifted facet equations (0 for none)
   const int32_t *simp, *nb;
   int n_pts, n_tri;
   double ps, psh, lo0, lo1, hi0, hi1;
@@ -155,6 +156,30 @@ __global__ void k_claim(TriDev d, int W, const int4* __restrict__ bbox,
   }
 }
 
+// Neighbour equations gathered per simplex, so a paraboloid sweep reads
+// them from its own simplex's row (one dependent load round per walk step
+// instead of two: nb, then the neighbour's equation).
+__global__ void k_nb_equations(TriDev d, double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d.n_tri) return;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int m = d.nb[3 * t + k];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[12 * t + 4 * k + i] = m >= 0 ? d.equations[4 * m + i] : 0.0;
+  }
+}
+
+// scipy _distplane on the lifted point, equation at e.
+__device__ __forceinline__ double distplane_eq(const double* __restrict__ e, double z0, double z1,
+                                               double z2) {
+  double dist = __ldg(e + 3);
+  dist = dadd(dist, dmul(__ldg(e), z0));
+  dist = dadd(dist, dmul(__ldg(e + 1), z1));
+  dist = dadd(dist, dmul(__ldg(e + 2), z2));
+  return dist;
+}
+
 // scipy _distplane on the lifted point.
 __device__ __forceinline__ double distplane(const TriDev& d, int s, double z0, double z1,
                                             double z2) {
@@ -217,6 +242,9 @@ __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0
   bool changed = true;
   while (changed) {
     if (best > 0.0) break;
+#ifdef MU_DIAG
+    atomicAdd(w.counts + 7, 1u);  // paraboloid sweeps
+#endif
     changed = false;
     // the three neighbours' distances, fetched in parallel; used as long as
     // s has not moved inside this sweep (scipy reads the neighbours of the
@@ -225,16 +253,13 @@ __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0
     const int s0 = s;
     double pre[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int m = tc.nb(k);
-      pre[k] = m >= 0 ? distplane(d, m, x0, x1, z2) : 0.0;
-    }
+    for (int k = 0; k < 3; ++k) pre[k] = distplane_eq(d.nb_eq + 12 * s0 + 4 * k, x0, x1, z2);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       tc.ensure(d, s);
       const int m = tc.nb(k);
       if (m == -1) continue;
-      const double dd = s == s0 ? pre[k] : distplane(d, m, x0, x1, z2);
+      const double dd = s == s0 ? pre[k] : distplane_eq(d.nb_eq + 12 * s + 4 * k, x0, x1, z2);
       if (dd > dadd(best, dmul(eps, dadd(1.0, fabs(best))))) {
         s = m;
         best = dd;
@@ -381,6 +406,8 @@ __global__ void __launch_bounds__(128, WALK_MIN_BLOCKS)
   // simplex, and that ends its run (so no later walk starts from its end
   // state), cannot influence mu: skip the walk.  This is the common case
   // (including the image-corner vertices, whose walks start a full row away).
+  int64_t end;
+  bool ends_run;
   {
     int64_t q = p;
     bool agnostic = true;
@@ -389,7 +416,11 @@ __global__ void __launch_bounds__(128, WALK_MIN_BLOCKS)
       w.chunk_of[q] = (int32_t)p;
       ++q;
     } while (q < npx && ambiguous(w, q) && !chunk_start(w, q));
-    const bool ends_run = q >= npx || !ambiguous(w, q);
+    end = q;
+    ends_run = q >= npx || !ambiguous(w, q);
+#ifdef MU_DIAG
+    atomicMax(w.counts + 5, (unsigned)(q - p));                    // longest chunk
+#endif
     if (agnostic && ends_run) {
       w.len[p] = (int32_t)(q - p);
       w.end0[p] = w.end1[p] = -1;  // never read: the run ends here
@@ -397,23 +428,29 @@ __global__ void __launch_bounds__(128, WALK_MIN_BLOCKS)
     }
   }
   if (nopt == 1) w.chosen[p] = 0;  // a run start: its incoming start is known
-  int64_t q = p;
+#ifdef MU_DIAG
+  const long long clk0 = clock64();
+#endif
+  // the chunk's extent is known from the scan: no per-pixel reload in the walk
   int st0 = opts[0], st1 = nopt > 1 ? opts[1] : 0;
   TriCache tc0, tc1;
-  do {
+  for (int64_t q = p; q < end; ++q) {
     const double x0 = (double)(q % W), x1 = (double)(q / W);
     w.res0[q] = find_simplex(d, w, q, x0, x1, st0, tc0);
     if (nopt > 1) w.res1[q] = find_simplex(d, w, q, x0, x1, st1, tc1);
-    w.chunk_of[q] = (int32_t)p;
-    ++q;
-  } while (q < npx && ambiguous(w, q) && !chunk_start(w, q));
+  }
+  const int64_t q = end;
   w.len[p] = (int32_t)(q - p);
+#ifdef MU_DIAG
+  atomicMax(w.counts + 6, (unsigned)min(clock64() - clk0, 0xffffffffll));  // slowest walk
+  atomicAdd(w.counts + 3, (unsigned)((clock64() - clk0) >> 10));            // total kcycles
+#endif
   w.end0[p] = st0;
   w.end1[p] = nopt > 1 ? st1 : st0;
   // Both speculative walks ended in the same simplex (the usual, "sticky"
   // case): the next chunk's incoming start no longer depends on this
   // chunk's choice, so decide it here.
-  if (w.end0[p] == w.end1[p] && q < npx && ambiguous(w, q)) {
+  if (w.end0[p] == w.end1[p] && !ends_run) {
     if ((int)w.tmin[q - 1] == st0)
       w.chosen[q] = 0;
     else if ((int)w.tmax[q - 1] == st0)
@@ -509,7 +546,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct MuLayout {
   size_t off[16];
-  size_t bbox, area, start, cub, cub_bytes;
+  size_t bbox, area, start, nb_eq, cub, cub_bytes;
   size_t total;
 };
 
@@ -526,6 +563,7 @@ MuLayout mu_layout(int W, int H, int n_tri) {
   L.bbox = o;  o += align_up(sizeof(int4) * nt);
   L.area = o;  o += align_up(sizeof(unsigned long long) * nt);
   L.start = o; o += align_up(sizeof(unsigned long long) * nt);
+  L.nb_eq = o; o += align_up(sizeof(double) * 12 * nt);
   L.cub_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, L.cub_bytes, (unsigned long long*)nullptr,
                                 (unsigned long long*)nullptr, (int)nt);
@@ -756,6 +794,7 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   d.lo1 = tri->min_bound[1];
   d.hi0 = tri->max_bound[0];
   d.hi1 = tri->max_bound[1];
+  d.nb_eq = (const double*)(ws + L.nb_eq);
   const int64_t npx = (int64_t)W * H;
   static const bool prof_on = getenv("ST_MU_PROFILE") != nullptr;  // diagnostics
   cudaEvent_t pev[8];
@@ -780,6 +819,8 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
     ST_CUDA_CHECK(cudaMemsetAsync(area + d.n_tri, 0, sizeof(unsigned long long), s));
     st::k_tri_bbox<<<(d.n_tri + 127) / 128, 128, 0, s>>>(d, W, H, bbox, area);
     ST_LAUNCH_CHECK("k_tri_bbox");
+    st::k_nb_equations<<<(d.n_tri + 127) / 128, 128, 0, s>>>(d, (double*)(ws + L.nb_eq));
+    ST_LAUNCH_CHECK("k_nb_equations");
     size_t tb = L.cub_bytes;
     ST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws + L.cub, tb, area, start, d.n_tri + 1, s));
     sthost::count_launch();
@@ -809,9 +850,12 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
       cudaEventElapsedTime(&ms, pev[i - 1], pev[i]);
       fprintf(stderr, " %.4f", ms);
     }
-    unsigned cnts[2] = {0, 0};
+    unsigned cnts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpy(cnts, w.counts, sizeof(cnts), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "  chunks %u\n", cnts[0]);
+    fprintf(stderr,
+            "  chunks %u - %u walk-kcycles %u - %u longest %u slowest-walk-cycles %u "
+            "paraboloid-sweeps %u\n",
+            cnts[0], cnts[2], cnts[3], cnts[4], cnts[5], cnts[6], cnts[7]);
     for (int i = 0; i < npev; ++i) cudaEventDestroy(pev[i]);
   }
   return ST_OK;
