@@ -138,6 +138,7 @@ typedef struct {
   int32_t n_pts, n_tri;
   double paraboloid_scale, paraboloid_shift;
   double min_bound[2], max_bound[2];
+  double centroid[2];         /* points.mean(axis=0) as numpy computes it (prior.py:290) */
 } st_tri;
 
 /* The two per-triangle tables the reference computes on the host with

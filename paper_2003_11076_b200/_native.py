@@ -53,7 +53,8 @@ class StTri(C.Structure):
                 ("planes", C.c_void_p), ("neighbors", C.c_void_p), ("transform", C.c_void_p),
                 ("equations", C.c_void_p), ("n_pts", C.c_int32), ("n_tri", C.c_int32),
                 ("paraboloid_scale", C.c_double), ("paraboloid_shift", C.c_double),
-                ("min_bound", C.c_double * 2), ("max_bound", C.c_double * 2)]
+                ("min_bound", C.c_double * 2), ("max_bound", C.c_double * 2),
+                ("centroid", C.c_double * 2)]
 
 
 class StCams(C.Structure):

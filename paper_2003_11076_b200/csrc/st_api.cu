@@ -179,19 +179,26 @@ void launch_e_step(int K, int64_t n, cudaStream_t s, const st::EmCtx& c,
   const bool exhaustive = getenv("ST_ESTEP_EXHAUSTIVE") != nullptr;  // cross-check
   st::EStepArgs a = args;
   a.exhaustive = exhaustive ? 1 : 0;
-  if (K <= 5 && a.flist && !exhaustive) {
+  if (a.flist && !exhaustive) {
     cudaMemsetAsync(a.flist_count, 0, sizeof(uint32_t), s);
     const unsigned bc = blocks_for(n, ESTEP_CERT_BLOCK);
     switch (K) {
       case 2: launch_cert<2>(bc, s, c, a); break;
       case 3: launch_cert<3>(bc, s, c, a); break;
       case 4: launch_cert<4>(bc, s, c, a); break;
-      default: launch_cert<5>(bc, s, c, a); break;
+      case 5: launch_cert<5>(bc, s, c, a); break;
+      default:  // 6 <= K <= 12: enumerated bounds, branch-and-bound fallback
+        if (c.rectified)
+          st::k_e_step_cert_big<true><<<bc, CERT_BIG_BLOCK, 0, s>>>(c, a);
+        else
+          st::k_e_step_cert_big<false><<<bc, CERT_BIG_BLOCK, 0, s>>>(c, a);
+        break;
     }
     sthost::count_launch();
     a.list = a.flist;
     a.list_count = a.flist_count;
-    n = std::min<int64_t>(n, 148 * ESTEP_MIN_BLOCKS * ESTEP_TAPS_BLOCK);
+    n = std::min<int64_t>(n, K <= 5 ? 148 * ESTEP_MIN_BLOCKS * ESTEP_TAPS_BLOCK
+                                     : 148 * 8 * ESTEP_BLOCK);
   }
   const unsigned bt = blocks_for(n, ESTEP_TAPS_BLOCK);
   switch (K) {

@@ -6,6 +6,7 @@
 // reference's per-pixel independence, solver.py:30-32); candidate energies
 // never leave registers (no cost volume in HBM).
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <math.h>
 #include <stdint.h>
 
@@ -880,6 +881,103 @@ __device__ uint32_t estep_generic(int K, const double* __restrict__ f, int strid
   return bm;
 }
 
+// Same argmax by bounding (6 <= K <= 12).  P(m) = fl(a + b), the prior sum
+// in the reference's order, bounds score(m) = fl(P(m) - fl(beta v(m)))
+// from above (v >= 0, fl monotone) and equals it up to the constant penalty
+// when pop(m) < min_static_rays.  The bounds are evaluated as exact integer
+// sums of the logs rounded to 2^-20 units, |Pq/2^20 - P| <= (K/2 + 3) 2^-20
+// (rounding of each term, the fp64 sum's own roundings).  The mask with the
+// largest bound is scored exactly first; every other admissible mask is
+// scored exactly only if its bound can still reach the best exact score, so
+// no skipped mask can tie or win.  Normally one or two exact scores instead
+// of 2^K.
+__device__ double score_generic(uint32_t m, int K, const double* __restrict__ f, int stride,
+                                const double* l1, const double* l0, const st_params& p) {
+  const int pop = __popc(m);
+  double vr;
+  if (pop < p.min_static_rays) {
+    vr = variance_ceiling();
+  } else {
+    double acc = 0.0;
+    for (int ch = 0; ch < 16; ++ch) {
+      double a1 = 0.0, a2 = 0.0;
+      int n = 0;
+      for (uint32_t r = m; r; r &= r - 1) {
+        const int k = __ffs(r) - 1;
+        const double x = f[(k * 16 + ch) * stride];
+        a1 = n ? dadd(a1, x) : x;
+        const double x2 = dmul(x, x);
+        a2 = n ? dadd(a2, x2) : x2;
+        ++n;
+      }
+      acc = dadd(acc, dsub(a2, div_n(dmul(a1, a1), n)));
+    }
+    vr = fmax(div_n(acc, pop), 0.0);
+  }
+  double a = 0.0, b = 0.0;
+  for (int k = 0; k < K; ++k) {
+    if ((m >> k) & 1)
+      a = dadd(a, l1[k]);
+    else
+      b = dadd(b, l0[k]);
+  }
+  return dsub(dadd(a, b), dmul(p.beta, vr));
+}
+
+__device__ uint32_t estep_bnb(int K, const double* __restrict__ f, int stride, const double* l1,
+                              const double* l0, uint32_t vbits, const st_params& p) {
+  constexpr double QS = 1048576.0;  // 2^20
+  long long dq[ST_MAX_VIEWS];
+  long long base = 0;
+  double lmax = 0.0;
+#pragma unroll
+  for (int k = 0; k < ST_MAX_VIEWS; ++k) {
+    dq[k] = 0;
+    if (k < K) {
+      const long long q1 = __double2ll_rn(l1[k] * QS), q0 = __double2ll_rn(l0[k] * QS);
+      dq[k] = q1 - q0;
+      base += q0;
+      lmax = fmax(lmax, fmax(fabs(l1[k]), fabs(l0[k])));
+    }
+  }
+  const long long penq = __double2ll_rn(fmin(dmul(p.beta, variance_ceiling()) * QS, 1e15));
+  const double errq = 0.5 * K + 3.0 + 1e-12 * K * lmax * QS;
+  auto bound = [&](uint32_t m) -> long long {
+    long long ub = base;
+#pragma unroll
+    for (int k = 0; k < ST_MAX_VIEWS; ++k)
+      if ((m >> k) & 1) ub += dq[k];
+    return __popc(m) < p.min_static_rays ? ub - penq : ub;
+  };
+  // the largest bound first
+  uint32_t mtop = 0;
+  long long btop = bound(0);
+  for (uint32_t m = vbits; m; m = (m - 1) & vbits) {
+    const long long ub = bound(m);
+    if (ub > btop) {
+      btop = ub;
+      mtop = m;
+    }
+  }
+  double best = score_generic(mtop, K, f, stride, l1, l0, p);
+  int bpop = __popc(mtop);
+  uint32_t bm = mtop;
+  uint32_t m = 0;
+  do {
+    if (m != mtop && (double)bound(m) + errq >= best * QS) {
+      const double sc = score_generic(m, K, f, stride, l1, l0, p);
+      const int pop = __popc(m);
+      if (prefer(sc, pop, m, best, bpop, bm)) {
+        best = sc;
+        bpop = pop;
+        bm = m;
+      }
+    }
+    m = (m - vbits) & vbits;
+  } while (m != 0);
+  return bm;
+}
+
 // Loader over rays staged in shared memory: element (k, ch) of thread t at
 // smem[(k * 16 + ch) * stride + t].
 struct SmemRays {
@@ -1189,6 +1287,191 @@ __global__ void __launch_bounds__(ESTEP_CERT_BLOCK, ESTEP_CERT_MIN_BLOCKS)
   }
 }
 
+// Certificate pass for 6 <= K <= 12 views: k_e_step_cert's argument with
+// the mask bounds enumerated instead of unrolled.  The fp32 log factors are
+// rounded to fixed point (2^-20 units), so every bound over the 2^popc(valid)
+// admissible masks is an exact integer sum; the top two bounds come from the
+// views sorted by their log ratio (per-thread table in shared memory).
+// |bound_q / 2^20 - bound64| <= K (E_l + 2^-21) + penalty rounding.
+template <bool RECT>
+__global__ void __launch_bounds__(CERT_BIG_BLOCK, 4) k_e_step_cert_big(EmCtx c, EStepArgs a) {
+  __shared__ int s_dl[ST_MAX_VIEWS][CERT_BIG_BLOCK];
+  if (a.stop && *a.stop) return;  // converged (st_solve_async)
+  constexpr float U = 5.9604645e-08f;  // 2^-24
+  constexpr float QS = 1048576.0f;     // 2^20
+  const int K = c.rig.num_views;
+  const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
+  const float eps = (float)c.p.epsilon_prior;
+  const float hi = (float)dsub(1.0, c.p.epsilon_prior);
+  const float lmax = fmaxf(fabsf(logf(eps)), 1.0f);
+  const float e_l = (8.0f * U) / eps * 1.01f + 4.0f * U * 2.0f * lmax;
+  const bool fits = (float)K * lmax * QS < 1.0e9f;  // integer sums cannot overflow
+  const float beta = (float)c.p.beta;
+  const float ceil32 = (float)variance_ceiling();
+  const float pen = beta * ceil32;
+  const int penq = __float2int_rn(fminf(pen * QS, 1.0e9f));
+  const float eps32 = (RECT ? 1024.0f : 4096.0f) * U;
+  const uint32_t* desc = reinterpret_cast<const uint32_t*>(c.desc);
+  const int su = c.W > 1 ? 1 : 0, sv = c.H > 1 ? c.W : 0;
+  int* dlq = &s_dl[0][threadIdx.x];
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_work;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = base + threadIdx.x;
+    bool fail = false;
+    int64_t i = 0;
+    if (t < n_work) {
+      i = a.list ? (int64_t)a.list[t] : t;
+      if (!(a.status && a.status[i] == ST_STATUS_LOW_TEXTURE)) {  // solver.py:476-478
+        const int64_t pix = a.pix ? a.pix[i] : i;
+        const double u = (double)(pix % c.W), v = (double)(pix / c.W);
+        const double d = a.d[i];
+        int idx[ST_MAX_VIEWS];
+        float fu[ST_MAX_VIEWS], fv[ST_MAX_VIEWS];
+        uint32_t vb = 0;
+        int baseq = 0;
+        float lsum = 0.0f;
+#pragma unroll
+        for (int k = 0; k < ST_MAX_VIEWS; ++k) {
+          idx[k] = 0;
+          fu[k] = 0.0f;
+          fv[k] = 0.0f;
+          if (k >= K) continue;
+          const WarpOut w = warp_ctx(c, k, u, v, d);
+          float q = 0.5f;  // invalid rays (solver.py:206-227)
+          if (in_margin(c.rig, k, w)) {
+            const Taps tp = taps_ctx(c, w);
+            idx[k] = tp.iv * c.W + tp.iu;
+            fu[k] = (float)tp.fu;
+            if (!RECT) fv[k] = (float)tp.fv;
+            const float* pl = c.priors + (size_t)k * c.HW + idx[k];
+            const float p0 = __ldg(pl), p1 = __ldg(pl + tp.su);
+            q = fmaf(fu[k], __fsub_rn(p1, p0), p0);
+            if (!RECT && tp.fv != 0.0) {
+              const float p2 = __ldg(pl + tp.sv), p3 = __ldg(pl + tp.sv + tp.su);
+              const float bot = fmaf(fu[k], __fsub_rn(p3, p2), p2);
+              q = fmaf(fv[k], bot - q, q);
+            }
+            vb |= 1u << k;
+          }
+          const float qc = fminf(fmaxf(q, eps), hi);
+          const float l1 = logf(qc), l0 = logf(1.0f - qc);
+          const int q1 = __float2int_rn(l1 * QS), q0 = __float2int_rn(l0 * QS);
+          dlq[k * CERT_BIG_BLOCK] = q1 - q0;
+          baseq += q0;
+          lsum += fabsf(l1) + fabsf(l0);
+        }
+        uint32_t m1 = 0;
+        int b1 = 0, b2 = 0;
+        if (!fits) {
+          fail = true;
+        } else if (vb) {
+          // Exact top two of bound(m) = base + sum_{k in m} dl_k - penq [pop(m) <
+          // min] over the submasks of vb: for each size p the best mask takes
+          // the p largest dl (views sorted descending), the runner-up of that
+          // size swaps its weakest member for the strongest outsider.
+          int dv[ST_MAX_VIEWS], kv[ST_MAX_VIEWS];
+#pragma unroll
+          for (int k = 0; k < ST_MAX_VIEWS; ++k) {
+            const bool in = k < K && ((vb >> k) & 1);
+            dv[k] = in ? dlq[k * CERT_BIG_BLOCK] : INT_MIN / 4;
+            kv[k] = k;
+          }
+#pragma unroll
+          for (int r = 0; r < ST_MAX_VIEWS - 1; ++r)
+#pragma unroll
+            for (int j = 0; j < ST_MAX_VIEWS - 1 - r; ++j)
+              if (dv[j] < dv[j + 1]) {
+                const int td = dv[j], tk = kv[j];
+                dv[j] = dv[j + 1];
+                kv[j] = kv[j + 1];
+                dv[j + 1] = td;
+                kv[j + 1] = tk;
+              }
+          const int nv = __popc(vb);
+          int vp[ST_MAX_VIEWS + 1];
+          int pre = 0;
+          vp[0] = baseq - (0 < c.p.min_static_rays ? penq : 0);
+#pragma unroll
+          for (int q = 1; q <= ST_MAX_VIEWS; ++q) {
+            pre += q <= nv ? dv[q - 1] : 0;
+            vp[q] = q <= nv ? baseq + pre - (q < c.p.min_static_rays ? penq : 0) : INT_MIN;
+          }
+          int ps = 0;
+#pragma unroll
+          for (int q = 1; q <= ST_MAX_VIEWS; ++q)
+            if (vp[q] > vp[ps]) ps = q;
+          b1 = vp[ps];
+          b2 = INT_MIN;
+#pragma unroll
+          for (int q = 0; q <= ST_MAX_VIEWS; ++q)
+            if (q != ps) b2 = max(b2, vp[q]);
+#pragma unroll
+          for (int q = 1; q < ST_MAX_VIEWS; ++q)
+            if (q == ps && q < nv) b2 = max(b2, b1 - dv[q - 1] + dv[q]);
+          m1 = 0;
+#pragma unroll
+          for (int q = 0; q < ST_MAX_VIEWS; ++q)
+            if (q < ps) m1 |= 1u << kv[q];
+          // quantised bounds vs the fp64 ones: K (E_l + 2^-21) + 1 unit for
+          // the penalty, doubled; in 2^-20 units
+          const float errq = 2.0f * (K * (e_l * QS + 0.5f) + 1.0f) + (2.0f * K + 8.0f) * U * lsum * QS;
+          const float gap = (float)(b1 - b2);  // exact integer difference (both >= -2^30)
+          if (__popc(m1) < c.p.min_static_rays) {
+            fail = !(gap > 2.0f * errq);
+          } else {
+            const int k0 = __ffs(vb) - 1;
+            float qs = 0.0f, ac = 0.0f, s2u = 0.0f;
+#pragma unroll 1
+            for (int w = 0; w < 4; ++w) {
+              float ref[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+              for (int k = 0; k < ST_MAX_VIEWS; ++k)
+                if (k == k0)
+                  desc_word32<RECT>(desc + (size_t)k * c.HW * 4, idx[k], su, sv, fu[k], fv[k], w,
+                                    ref);
+              float b1s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+              for (int k = 0; k < ST_MAX_VIEWS; ++k) {
+                if (!((m1 >> k) & 1)) continue;
+                float x[4];
+                desc_word32<RECT>(desc + (size_t)k * c.HW * 4, idx[k], su, sv, fu[k], fv[k], w, x);
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                  const float gdev = x[jj] - ref[jj];
+                  b1s[jj] += gdev;
+                  qs = fmaf(gdev, gdev, qs);
+                  s2u = fmaf(x[jj], x[jj], s2u);
+                }
+              }
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) ac = fmaf(b1s[jj], b1s[jj], ac);
+            }
+            const float n = (float)__popc(m1);
+            const float rn = 1.0f / n;
+            const float var = fmaxf((qs - ac * rn) * rn, 0.0f);
+            // estep_small's D generalised to n <= 12 rays (16 n samples)
+            const float D = 2.0f * (fabsf(beta) * ((4.0f * n + 44.0f) * U * qs +
+                                                   2.0f * U * fmaxf(ceil32, qs) +
+                                                   7.1054274e-15f * s2u + 2.0f * U * ceil32 +
+                                                   2.0f * eps32 * sqrtf(16.0f * n * qs) +
+                                                   16.0f * n * eps32 * eps32));
+            fail = !(gap / QS - beta * var - D > 2.0f * errq / QS);
+          }
+        }
+        if (!fail) {
+          const int64_t o = a.scatter ? pix : i;
+          a.static_out[o] = m1;
+          a.valid_out[o] = vb;
+        }
+      }
+    }
+    list_append(fail, (int32_t)i, a.flist, a.flist_count);
+  }
+}
+
+template __global__ void k_e_step_cert_big<false>(EmCtx, EStepArgs);
+template __global__ void k_e_step_cert_big<true>(EmCtx, EStepArgs);
+
 template __global__ void k_e_step_cert<2, false>(EmCtx, EStepArgs);
 template __global__ void k_e_step_cert<3, false>(EmCtx, EStepArgs);
 template __global__ void k_e_step_cert<4, false>(EmCtx, EStepArgs);
@@ -1232,7 +1515,8 @@ __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a)
     }
     clamp_logs(q, c.p.epsilon_prior, a.eps_logs, l1[k], l0[k]);
   }
-  const uint32_t m = estep_generic(K, f, stride, l1, l0, vb, c.p);
+  const uint32_t m = a.exhaustive ? estep_generic(K, f, stride, l1, l0, vb, c.p)
+                                  : estep_bnb(K, f, stride, l1, l0, vb, c.p);
   const int64_t o = a.scatter ? pix : i;
   a.static_out[o] = m;
   a.valid_out[o] = vb;

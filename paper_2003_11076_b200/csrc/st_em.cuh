@@ -20,6 +20,7 @@
 #define ESTEP_BLOCK 64
 #define ESTEP_TAPS_BLOCK 128
 #define ESTEP_CERT_BLOCK 128
+#define CERT_BIG_BLOCK 128
 #ifndef ESTEP_CERT_MIN_BLOCKS
 #define ESTEP_CERT_MIN_BLOCKS 6  // <= 80 registers
 #endif
@@ -114,6 +115,8 @@ __global__ void k_e_step_taps(EmCtx c, EStepArgs a);
 __global__ void k_e_step_at(EmCtx c, EStepArgs a);
 template <int KT, bool RECT>
 __global__ void k_e_step_cert(EmCtx c, EStepArgs a);
+template <bool RECT>
+__global__ void k_e_step_cert_big(EmCtx c, EStepArgs a);
 __global__ void k_initial_masks(EmCtx c, const int64_t* pix, int64_t n, uint32_t* static_out,
                                 uint32_t* valid_out);
 __global__ void k_gather_rays(EmCtx c, const int64_t* pix, const double* d, int64_t n,

@@ -42,6 +42,7 @@ namespace st {
 struct TriDev {
   const double *pts, *disp, *planes, *transform, *equations;
   const double* nb_eq;  // (n_tri, 3, 4): the neighbours' lifted facet equations (0 for none)
+  double cen0, cen1;    // points.mean(axis=0) (numpy, host): the off-hull nudge target
   const int32_t *simp, *nb;
   int n_pts, n_tri;
   double ps, psh, lo0, lo1, hi0, hi1;
@@ -55,6 +56,8 @@ struct MuWs {
   int32_t *chunks, *runs;  // worklists of chunk starts / run starts
   unsigned* counts;        // [0] chunks, [1] runs
   int chunk;  // chunk length for the speculative walks (MU_CHUNK, env ST_MU_CHUNK)
+  unsigned* miss_bits;  // pixels the raster walk left outside the triangulation
+  int32_t* miss_list;   // ... in pixel order (k_mu_nudge)
 };
 
 // prior.py:296: pl[:, 0] * u + pl[:, 1] * v + pl[:, 2], left to right.
@@ -225,6 +228,19 @@ struct TriCache {
 // _find_simplex + _find_simplex_directed for one query; `start` in/out.
 // The brute-force fallback (lowest-index including simplex) is the claim
 // pass's tmin.
+// scipy _find_simplex_bruteforce for a point that is not a pixel centre
+// (the nudged off-hull queries): the lowest-index simplex with a valid
+// transform whose barycentric test passes.
+__device__ int brute_force_simplex(const TriDev& d, double x0, double x1) {
+  for (int t = 0; t < d.n_tri; ++t) {
+    const double* T = d.transform + 6 * t;
+    if (T[0] == T[0] && bary_inside(T, x0, x1)) return t;
+  }
+  return -1;
+}
+
+// p >= 0: pixel centre p (its claims give the brute-force answer);
+// p < 0: any point (brute force by scanning the simplices).
 __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0, double x1,
                             int& start, TriCache& tc) {
   const double eps = QH_EPS;
@@ -242,9 +258,6 @@ __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0
   bool changed = true;
   while (changed) {
     if (best > 0.0) break;
-#ifdef MU_DIAG
-    atomicAdd(w.counts + 7, 1u);  // paraboloid sweeps
-#endif
     changed = false;
     // the three neighbours' distances, fetched in parallel; used as long as
     // s has not moved inside this sweep (scipy reads the neighbours of the
@@ -325,11 +338,12 @@ __device__ int find_simplex(const TriDev& d, const MuWs& w, int64_t p, double x0
       start = s;
       return s;
     }
-    s = w.cnt[p] ? (int)w.tmin[p] : -1;  // brute force
+    s = p < 0 ? brute_force_simplex(d, x0, x1) : w.cnt[p] ? (int)w.tmin[p] : -1;  // brute force
     start = s;
     return s;
   }
-  s = w.cnt[p] ? (int)w.tmin[p] : -1;  // walk did not converge: brute force
+  // walk did not converge: brute force
+  s = p < 0 ? brute_force_simplex(d, x0, x1) : w.cnt[p] ? (int)w.tmin[p] : -1;
   start = s;
   return s;
 }
@@ -370,6 +384,7 @@ __global__ void k_mu_init(int64_t npx, MuWs w) {
     w.vmin[p] = ~0ull;
     w.vmax[p] = 0ull;
     w.chosen[p] = 0xff;
+    if ((p & 31) == 0) w.miss_bits[p >> 5] = 0u;
   }
   if (blockIdx.x == 0 && threadIdx.x < 8) w.counts[threadIdx.x] = 0u;
 }
@@ -418,9 +433,6 @@ __global__ void __launch_bounds__(128, WALK_MIN_BLOCKS)
     } while (q < npx && ambiguous(w, q) && !chunk_start(w, q));
     end = q;
     ends_run = q >= npx || !ambiguous(w, q);
-#ifdef MU_DIAG
-    atomicMax(w.counts + 5, (unsigned)(q - p));                    // longest chunk
-#endif
     if (agnostic && ends_run) {
       w.len[p] = (int32_t)(q - p);
       w.end0[p] = w.end1[p] = -1;  // never read: the run ends here
@@ -428,9 +440,6 @@ __global__ void __launch_bounds__(128, WALK_MIN_BLOCKS)
     }
   }
   if (nopt == 1) w.chosen[p] = 0;  // a run start: its incoming start is known
-#ifdef MU_DIAG
-  const long long clk0 = clock64();
-#endif
   // the chunk's extent is known from the scan: no per-pixel reload in the walk
   int st0 = opts[0], st1 = nopt > 1 ? opts[1] : 0;
   TriCache tc0, tc1;
@@ -441,10 +450,6 @@ __global__ void __launch_bounds__(128, WALK_MIN_BLOCKS)
   }
   const int64_t q = end;
   w.len[p] = (int32_t)(q - p);
-#ifdef MU_DIAG
-  atomicMax(w.counts + 6, (unsigned)min(clock64() - clk0, 0xffffffffll));  // slowest walk
-  atomicAdd(w.counts + 3, (unsigned)((clock64() - clk0) >> 10));            // total kcycles
-#endif
   w.end0[p] = st0;
   w.end1[p] = nopt > 1 ? st1 : st0;
   // Both speculative walks ended in the same simplex (the usual, "sticky"
@@ -521,21 +526,91 @@ __global__ void k_mu_eval(TriDev d, int W, int64_t npx, MuWs w, double clip_dmax
     const double* pl = d.planes + 3 * s;
     m = dadd(dadd(dmul(pl[0], u), dmul(pl[1], v)), pl[2]);
   } else {
-    // prior.py:298-301: nearest vertex (only reachable off the hull)
-    double best = INFINITY;
-    int bi = 0;
-    for (int i = 0; i < d.n_pts; ++i) {
-      const double dx = d.pts[2 * i] - u, dy = d.pts[2 * i + 1] - v;
-      const double d2 = dx * dx + dy * dy;
-      if (d2 < best) {
-        best = d2;
-        bi = i;
-      }
-    }
-    m = d.disp[bi];
+    // off the hull after the raster walk: k_mu_nudge (prior.py:287-301)
+    atomicOr(w.miss_bits + (p >> 5), 1u << (p & 31));
+    w.counts[6] = 1u;  // (any miss: k_mu_nudge has work)
+    return;
   }
   if (clip_dmax > 0.0) m = fmin(fmax(m, 1e-6), clip_dmax);
   mu[p] = m;
+}
+
+// prior.py:287-301 for the pixels the raster walk left outside the
+// triangulation (s < 0): a second find_simplex batch on the points nudged
+// 1e-9 toward the vertex centroid -- in pixel order, the walk start carried
+// from one query to the next and starting at simplex 0, like scipy's -- and
+// the nearest vertex for what is still outside.  The plane is evaluated at
+// the original pixel centre.  One block: the bitmap is compacted in pixel
+// order (block scan), then thread 0 walks the list.
+#define NUDGE_CAP 16384
+__global__ void __launch_bounds__(1024) k_mu_nudge(TriDev d, int W, int64_t npx, MuWs w,
+                                                   double clip_dmax, double* __restrict__ mu) {
+  __shared__ unsigned s_cnt[1024];
+  if (w.counts[6] == 0u) return;  // the common case: every pixel found its simplex
+  const int64_t words = (npx + 31) / 32;
+  const int64_t per = (words + blockDim.x - 1) / blockDim.x;
+  const int64_t w0 = (int64_t)threadIdx.x * per, w1 = min(w0 + per, words);
+  unsigned c = 0;
+  for (int64_t i = w0; i < w1; ++i) c += __popc(w.miss_bits[i]);
+  s_cnt[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan (1024 entries)
+    unsigned acc = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const unsigned x = s_cnt[i];
+      s_cnt[i] = acc;
+      acc += x;
+    }
+    w.counts[7] = acc;
+  }
+  __syncthreads();
+  const unsigned total = w.counts[7];
+  if (total == 0) return;
+  if (total <= NUDGE_CAP) {
+    unsigned o = s_cnt[threadIdx.x];
+    for (int64_t i = w0; i < w1; ++i)
+      for (unsigned b = w.miss_bits[i]; b; b &= b - 1) w.miss_list[o++] = (int32_t)(i * 32 + __ffs(b) - 1);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int start = 0;
+  TriCache tc;
+  int64_t wi = 0;
+  unsigned bits = 0;
+  for (unsigned j = 0; j < total; ++j) {
+    int64_t p;
+    if (total <= NUDGE_CAP) {
+      p = w.miss_list[j];
+    } else {  // (never seen in practice) scan the bitmap in order
+      while (!bits) bits = w.miss_bits[wi++];
+      p = (wi - 1) * 32 + __ffs(bits) - 1;
+      bits &= bits - 1;
+    }
+    const double u = (double)(p % W), v = (double)(p / W);
+    // q + 1e-9 * (centroid - q), numpy's elementwise order
+    const double x0 = dadd(u, dmul(1e-9, dsub(d.cen0, u)));
+    const double x1 = dadd(v, dmul(1e-9, dsub(d.cen1, v)));
+    const int s = find_simplex(d, w, -1, x0, x1, start, tc);
+    double m;
+    if (s >= 0) {
+      m = plane_at(d, s, u, v);
+    } else {
+      // cKDTree nearest vertex of the original point (first minimum)
+      double best = INFINITY;
+      int bi = 0;
+      for (int i = 0; i < d.n_pts; ++i) {
+        const double dx = d.pts[2 * i] - u, dy = d.pts[2 * i + 1] - v;
+        const double d2 = dx * dx + dy * dy;
+        if (d2 < best) {
+          best = d2;
+          bi = i;
+        }
+      }
+      m = d.disp[bi];
+    }
+    if (clip_dmax > 0.0) m = fmin(fmax(m, 1e-6), clip_dmax);
+    mu[p] = m;
+  }
 }
 
 }  // namespace st
@@ -546,7 +621,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct MuLayout {
   size_t off[16];
-  size_t bbox, area, start, nb_eq, cub, cub_bytes;
+  size_t bbox, area, start, nb_eq, miss_bits, miss_list, cub, cub_bytes;
   size_t total;
 };
 
@@ -564,6 +639,8 @@ MuLayout mu_layout(int W, int H, int n_tri) {
   L.area = o;  o += align_up(sizeof(unsigned long long) * nt);
   L.start = o; o += align_up(sizeof(unsigned long long) * nt);
   L.nb_eq = o; o += align_up(sizeof(double) * 12 * nt);
+  L.miss_bits = o; o += align_up(sizeof(unsigned) * ((npx + 31) / 32));
+  L.miss_list = o; o += align_up(sizeof(int32_t) * NUDGE_CAP);
   L.cub_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, L.cub_bytes, (unsigned long long*)nullptr,
                                 (unsigned long long*)nullptr, (int)nt);
@@ -772,6 +849,8 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   w.counts = (unsigned*)(ws + L.off[13]);
   w.vmin = (unsigned long long*)(ws + L.off[14]);
   w.vmax = (unsigned long long*)(ws + L.off[15]);
+  w.miss_bits = (unsigned*)(ws + L.miss_bits);
+  w.miss_list = (int32_t*)(ws + L.miss_list);
   static const int chunk_env = [] {
     const char* e = getenv("ST_MU_CHUNK");
     const int v = e ? atoi(e) : 0;
@@ -795,6 +874,8 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   d.hi0 = tri->max_bound[0];
   d.hi1 = tri->max_bound[1];
   d.nb_eq = (const double*)(ws + L.nb_eq);
+  d.cen0 = tri->centroid[0];
+  d.cen1 = tri->centroid[1];
   const int64_t npx = (int64_t)W * H;
   static const bool prof_on = getenv("ST_MU_PROFILE") != nullptr;  // diagnostics
   cudaEvent_t pev[8];
@@ -841,6 +922,8 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   prof();
   st::k_mu_eval<<<blocks, 256, 0, s>>>(d, W, npx, w, clip_dmax, mu_out);
   ST_LAUNCH_CHECK("k_mu_eval");
+  st::k_mu_nudge<<<1, 1024, 0, s>>>(d, W, npx, w, clip_dmax, mu_out);
+  ST_LAUNCH_CHECK("k_mu_nudge");
   prof();
   if (prof_on && npev > 1) {
     cudaEventSynchronize(pev[npev - 1]);
@@ -852,10 +935,7 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
     }
     unsigned cnts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpy(cnts, w.counts, sizeof(cnts), cudaMemcpyDeviceToHost);
-    fprintf(stderr,
-            "  chunks %u - %u walk-kcycles %u - %u longest %u slowest-walk-cycles %u "
-            "paraboloid-sweeps %u\n",
-            cnts[0], cnts[2], cnts[3], cnts[4], cnts[5], cnts[6], cnts[7]);
+    fprintf(stderr, "  chunks %u off-hull %u\n", cnts[0], cnts[7]);
     for (int i = 0; i < npev; ++i) cudaEventDestroy(pev[i]);
   }
   return ST_OK;

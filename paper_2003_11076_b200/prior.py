@@ -178,9 +178,11 @@ class TriDevice:
         s.n_pts, s.n_tri = self.n_pts, self.n_tri
         s.paraboloid_scale = float(dl.paraboloid_scale)
         s.paraboloid_shift = float(dl.paraboloid_shift)
+        cen = np.asarray(points, dtype=np.float64).mean(axis=0)  # prior.py:290, numpy's sum
         for k in range(2):
             s.min_bound[k] = float(dl.min_bound[k])
             s.max_bound[k] = float(dl.max_bound[k])
+            s.centroid[k] = float(cen[k])
         self.st = s
         if self.device_tables:
             N.invoke("st_tri_tables", s, self.planes, self.transform, self.flags)

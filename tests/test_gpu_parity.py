@@ -324,3 +324,25 @@ def test_refocus_pixel_matches_dense(st):
         rgb, n, p = st.refocus_pixel(frame, rig, u, v, float(dmap.values[v, u]),
                                      int(seg.static_bits[v, u]))
         assert n == nr[v, u] and p == prov[v, u] and np.array_equal(rgb, img[v, u])
+
+
+@pytest.mark.parametrize("name", ["occ128_k9"])
+def test_k9_certificate_and_bnb_equal_exhaustive(st, monkeypatch, name):
+    """K = 9: the enumerated-bound certificate (k_e_step_cert_big) and the
+    branch-and-bound fallback decide exactly what scoring all 512 masks in
+    fp64 decides (ST_ESTEP_EXHAUSTIVE), over 5 forced iterations, with and
+    without dynamic_only."""
+    g = load(name)
+    sp, pp = _params(st, g)
+    frame = _frame(st, g)
+    for dyn in (False, True):
+        monkeypatch.delenv("ST_ESTEP_EXHAUSTIVE", raising=False)
+        a = st.reconstruct(frame, _Rig(g), _Tri(g), params=sp, prior_params=pp,
+                           dynamic_only=dyn, forced_iters=5)
+        monkeypatch.setenv("ST_ESTEP_EXHAUSTIVE", "1")
+        b = st.reconstruct(frame, _Rig(g), _Tri(g), params=sp, prior_params=pp,
+                           dynamic_only=dyn, forced_iters=5)
+        assert np.array_equal(a.segmentation.static_bits, b.segmentation.static_bits)
+        assert np.array_equal(a.segmentation.valid_bits, b.segmentation.valid_bits)
+        assert np.array_equal(a.disparity.values, b.disparity.values)
+        assert list(a.stats.mean_energy) == list(b.stats.mean_energy)

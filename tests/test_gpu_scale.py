@@ -21,6 +21,11 @@ def st():
     return pkg
 
 
+def bench_inputs(cfg):
+    import bench
+    return bench.load_inputs(cfg)
+
+
 def _inputs(cfg):
     import bench
     frame, rig, tri, exact = bench.load_inputs(cfg)
@@ -132,3 +137,19 @@ def test_async_solve_equals_sync(st, forced):
               "changed_fraction", "candidates_total", "energy_evals", "msteps", "esteps",
               "prev_evals", "active_pixels"):
         assert getattr(a.stats, f) == getattr(b.stats, f), f
+
+
+@pytest.mark.slow
+def test_c4_mu_raster_bit_exact_incl_off_hull_pixels(st):
+    """C4 (3840x2160, 296k support points): the raster walk leaves a few
+    interior pixels near the top edge outside the triangulation, exactly as
+    scipy's find_simplex does; the reference then re-queries them nudged
+    1e-9 toward the centroid (prior.py:287-293).  The device raster
+    (k_mu_nudge) must reproduce the reference's surface bit for bit."""
+    import oracle
+    frame, rig, tri, exact = bench_inputs("C4")
+    h, w = frame.shape
+    got = st.TriangulationPrior(tri.points, tri.disparities, tri.triangles, tri.planes,
+                                tri.num_anchors).disparity_map(w, h)
+    want = oracle.mu_raster(tri.points, tri.disparities, tri.triangles, tri.planes, w, h)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), int((got != want).sum())
