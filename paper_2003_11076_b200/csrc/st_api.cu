@@ -195,6 +195,12 @@ void launch_e_step(int K, int64_t n, cudaStream_t s, const st::EmCtx& c,
         break;
     }
     sthost::count_launch();
+    if (getenv("ST_ESTEP_STATS")) {  // diagnostics: rows left for the fallback (synchronises)
+      uint32_t nf = 0;
+      cudaMemcpyAsync(&nf, a.flist_count, sizeof(nf), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      fprintf(stderr, "e-step certificate: %u rows to the fallback\n", nf);
+    }
     a.list = a.flist;
     a.list_count = a.flist_count;
     n = std::min<int64_t>(n, K <= 5 ? 148 * ESTEP_MIN_BLOCKS * ESTEP_TAPS_BLOCK
