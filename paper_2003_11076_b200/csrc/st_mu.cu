@@ -572,6 +572,29 @@ __global__ void __launch_bounds__(1024) k_mu_nudge(TriDev d, int W, int64_t npx,
       for (unsigned b = w.miss_bits[i]; b; b &= b - 1) w.miss_list[o++] = (int32_t)(i * 32 + __ffs(b) - 1);
   }
   __syncthreads();
+  // vertex centroid (NaN from the host: integer coordinates, exact sums in
+  // any order, then one division like numpy's mean)
+  __shared__ double s_sum[2][1024];
+  TriDev dd = d;
+  if (!(d.cen0 == d.cen0)) {
+    double a0 = 0.0, a1 = 0.0;
+    for (int i = threadIdx.x; i < d.n_pts; i += blockDim.x) {
+      a0 += d.pts[2 * i];
+      a1 += d.pts[2 * i + 1];
+    }
+    s_sum[0][threadIdx.x] = a0;
+    s_sum[1][threadIdx.x] = a1;
+    __syncthreads();
+    for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+      if ((int)threadIdx.x < h) {
+        s_sum[0][threadIdx.x] += s_sum[0][threadIdx.x + h];
+        s_sum[1][threadIdx.x] += s_sum[1][threadIdx.x + h];
+      }
+      __syncthreads();
+    }
+    dd.cen0 = ddiv(s_sum[0][0], (double)d.n_pts);
+    dd.cen1 = ddiv(s_sum[1][0], (double)d.n_pts);
+  }
   if (threadIdx.x != 0) return;
   int start = 0;
   TriCache tc;
@@ -588,8 +611,8 @@ __global__ void __launch_bounds__(1024) k_mu_nudge(TriDev d, int W, int64_t npx,
     }
     const double u = (double)(p % W), v = (double)(p / W);
     // q + 1e-9 * (centroid - q), numpy's elementwise order
-    const double x0 = dadd(u, dmul(1e-9, dsub(d.cen0, u)));
-    const double x1 = dadd(v, dmul(1e-9, dsub(d.cen1, v)));
+    const double x0 = dadd(u, dmul(1e-9, dsub(dd.cen0, u)));
+    const double x1 = dadd(v, dmul(1e-9, dsub(dd.cen1, v)));
     const int s = find_simplex(d, w, -1, x0, x1, start, tc);
     double m;
     if (s >= 0) {

@@ -178,7 +178,12 @@ class TriDevice:
         s.n_pts, s.n_tri = self.n_pts, self.n_tri
         s.paraboloid_scale = float(dl.paraboloid_scale)
         s.paraboloid_shift = float(dl.paraboloid_shift)
-        cen = np.asarray(points, dtype=np.float64).mean(axis=0)  # prior.py:290, numpy's sum
+        # prior.py:290 `points.mean(axis=0)` (the off-hull nudge target).  With
+        # integer vertex coordinates the column sums are exact in any order, so
+        # k_mu_nudge computes it on the device when it is needed (NaN here);
+        # otherwise numpy's value is shipped.
+        cen = ((np.nan, np.nan) if self.device_tables
+               else np.asarray(points, dtype=np.float64).mean(axis=0))
         for k in range(2):
             s.min_bound[k] = float(dl.min_bound[k])
             s.max_bound[k] = float(dl.max_bound[k])

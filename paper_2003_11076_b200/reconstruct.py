@@ -357,8 +357,8 @@ def _outputs_of(pipe, stats, host):
         stats = stats.resolve(raw_stats)
     return Reconstruction(
         disparity=DisparityMap(values=values, status=status),
-        segmentation=SegmentationState(static_bits=sbits.view(np.uint32),
-                                       valid_bits=vbits.view(np.uint32)),
+        segmentation=SegmentationState._device_result(sbits.view(np.uint32),
+                                                      vbits.view(np.uint32)),
         stats=stats, image=img, provenance=prov, n_rays=nr)
 
 

@@ -53,6 +53,15 @@ class SegmentationState:
         if (self.static_bits & ~self.valid_bits).any():
             raise ValueError("static rays must be a subset of valid rays")
 
+    @classmethod
+    def _device_result(cls, static_bits, valid_bits):
+        """Wrap the E-step's outputs without the subset scan (solver.py:78-81):
+        the kernels only ever set static bits of valid rays."""
+        obj = cls.__new__(cls)
+        obj.static_bits = static_bits
+        obj.valid_bits = valid_bits
+        return obj
+
 
 @dataclass
 class EMStats:
