@@ -22,7 +22,7 @@
 #define ESTEP_CERT_BLOCK 128
 #define CERT_BIG_BLOCK 128
 #ifndef ESTEP_CERT_MIN_BLOCKS
-#define ESTEP_CERT_MIN_BLOCKS 6  // <= 80 registers
+#define ESTEP_CERT_MIN_BLOCKS 8  // <= 64 registers (no spills; measured best)
 #endif
 #ifndef ESTEP_MIN_BLOCKS
 #define ESTEP_MIN_BLOCKS 4  // <= 128 registers

@@ -397,7 +397,7 @@ __global__ void k_mu_lists(int64_t npx, MuWs w) {
 }
 
 #ifndef WALK_MIN_BLOCKS
-#define WALK_MIN_BLOCKS 1
+#define WALK_MIN_BLOCKS 5  // <= 102 registers: no spills, measured best
 #endif
 __global__ void __launch_bounds__(128, WALK_MIN_BLOCKS)
     k_walk_chunks(TriDev d, int W, int64_t npx, MuWs w) {
