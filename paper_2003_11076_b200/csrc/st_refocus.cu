@@ -18,16 +18,26 @@ struct RefocusOut {
 };
 
 // gather_static_colors for one pixel (refocus.py:24-49).
+// rectified: every view has A = I, b = (bx, 0, 0); then warp_ab's roundings
+// reduce to pu = u + d bx, pv = v exactly (as the EM kernels' warp_ctx).
 __device__ __forceinline__ RefocusOut gather_colors(const uint8_t* __restrict__ images,
                                                     const st_rig& rig, int W, int H, double u,
-                                                    double v, double d, uint32_t bits) {
+                                                    double v, double d, uint32_t bits,
+                                                    bool rectified = false) {
   RefocusOut r;
   r.tot[0] = r.tot[1] = r.tot[2] = 0.0;
   r.count = 0;
   const size_t plane = (size_t)W * H * 3;
   for (int k = 0; k < rig.num_views; ++k) {
     if (!((bits >> k) & 1u)) continue;
-    const WarpOut w = warp_to(rig, k, u, v, d);
+    WarpOut w;
+    if (rectified) {
+      w.pu = dadd(u, dmul(d, rig.warp_b[k][0]));
+      w.pv = v;
+      w.front = true;
+    } else {
+      w = warp_to(rig, k, u, v, d);
+    }
     // refocus.py:42: margin 0 against the frame size
     if (!(w.front && w.pu >= 0.0 && w.pu <= (double)W - 1.0 && w.pv >= 0.0 &&
           w.pv <= (double)H - 1.0))
@@ -56,11 +66,20 @@ __device__ __forceinline__ uint8_t round_u8(double x) {
   return (uint8_t)fmin(fmax(rint(x), 0.0), 255.0);
 }
 
+// total / count correctly rounded for a small positive integer count: the
+// 3-FMA Markstein step with r = RN(1/n) (st_common.cuh div_small, checked
+// against __ddiv_rn by st_selftest).
+__device__ __forceinline__ double div_count(double x, int n) {
+  const double nn = (double)n;
+  return div_small(x, nn, __drcp_rn(nn));
+}
+
 __global__ void k_refocus(const uint8_t* __restrict__ images, st_rig rig, int W, int H,
                           const float* __restrict__ values, const uint8_t* __restrict__ status,
                           const uint32_t* __restrict__ static_bits, int min_static_rays,
                           const uint8_t* __restrict__ copy_mask, uint8_t* __restrict__ out,
-                          uint8_t* __restrict__ prov, uint8_t* __restrict__ n_rays) {
+                          uint8_t* __restrict__ prov, uint8_t* __restrict__ n_rays,
+                          int rectified) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= (int64_t)W * H) return;
   const uint8_t* ref = images + (size_t)rig.ref_index * W * H * 3 + (size_t)p * 3;
@@ -71,13 +90,12 @@ __global__ void k_refocus(const uint8_t* __restrict__ images, st_rig rig, int W,
   if (!copied && status[p] == ST_STATUS_VALID) {
     const double d = (double)values[p];  // refocus.py:133
     const RefocusOut r = gather_colors(images, rig, W, H, (double)(p % W), (double)(p / W), d,
-                                       static_bits[p]);
+                                       static_bits[p], rectified != 0);
     nr = (uint8_t)min(r.count, 255);
     if (r.count >= min_static_rays) {
-      const double n = (double)r.count;
-      c0 = round_u8(ddiv(r.tot[0], n));
-      c1 = round_u8(ddiv(r.tot[1], n));
-      c2 = round_u8(ddiv(r.tot[2], n));
+      c0 = round_u8(div_count(r.tot[0], r.count));
+      c1 = round_u8(div_count(r.tot[1], r.count));
+      c2 = round_u8(div_count(r.tot[2], r.count));
       pv = ST_PROV_REFOCUSED;
     }
   }
@@ -224,8 +242,18 @@ extern "C" int st_synthesize(const uint8_t* images, const st_rig* rig, const flo
   const int64_t npx = (int64_t)W * H;
   const unsigned blocks = (unsigned)((npx + 127) / 128);
   uint8_t* stage = median_radius > 0 ? scratch : image_out;
+  int rectified = 1;
+  for (int k = 0; k < rig->num_views; ++k) {
+    const double* a = rig->warp_a[k];
+    const double* b = rig->warp_b[k];
+    if (!(a[0] == 1.0 && a[1] == 0.0 && a[2] == 0.0 && a[3] == 0.0 && a[4] == 1.0 &&
+          a[5] == 0.0 && a[6] == 0.0 && a[7] == 0.0 && a[8] == 1.0 && b[1] == 0.0 &&
+          b[2] == 0.0 && fabs(b[0]) < 1e300))
+      rectified = 0;
+  }
   st::k_refocus<<<blocks, 128, 0, s>>>(images, *rig, W, H, values, status, static_bits,
-                                       min_static_rays, copy_mask, stage, prov_out, n_rays_out);
+                                       min_static_rays, copy_mask, stage, prov_out, n_rays_out,
+                                       rectified);
   ST_LAUNCH_CHECK("k_refocus");
   if (median_radius > 0) {
     st::k_median_small<<<(unsigned)((npx + 255) / 256), 256, 0, s>>>(
