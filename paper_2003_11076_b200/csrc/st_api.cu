@@ -175,12 +175,12 @@ void launch_cert(unsigned blocks, cudaStream_t s, const st::EmCtx& c, const st::
 // (k_e_step_cert) decides most rows without any fp64 score; the rows it
 // cannot certify go through the screened kernel, one grid-stride wave.
 void launch_e_step(int K, int64_t n, cudaStream_t s, const st::EmCtx& c,
-                   const st::EStepArgs& args) {
+                   const st::EStepArgs& args, bool count_cleared = false) {
   const bool exhaustive = getenv("ST_ESTEP_EXHAUSTIVE") != nullptr;  // cross-check
   st::EStepArgs a = args;
   a.exhaustive = exhaustive ? 1 : 0;
   if (a.flist && !exhaustive) {
-    cudaMemsetAsync(a.flist_count, 0, sizeof(uint32_t), s);
+    if (!count_cleared) cudaMemsetAsync(a.flist_count, 0, sizeof(uint32_t), s);
     const unsigned bc = blocks_for(n, ESTEP_CERT_BLOCK);
     switch (K) {
       case 2: launch_cert<2>(bc, s, c, a); break;
@@ -749,6 +749,8 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
 
   ST_CUDA_CHECK(cudaMemsetAsync(stats_dev, 0, sizeof(st_stats), s));
   ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t) + sizeof(int), s));
+  // E-step fallback count (byte 48) and the stats kernel's block counter (52)
+  ST_CUDA_CHECK(cudaMemsetAsync(counts + 12, 0, 4 * sizeof(uint32_t), s));
   st::k_stats_init<<<1, 32, 0, s>>>(stats_dev, npx);
   ST_LAUNCH_CHECK("k_stats_init");
   double* eps_logs = (double*)(counts + 4);
@@ -807,17 +809,26 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     e.flist = (int32_t*)(ws + L.flist);
     e.flist_count = (uint32_t*)(eps_logs + 4);
     e.stop = stop;
-    launch_e_step(rig->num_views, it > 1 ? std::min<int64_t>(npx, 148 * 8 * 128) : npx, s, c, e);
+    launch_e_step(rig->num_views, it > 1 ? std::min<int64_t>(npx, 148 * 8 * 128) : npx, s, c, e,
+                  true);
     ST_LAUNCH_CHECK("k_e_step_at");
+    // statistics, their fixed-order reduction and the control in one launch
+    // (the last block folds the partials; it also clears the fallback count)
+    st::StatsTail tail = {};
+    tail.on = 1;
+    tail.it = it;
+    tail.done = counts + 13;
+    tail.reduced = reduced;
+    tail.counts = counts;
+    tail.n_act = npx;
+    tail.forced_iters = p->forced_iters;
+    tail.stats = stats_dev;
+    tail.stop_rw = stop;
+    tail.flist_count = e.flist_count;
     st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(npx, it > 1, e_act, pe_act, chg, work,
                                                 (it > 1 ? wave : nblk) * (EM_BLOCK / 32),
-                                                parts, stop);
+                                                parts, stop, tail);
     ST_LAUNCH_CHECK("k_em_stats");
-    st::k_reduce_partials<<<1, 256, 0, s>>>(parts, sblk, reduced + it, stop);
-    ST_LAUNCH_CHECK("k_reduce_partials");
-    st::k_solve_control<<<1, 32, 0, s>>>(it, reduced, counts, npx, p->forced_iters, stats_dev,
-                                         stop);
-    ST_LAUNCH_CHECK("k_solve_control");
   }
   st::k_pack_outputs<<<blocks_for(npx, 256), 256, 0, s>>>(f->mu, npx, nullptr, npx, d_act,
                                                           st_act, values, status, 1);

@@ -493,10 +493,16 @@ __global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n,
 // Per-iteration statistics over every active slot, as fixed-order per-warp
 // partials (solver.py:463-475: mean of finite E, mean of finite previous
 // energies, changed count).
+__device__ void reduce_partials_block(const Partial* __restrict__ parts, int nparts,
+                                      Partial* __restrict__ out);
+__device__ void solve_control(int it, const Partial* __restrict__ reduced,
+                              uint32_t* __restrict__ counts, int64_t n_act, int forced_iters,
+                              st_stats* __restrict__ stats, int* __restrict__ stop);
+
 __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ e,
                            const double* __restrict__ pe, const uint8_t* __restrict__ chg,
                            const Partial* __restrict__ work, int n_work_parts,
-                           Partial* __restrict__ parts, const int* stop) {
+                           Partial* __restrict__ parts, const int* stop, StatsTail tail) {
   if (stop && *stop) return;
   // fixed grid (STATS_GRID), fixed per-thread order: deterministic sums
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -566,6 +572,26 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ 
       B.n_samples += sp[j].n_samples;
     }
     parts[blockIdx.x] = B;
+  }
+  if (!tail.on) return;
+  // the last block to finish folds every block's partial (fixed order) and
+  // runs the iteration's control: no separate reduce / control launches
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(tail.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  reduce_partials_block(parts, gridDim.x, tail.reduced + tail.it);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    *tail.done = 0u;
+    solve_control(tail.it, tail.reduced, tail.counts, tail.n_act, tail.forced_iters, tail.stats,
+                  tail.stop_rw);
+    if (tail.flist_count) *tail.flist_count = 0u;
   }
 }
 
@@ -1692,10 +1718,10 @@ __global__ void k_fill_mu(const double* __restrict__ mu, int64_t npx, float* __r
 }
 
 // Fixed-order sum of the per-block partials into slot `it` of the stats.
-__global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
-                                  Partial* __restrict__ out, const int* stop) {
+// Fixed-order sum of the per-block partials by one 256-thread block.
+__device__ void reduce_partials_block(const Partial* __restrict__ parts, int nparts,
+                                      Partial* __restrict__ out) {
   __shared__ double sd[2][256];
-  if (stop && *stop) return;
   __shared__ long long si[7][256];
   double a = 0.0, b = 0.0;
   long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0;
@@ -1747,6 +1773,12 @@ __global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
   }
 }
 
+__global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
+                                  Partial* __restrict__ out, const int* stop) {
+  if (stop && *stop) return;
+  reduce_partials_block(parts, nparts, out);
+}
+
 // dynamic_only / explicit active-set compaction: count then scatter, in
 // pixel order (the reference's `active` is ascending).
 __global__ void k_flag_active(const float* __restrict__ ref_prior, const uint8_t* __restrict__ mask,
@@ -1773,10 +1805,10 @@ __global__ void k_stats_init(st_stats* stats, int64_t n_act) {
   }
 }
 
-__global__ void k_solve_control(int it, const Partial* __restrict__ reduced,
-                                uint32_t* __restrict__ counts, int64_t n_act, int forced_iters,
-                                st_stats* __restrict__ stats, int* __restrict__ stop) {
-  if (threadIdx.x != 0 || blockIdx.x != 0 || *stop) return;
+// Device-side EM control (solver.py:463-485): one thread.
+__device__ void solve_control(int it, const Partial* __restrict__ reduced,
+                              uint32_t* __restrict__ counts, int64_t n_act, int forced_iters,
+                              st_stats* __restrict__ stats, int* __restrict__ stop) {
   const Partial r = reduced[it];
   stats->iterations_run = it;
   stats->msteps += it > 1 ? (int64_t)counts[0] : n_act;
@@ -1803,6 +1835,13 @@ __global__ void k_solve_control(int it, const Partial* __restrict__ reduced,
   }
   counts[0] = 0;  // next iteration's worklists
   counts[1] = 0;
+}
+
+__global__ void k_solve_control(int it, const Partial* __restrict__ reduced,
+                                uint32_t* __restrict__ counts, int64_t n_act, int forced_iters,
+                                st_stats* __restrict__ stats, int* __restrict__ stop) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || *stop) return;
+  solve_control(it, reduced, counts, n_act, forced_iters, stats, stop);
 }
 
 }  // namespace st

@@ -107,9 +107,23 @@ __global__ void k_m_step(EmCtx c, MStepArgs a);
 __global__ void k_flag_mstep(const int64_t* active, int64_t n, const uint32_t* static_all,
                              const uint32_t* mask_in, const double* e, double* pe, uint8_t* chg,
                              int32_t* list, uint32_t* count, const int* stop = nullptr);
+// st_solve_async: k_em_stats' last block also reduces the partials and runs
+// the iteration's control (k_reduce_partials + k_solve_control fused).
+struct StatsTail {
+  int on;
+  int it;
+  unsigned* done;          // zero-initialised block counter (reset by the last block)
+  Partial* reduced;
+  uint32_t* counts;
+  int64_t n_act;
+  int forced_iters;
+  st_stats* stats;
+  int* stop_rw;
+  uint32_t* flist_count;   // nullable: the E-step fallback count, cleared for the next E-step
+};
 __global__ void k_em_stats(int64_t n, int with_prev, const double* e, const double* pe,
                            const uint8_t* chg, const Partial* work, int n_work_parts,
-                           Partial* parts, const int* stop = nullptr);
+                           Partial* parts, const int* stop = nullptr, StatsTail tail = {});
 template <int KT, bool RECT>
 __global__ void k_e_step_taps(EmCtx c, EStepArgs a);
 __global__ void k_e_step_at(EmCtx c, EStepArgs a);
