@@ -771,8 +771,12 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     const char* e = getenv("ST_WAVE_BLOCKS_PER_SM");
     return e ? atoi(e) : 16;
   }();
-  const int wave = std::min(nblk, 148 * wave_env);
+  const int wave2 = std::min(nblk, 148 * wave_env);
   for (int it = 1; it <= iters; ++it) {
+    // iteration 2 re-solves the pixels whose mask changed at iteration 1
+    // (~20 %); later iterations have far smaller worklists, or none once
+    // converged (the launches then exit at once): a smaller grid
+    const int wave = it <= 2 ? wave2 : std::min(nblk, 148 * 4);
     if (it > 1) {
       st::k_flag_mstep<<<wave, EM_BLOCK, 0, s>>>(nullptr, npx, static_bits, mask_in, e_act,
                                                  pe_act, chg, mlist, counts, stop);
@@ -809,7 +813,8 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     e.flist = (int32_t*)(ws + L.flist);
     e.flist_count = (uint32_t*)(eps_logs + 4);
     e.stop = stop;
-    launch_e_step(rig->num_views, it > 1 ? std::min<int64_t>(npx, 148 * 8 * 128) : npx, s, c, e,
+    launch_e_step(rig->num_views,
+                  it == 1 ? npx : std::min<int64_t>(npx, 148 * (it == 2 ? 8 : 4) * 128), s, c, e,
                   true);
     ST_LAUNCH_CHECK("k_e_step_at");
     // statistics, their fixed-order reduction and the control in one launch
