@@ -300,3 +300,147 @@ def run_reconstruct_sequence(calib_path, frame_dirs, out_dirs, priors_dirs=None,
     finally:
         io.shutdown(wait=True)
     return stats
+
+
+# -- synthetic frame directories and evaluation ---------------------
+
+def _presets():
+    from . import synth
+    return {"two_plane": synth.two_plane_scene, "occluder": synth.occluder_scene,
+            "low_texture": synth.low_texture_scene}
+
+
+def run_synth(out_dir, scene=None, preset=None, seed=None):
+    """pipeline.py:320-358: render a scene file or preset (the renderer port,
+    bit-exact with synth.py:244-309) into a frame directory with ground truth:
+    calib.txt, scene.txt, view_XX.ppm, prior_XX.pgm, gt_mask_XX.pgm,
+    gt_disparity.pgm, disparity_scale.txt, gt_background.ppm."""
+    from dataclasses import replace
+
+    from . import synth
+    if (scene is None) == (preset is None):
+        raise PipelineError("give exactly one of scene or preset")
+    if scene is not None:
+        try:
+            spec = synth.load_scene(scene)
+        except (ValueError, OSError) as exc:
+            raise PipelineError(str(exc))
+    else:
+        presets = _presets()
+        if preset not in presets:
+            raise PipelineError(f"unknown preset {preset!r}; choose from {sorted(presets)}")
+        spec = presets[preset]()
+    if seed is not None:
+        spec = replace(spec, seed=int(seed))
+    try:
+        spec.validate()
+    except ValueError as exc:
+        raise PipelineError(str(exc))
+    frame, gt = synth.render(spec)
+    rig = spec.rig()
+    write_frame_dir(out_dir, frame, rig)
+    synth.save_scene(spec, os.path.join(out_dir, "scene.txt"))
+    for k in range(frame.num_views):
+        pnm.write_pgm(os.path.join(out_dir, view_name("gt_mask", k, "pgm")),
+                      np.asarray(gt.masks[k]).astype(np.uint8) * 255)
+    code = np.clip(np.rint(gt.disparity * DISPARITY_SCALE), 0, 65535).astype(np.uint16)
+    pnm.write_pgm(os.path.join(out_dir, "gt_disparity.pgm"), code)
+    with open(os.path.join(out_dir, "disparity_scale.txt"), "w") as fh:
+        fh.write(f"{int(DISPARITY_SCALE)}\n")
+    pnm.write_ppm(os.path.join(out_dir, "gt_background.ppm"), gt.background)
+    return {"out_dir": out_dir, "num_views": frame.num_views}
+
+
+def _keyvals(path):
+    out = {}
+    with open(path, "r") as fh:
+        for raw in fh:
+            text = raw.split("#", 1)[0].strip()
+            if text and "=" in text:
+                key, _, value = text.partition("=")
+                out[key.strip()] = value.strip()
+    return out
+
+
+def run_evaluate(run_dir, gt_dir, out_path=None):
+    """pipeline.py:361-458: score a run directory against rendered ground
+    truth and write report.txt (key = value).  Disparity metrics over
+    status-valid pixels; refocus RMSE over refocused pixels; per-ray
+    segmentation accuracy of the thresholded input priors (before) and the
+    solved masks (after) against the ground-truth occluder masks, at rays
+    cast with the true disparity (the prior samples through the device
+    bilinear, st_bilinear)."""
+    from .refocus import PROV_COPIED, PROV_FALLBACK, PROV_REFOCUSED
+    from .sampling import bilinear, flatten_channels
+
+    def need(path):
+        if not os.path.exists(path):
+            raise PipelineError(f"missing artifact: {path}")
+        return path
+
+    try:
+        rig = load_calibration(need(os.path.join(gt_dir, "calib.txt")))
+    except CalibrationError as exc:
+        raise PipelineError(f"calibration: {exc}")
+    gt_disp = pnm.read_pnm(need(os.path.join(gt_dir, "gt_disparity.pgm"))).astype(
+        np.float64) / DISPARITY_SCALE
+    gt_bg = pnm.read_pnm(need(os.path.join(gt_dir, "gt_background.ppm")))
+    est = pnm.read_pnm(need(os.path.join(run_dir, "disparity.pgm"))).astype(
+        np.float64) / DISPARITY_SCALE
+    status = pnm.read_pnm(need(os.path.join(run_dir, "status.pgm")))
+    refocused = pnm.read_pnm(need(os.path.join(run_dir, "refocused.ppm")))
+    prov = pnm.read_pnm(need(os.path.join(run_dir, "provenance.pgm")))
+    config = _keyvals(need(os.path.join(run_dir, "config_used.txt")))
+    stats = _keyvals(need(os.path.join(run_dir, "em_stats.txt")))
+    threshold = float(config.get("threshold", SolverParams().threshold))
+    h, w = gt_disp.shape
+    if est.shape != (h, w) or refocused.shape[:2] != (h, w):
+        raise PipelineError("run and ground truth dimensions do not match")
+
+    nan = float("nan")
+    rep = {}
+    ok = status == STATUS_VALID
+    err = np.abs(est - gt_disp)[ok]
+    rep["disparity_mae"] = float(err.mean()) if err.size else nan
+    rep["disparity_rmse"] = float(np.sqrt((err ** 2).mean())) if err.size else nan
+    rep["disparity_bad1"] = float((err > 1.0).mean()) if err.size else nan
+    rep["disparity_invalid_frac"] = float(1.0 - ok.mean())
+    sel = prov == PROV_REFOCUSED
+    diff = (refocused.astype(np.float64) - gt_bg.astype(np.float64))[sel]
+    rep["refocus_rmse"] = float(np.sqrt((diff ** 2).mean()) / 255.0) if diff.size else nan
+    npx = float(h * w)
+    rep["refocus_refocused_frac"] = float(sel.sum() / npx)
+    rep["refocus_fallback_frac"] = float((prov == PROV_FALLBACK).sum() / npx)
+    rep["refocus_copied_frac"] = float((prov == PROV_COPIED).sum() / npx)
+
+    hits_before = hits_after = rays = 0
+    uu, vv = np.meshgrid(np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64))
+    u, v, d = uu.ravel(), vv.ravel(), gt_disp.ravel()
+    for k in range(len(rig)):
+        seg = pnm.read_pnm(need(os.path.join(run_dir, view_name("seg", k, "pgm"))))
+        val = pnm.read_pnm(need(os.path.join(run_dir, view_name("valid", k, "pgm"))))
+        pri = pnm.read_pnm(need(os.path.join(gt_dir, view_name("prior", k, "pgm"))))
+        mask = pnm.read_pnm(need(os.path.join(gt_dir, view_name("gt_mask", k, "pgm"))))
+        pu, pv, front = rig.warp(u, v, d, k)
+        kh, kw = mask.shape
+        keep = front & (pu >= 0.0) & (pu <= kw - 1.0) & (pv >= 0.0) & (pv <= kh - 1.0)
+        keep &= val.ravel() > 0  # rays the solver classified
+        idx = np.flatnonzero(keep)
+        iu = np.clip(np.rint(pu[idx]), 0, kw - 1).astype(np.int64)
+        iv = np.clip(np.rint(pv[idx]), 0, kh - 1).astype(np.int64)
+        truth = mask[iv, iu] == 0
+        flat, ph, pw = flatten_channels(pri.astype(np.float32) / 255.0)
+        q = bilinear(flat, ph, pw, pu[idx], pv[idx])[:, 0]
+        hits_before += int(((q >= threshold) == truth).sum())
+        hits_after += int(((seg.ravel()[idx] > 0) == truth).sum())
+        rays += idx.size
+    rep["seg_accuracy_before"] = hits_before / rays if rays else nan
+    rep["seg_accuracy_after"] = hits_after / rays if rays else nan
+    rep["iterations_run"] = int(stats.get("iterations_run", "0"))
+    conv = stats.get("converged_after", "none")
+    rep["converged_after"] = -1 if conv == "none" else int(conv)
+    text = "".join(f"{k} = {v:.6f}\n" if isinstance(v, float) else f"{k} = {v}\n"
+                   for k, v in rep.items())
+    with open(out_path or os.path.join(run_dir, "report.txt"), "w") as fh:
+        fh.write(text)
+    return rep

@@ -55,7 +55,7 @@ def write_frame_dir(out, frame, rig):
 
 def main():
     out = {}
-    with tempfile.TemporaryDirectory() as tmp:
+    with tempfile.TemporaryDirectory() as tmp:  # noqa: SIM117
         for name, scene, opts in CASES:
             spec = st.occluder_scene(**scene)
             frame, _ = st.render(spec)
@@ -80,6 +80,28 @@ def main():
             }
             print(name, "artefacts", len(out[name]["artefacts"]), "iterations",
                   stats.iterations_run)
+        # run_synth presets (pipeline.py:320-358) -> run_reconstruct -> run_evaluate
+        # (pipeline.py:361-458): every synth file, the artefacts and report.txt
+        synth_cases = {}
+        for preset, seed in (("occluder", None), ("two_plane", 7), ("low_texture", None)):
+            name = f"synth_{preset}"
+            sdir = os.path.join(tmp, name, "synth")
+            rdir = os.path.join(tmp, name, "run")
+            rp.run_synth(sdir, preset=preset, seed=seed)
+            rp.run_reconstruct(os.path.join(sdir, "calib.txt"), sdir, rdir)
+            rep = rp.run_evaluate(rdir, sdir)
+            synth_cases[name] = {
+                "preset": preset, "seed": seed,
+                "synth": {f: digest(os.path.join(sdir, f)) for f in sorted(os.listdir(sdir))},
+                "artefacts": {f: digest(os.path.join(rdir, f))
+                              for f in sorted(os.listdir(rdir))
+                              if f not in ("timings.txt", "report.txt")},
+                "report_txt": open(os.path.join(rdir, "report.txt")).read(),
+                "report": {k: (None if isinstance(v, float) and v != v else v)
+                           for k, v in rep.items()},
+            }
+            print(name, rep)
+        out["_synth"] = synth_cases
     with open(os.path.join(HERE, "pipeline_cases.json"), "w") as fh:
         json.dump(out, fh, indent=1, sort_keys=True)
 

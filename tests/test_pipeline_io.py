@@ -1,4 +1,5 @@
-"""Frame-directory I/O and the artefact set.
+"""Frame-directory I/O and the artefact set, synthetic
+frame directories and evaluation (§8(f)4).
 
 CPU tests mirror the reference's test_pnm.py and test_pipeline.py:51-147
 (PNM wire format, config parsing, frame-directory validation) and check
@@ -23,7 +24,9 @@ from paper_2003_11076_b200 import pnm
 from paper_2003_11076_b200.synth import occluder_scene, render
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-CASES = json.load(open(os.path.join(HERE, "golden", "pipeline_cases.json")))
+_GOLD = json.load(open(os.path.join(HERE, "golden", "pipeline_cases.json")))
+CASES = {k: v for k, v in _GOLD.items() if not k.startswith("_")}
+SYNTH = _GOLD["_synth"]
 
 
 def _digest(path):
@@ -255,3 +258,57 @@ def test_run_reconstruct_sequence_equals_single_runs(tmp_path):
     assert len(stats) == 4
     for out in outs:
         _check_run(out, case)
+
+
+# -- run_synth / run_evaluate (§8(f)4) ----------------------------------------------------
+
+@pytest.mark.parametrize("name", sorted(SYNTH))
+def test_run_synth_matches_reference_files(tmp_path, name):
+    """Every file run_synth writes (scene.txt, calibration, views, priors,
+    ground-truth masks / disparity / background) equals the reference's."""
+    case = SYNTH[name]
+    out = str(tmp_path / "synth")
+    pl.run_synth(out, preset=case["preset"], seed=case["seed"])
+    got = {f: _digest(os.path.join(out, f)) for f in sorted(os.listdir(out))}
+    assert got == case["synth"]
+
+
+def test_run_synth_scene_file_and_errors(tmp_path):
+    from paper_2003_11076_b200 import synth
+    a = str(tmp_path / "a")
+    pl.run_synth(a, preset="occluder")
+    b = str(tmp_path / "b")
+    pl.run_synth(b, scene=os.path.join(a, "scene.txt"))
+    for f in os.listdir(a):
+        assert _digest(os.path.join(a, f)) == _digest(os.path.join(b, f)), f
+    with pytest.raises(pl.PipelineError, match="exactly one"):
+        pl.run_synth(str(tmp_path / "c"))
+    with pytest.raises(pl.PipelineError, match="unknown preset"):
+        pl.run_synth(str(tmp_path / "c"), preset="teapot")
+    bad = tmp_path / "bad.txt"
+    bad.write_text("width 64\nteapot 3\n")
+    with pytest.raises(pl.PipelineError, match="unknown directive"):
+        pl.run_synth(str(tmp_path / "c"), scene=str(bad))
+    spec = synth.load_scene(os.path.join(a, "scene.txt"))
+    assert spec.cameras == 5 and len(spec.occluders) == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(SYNTH))
+def test_run_evaluate_report_equals_reference(tmp_path, name):
+    """run_synth -> run_reconstruct -> run_evaluate: the artefacts and the
+    report.txt text equal the reference pipeline's on the same preset."""
+    from paper_2003_11076_b200.device import require_cuda
+    require_cuda()
+    case = SYNTH[name]
+    sdir = str(tmp_path / "synth")
+    rdir = str(tmp_path / "run")
+    pl.run_synth(sdir, preset=case["preset"], seed=case["seed"])
+    pl.run_reconstruct(os.path.join(sdir, "calib.txt"), sdir, rdir)
+    for f, want in case["artefacts"].items():
+        if f != "em_stats.txt":
+            assert _digest(os.path.join(rdir, f)) == want, f
+    pl.run_evaluate(rdir, sdir)
+    assert open(os.path.join(rdir, "report.txt")).read() == case["report_txt"]
+    with pytest.raises(pl.PipelineError, match="missing artifact"):
+        pl.run_evaluate(str(tmp_path / "nothing"), sdir)
