@@ -988,17 +988,56 @@ __device__ uint32_t estep_bnb(int K, const double* __restrict__ f, int stride, c
   double best = score_generic(mtop, K, f, stride, l1, l0, p);
   int bpop = __popc(mtop);
   uint32_t bm = mtop;
+  auto consider = [&](uint32_t mm) {
+    const double sc = score_generic(mm, K, f, stride, l1, l0, p);
+    const int pop = __popc(mm);
+    if (prefer(sc, pop, mm, best, bpop, bm)) {
+      best = sc;
+      bpop = pop;
+      bm = mm;
+    }
+  };
+  // The masks whose bound can still reach the best score, visited in
+  // decreasing bound order: the winner is usually among the first, and the
+  // rising best score then ends the visit early.  (More than BNB_LIST such
+  // masks: all of them are scored, in enumeration order.)
+  constexpr int BNB_LIST = 48;
+  uint32_t lm[BNB_LIST];
+  long long lb[BNB_LIST];
+  int nl = 0;
+  bool overflow = false;
+  const double thr0 = best * QS - errq;
   uint32_t m = 0;
   do {
-    if (m != mtop && (double)bound(m) + errq >= best * QS) {
-      const double sc = score_generic(m, K, f, stride, l1, l0, p);
-      const int pop = __popc(m);
-      if (prefer(sc, pop, m, best, bpop, bm)) {
-        best = sc;
-        bpop = pop;
-        bm = m;
+    if (m != mtop) {
+      const long long ub = bound(m);
+      if ((double)ub >= thr0) {
+        if (nl < BNB_LIST) {
+          int q = nl++;  // insertion, descending bound
+          while (q > 0 && lb[q - 1] < ub) {
+            lb[q] = lb[q - 1];
+            lm[q] = lm[q - 1];
+            --q;
+          }
+          lb[q] = ub;
+          lm[q] = m;
+        } else {
+          overflow = true;
+        }
       }
     }
+    m = (m - vbits) & vbits;
+  } while (m != 0);
+  if (!overflow) {
+    for (int q = 0; q < nl; ++q) {
+      if ((double)lb[q] + errq < best * QS) break;  // every later bound is lower still
+      consider(lm[q]);
+    }
+    return bm;
+  }
+  m = 0;
+  do {
+    if (m != mtop && (double)bound(m) + errq >= best * QS) consider(m);
     m = (m - vbits) & vbits;
   } while (m != 0);
   return bm;
