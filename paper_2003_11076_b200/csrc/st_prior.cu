@@ -152,15 +152,42 @@ __global__ void k_tile_groups(SupGeom g, double r2, const uint32_t* __restrict__
       __syncthreads();
     }
   }
-  // group ids (value = high 32 bits): serial scan by thread 0 over heads is
-  // cheap at these sizes; masks accumulate in scratch (global) for large
-  // buckets, in shared memory otherwise
-  if (threadIdx.x == 0) {
-    uint32_t gcur = 0;
-    for (int i = 0; i < n; ++i) {
-      if (i > 0 && (k[i] >> 32) != (k[i - 1] >> 32)) ++gcur;
-      if (in_smem) gid[i] = gcur;
+  // group ids (value = high 32 bits): the number of value changes up to
+  // each record -- a block-wide scan of the head flags over contiguous
+  // per-thread ranges (large buckets: counted on the fly below)
+  if (in_smem) {
+    __shared__ uint32_t s_wsum[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int i0 = min(n, (int)threadIdx.x * per), i1 = min(n, i0 + per);
+    uint32_t c = 0;
+    for (int i = i0; i < i1; ++i) c += (i > 0 && (k[i] >> 32) != (k[i - 1] >> 32)) ? 1u : 0u;
+    uint32_t x = c;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
+    if (lane == 31) s_wsum[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t acc = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        const uint32_t v = s_wsum[w];
+        s_wsum[w] = acc;
+        acc += v;
+      }
+      s_ng = acc + 1;
+    }
+    __syncthreads();
+    uint32_t gcur = s_wsum[wid] + (x - c);
+    for (int i = i0; i < i1; ++i) {
+      if (i > 0 && (k[i] >> 32) != (k[i - 1] >> 32)) ++gcur;
+      gid[i] = gcur;
+    }
+  } else if (threadIdx.x == 0) {
+    uint32_t gcur = 0;
+    for (int i = 1; i < n; ++i) gcur += (k[i] >> 32) != (k[i - 1] >> 32);
     s_ng = gcur + 1;
   }
   __syncthreads();
