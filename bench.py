@@ -640,9 +640,15 @@ def run_ours(args):
     model_full = npx * (s0.iterations_run * (c_bar * k * 16 + k * 20) + 7 * k)
     step_ms_mean = total_ms / args.steps
     traffic = None
+    pipes = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
     if os.path.exists(prof):
-        traffic = json.load(open(prof)).get("k_m_step_dram_bytes_per_launch")
+        tj = json.load(open(prof))
+        traffic = tj.get("k_m_step_dram_bytes_per_launch")
+        pipes = tj.get("k_m_step_pipes")
+        if pipes is not None:
+            pipes = dict(pipes, source=tj.get("source"),
+                         note="the bound that binds: FP64 issue + latency, not HBM")
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -669,7 +675,7 @@ def run_ours(args):
         "config": config_block(cfg, args, exact),
         "roofline": {"bound": "hbm", "kernel": "k_m_step", "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic,
+                     "traffic": traffic, "pipes": pipes,
                      "algorithmic_bytes_per_launch": bytes_m / max(1, n_m),
                      "unit_note": "16 B per descriptor sample the kernel takes: (pixel, "
                                   "evaluated real candidate, static in-margin view), "
