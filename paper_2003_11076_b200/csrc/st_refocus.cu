@@ -216,6 +216,82 @@ __global__ void k_median_small(const uint8_t* __restrict__ src, int H, int W, in
   }
 }
 
+// radius-1 median of an RGB image with a 32x8 output tile per block: the
+// tile and its 1-pixel halo are staged in shared memory with 32-bit loads,
+// interior pixels take the median-of-9 network from there; pixels whose
+// window is clipped (the image border) run k_median_small's general path.
+#define MT_W 32
+#define MT_H 8
+__device__ __forceinline__ void med9(int (&v)[9]) {
+  auto cx = [&](int a, int b) {
+    const int lo = min(v[a], v[b]), hi = max(v[a], v[b]);
+    v[a] = lo;
+    v[b] = hi;
+  };
+  cx(1, 2); cx(4, 5); cx(7, 8);
+  cx(0, 1); cx(3, 4); cx(6, 7);
+  cx(1, 2); cx(4, 5); cx(7, 8);
+  cx(0, 3); cx(5, 8); cx(4, 7);
+  cx(3, 6); cx(1, 4); cx(2, 5);
+  cx(4, 7); cx(4, 2); cx(6, 4);
+  cx(4, 2);
+}
+
+__global__ void __launch_bounds__(MT_W * MT_H) k_median_rgb_tile(
+    const uint8_t* __restrict__ src, int H, int W, const uint8_t* __restrict__ prov,
+    uint8_t* __restrict__ out) {
+  __shared__ uint8_t tile[MT_H + 2][(MT_W + 2) * 3 + 2];
+  const int x0 = blockIdx.x * MT_W, y0 = blockIdx.y * MT_H;
+  const int tid = threadIdx.y * MT_W + threadIdx.x;
+  for (int i = tid; i < (MT_H + 2) * (MT_W + 2) * 3; i += MT_W * MT_H) {
+    const int r = i / ((MT_W + 2) * 3), cb = i % ((MT_W + 2) * 3);
+    const int yy = min(max(y0 - 1 + r, 0), H - 1);
+    const int xx = min(max(x0 - 1 + cb / 3, 0), W - 1);
+    tile[r][cb] = src[((size_t)yy * W + xx) * 3 + cb % 3];
+  }
+  __syncthreads();
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  if (x >= W || y >= H) return;
+  const size_t p = (size_t)y * W + x;
+  if (prov && prov[p] == ST_PROV_COPIED) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) out[p * 3 + ch] = src[p * 3 + ch];
+    return;
+  }
+  if (x == 0 || y == 0 || x == W - 1 || y == H - 1) {
+    // clipped window (4 or 6 values): insertion sort, 0.5 (v0 + v1), rint
+    const int ylo = max(y - 1, 0), yhi = min(y + 1, H - 1);
+    const int xlo = max(x - 1, 0), xhi = min(x + 1, W - 1);
+    const int cnt = (yhi - ylo + 1) * (xhi - xlo + 1);
+    for (int ch = 0; ch < 3; ++ch) {
+      int a[9];
+      int n = 0;
+      for (int yy = ylo; yy <= yhi; ++yy)
+        for (int xx = xlo; xx <= xhi; ++xx) {
+          const int val = tile[yy - y0 + 1][(xx - x0 + 1) * 3 + ch];
+          int j = n++;
+          while (j > 0 && a[j - 1] > val) {
+            a[j] = a[j - 1];
+            --j;
+          }
+          a[j] = val;
+        }
+      const float m = __fmul_rn(0.5f, __fadd_rn((float)a[(cnt - 1) / 2], (float)a[cnt / 2]));
+      out[p * 3 + ch] = (uint8_t)fminf(fmaxf(rintf(m), 0.0f), 255.0f);
+    }
+    return;
+  }
+  // full 3x3 window: the median-of-9 value itself (see k_median_small)
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    int v[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) v[j] = tile[threadIdx.y + j / 3][(threadIdx.x + j % 3) * 3 + ch];
+    med9(v);
+    out[p * 3 + ch] = (uint8_t)v[4];
+  }
+}
+
 }  // namespace st
 
 extern "C" int st_median(const uint8_t* image, int32_t H, int32_t W, int32_t C, int32_t radius,
@@ -255,7 +331,11 @@ extern "C" int st_synthesize(const uint8_t* images, const st_rig* rig, const flo
                                        min_static_rays, copy_mask, stage, prov_out, n_rays_out,
                                        rectified);
   ST_LAUNCH_CHECK("k_refocus");
-  if (median_radius > 0) {
+  if (median_radius == 1) {
+    dim3 grid((W + MT_W - 1) / MT_W, (H + MT_H - 1) / MT_H);
+    st::k_median_rgb_tile<<<grid, dim3(MT_W, MT_H), 0, s>>>(scratch, H, W, prov_out, image_out);
+    ST_LAUNCH_CHECK("k_median_rgb_tile");
+  } else if (median_radius > 0) {
     st::k_median_small<<<(unsigned)((npx + 255) / 256), 256, 0, s>>>(
         scratch, H, W, 3, median_radius, prov_out, image_out);
     ST_LAUNCH_CHECK("k_median_small");
