@@ -16,7 +16,9 @@
 #endif
 #define MSTEP_BOUNDS __launch_bounds__(EM_BLOCK, MSTEP_MIN_BLOCKS)
 #define STATS_BLOCK 256
-#define STATS_GRID (148 * 4)  // fixed grid of k_em_stats: its sums are deterministic
+#ifndef STATS_GRID
+#define STATS_GRID (148 * 2)  // fixed grid of k_em_stats: deterministic sums (measured best)
+#endif
 #define ESTEP_BLOCK 64
 #define ESTEP_TAPS_BLOCK 128
 #define ESTEP_CERT_BLOCK 128
