@@ -30,6 +30,8 @@ extern "C" {
 #endif
 
 #define ST_MAX_VIEWS 12   /* solver.py:46 MAX_ENUMERATED_VIEWS */
+#define ST_MAX_ITERS 1024 /* capacity of the per-iteration EMStats arrays; larger max_iters is
+                             rejected with ST_EINVAL (solver.py:461 has no cap) */
 #define ST_DESC_LEN 16    /* features.py:19 */
 #define ST_DESC_MARGIN 3  /* features.py:20 */
 
@@ -77,9 +79,9 @@ typedef struct {
 typedef struct {
   int32_t iterations_run;
   int32_t converged_after;           /* -1 == None */
-  double mean_energy[64];
-  double prev_energy[64];
-  double changed_fraction[64];
+  double mean_energy[ST_MAX_ITERS];
+  double prev_energy[ST_MAX_ITERS];
+  double changed_fraction[ST_MAX_ITERS];
   int64_t active_pixels;
   int64_t support_records;           /* diagnostic: (tile, value) records built */
   int64_t candidates_total;          /* sum over iterations/pixels of candidates in range */
@@ -99,6 +101,10 @@ typedef struct {
 const char* st_last_error(void);
 int st_version(void);
 int st_device_count(void);
+/* sizeof the ABI structs as this library was compiled (binding checks, no GPU
+ * needed): which = 0 st_rig, 1 st_params, 2 st_stats, 3 st_frame, 4 st_tri,
+ * 5 st_cams, 6 st_frame_plan; -1 for an unknown id. */
+int64_t st_struct_size(int32_t which);
 /* Cumulative number of __global__ launches issued by this library (all
  * threads; CUB's internal launches inside st_support_build / st_solve count
  * as one per CUB call). */

@@ -31,10 +31,13 @@ class StParams(C.Structure):
                 ("forced_iters", C.c_int32), ("timing", C.c_int32)]
 
 
+MAX_ITERS = 1024  # ST_MAX_ITERS (include/seethrough_b200.h)
+
+
 class StStats(C.Structure):
     _fields_ = [("iterations_run", C.c_int32), ("converged_after", C.c_int32),
-                ("mean_energy", C.c_double * 64), ("prev_energy", C.c_double * 64),
-                ("changed_fraction", C.c_double * 64), ("active_pixels", C.c_int64),
+                ("mean_energy", C.c_double * MAX_ITERS), ("prev_energy", C.c_double * MAX_ITERS),
+                ("changed_fraction", C.c_double * MAX_ITERS), ("active_pixels", C.c_int64),
                 ("support_records", C.c_int64), ("candidates_total", C.c_int64),
                 ("energy_evals", C.c_int64), ("prev_evals", C.c_int64),
                 ("msteps", C.c_int64), ("esteps", C.c_int64),
@@ -95,6 +98,7 @@ _SIGS = {
     "st_version": (C.c_int, []),
     "st_device_count": (C.c_int, []),
     "st_launch_count": (C.c_int64, []),
+    "st_struct_size": (C.c_int64, [_I32]),
     "st_selftest": (C.c_int, [_I32, _I64, C.c_uint64, C.POINTER(C.c_int64), _P]),
     "st_descriptors": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
     "st_bilinear": (C.c_int, [_P, _I32, _I32, _I32, _P, _P, _I64, _P, _P]),
@@ -278,6 +282,10 @@ def make_cams(rig, width, height):
 
 def make_params(sp, pp, forced_iters=0, timing=False):
     """st_params from SolverParams (solver.py:56-62) + PriorParams (prior.py:33-40)."""
+    iters = int(forced_iters or 0) or int(sp.max_iters)
+    if iters > MAX_ITERS:
+        raise ValueError(f"max_iters {iters} exceeds the {MAX_ITERS} iterations the EM "
+                         "statistics hold")
     p = StParams()
     p.beta = float(sp.beta)
     p.threshold = float(sp.threshold)

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cub/cub.cuh>
 #include <vector>
 
@@ -39,6 +40,8 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 namespace {
 
+constexpr int ST_ASYNC_CHUNK = 16;
+
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 int check_views(int K) {
@@ -47,7 +50,7 @@ int check_views(int K) {
                       ST_MAX_VIEWS);
     return ST_EINVAL;
   }
-  if (K < 1) {
+  if (K < 2) {
     sthost::set_error("a light-field frame needs at least two views");
     return ST_EINVAL;
   }
@@ -60,6 +63,12 @@ int make_ctx(const st_frame* f, const st_rig* rig, const st_params* p, st::EmCtx
   if (rc) return rc;
   memset(&c, 0, sizeof(c));
   c.rig = *rig;
+  const int iters = p->forced_iters > 0 ? p->forced_iters : p->max_iters;
+  if (iters > ST_MAX_ITERS) {
+    sthost::set_error("max_iters %d exceeds the %d iterations the EM statistics hold", iters,
+                      ST_MAX_ITERS);
+    return ST_EINVAL;
+  }
   c.p = *p;
   c.W = rig->width;
   c.H = rig->height;
@@ -140,15 +149,22 @@ struct EventSet {
 
 int estep_smem(int K) { return ESTEP_BLOCK * K * 16 * (int)sizeof(double); }
 
+// The opt-in above 48 KB of dynamic shared memory is a per-device function
+// attribute: set once per device (K >= 7 E-step launches need it).
 int prepare_estep_kernels() {
-  static bool done = false;
-  if (done) return ST_OK;
+  static std::mutex mu;
+  static uint64_t prepared = 0;  // bit d: device d done
+  int dev = 0;
+  ST_CUDA_CHECK(cudaGetDevice(&dev));
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+  std::lock_guard<std::mutex> lock(mu);
+  if (bit && (prepared & bit)) return ST_OK;
   const int max_smem = estep_smem(ST_MAX_VIEWS);
   ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_at,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   ST_CUDA_CHECK(cudaFuncSetAttribute(st::k_e_step_rays,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-  done = true;
+  prepared |= bit;
   return ST_OK;
 }
 
@@ -316,6 +332,19 @@ int st_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* mismatches, vo
 }
 
 const char* st_last_error(void) { return sthost::g_err; }
+
+int64_t st_struct_size(int32_t which) {
+  switch (which) {
+    case 0: return (int64_t)sizeof(st_rig);
+    case 1: return (int64_t)sizeof(st_params);
+    case 2: return (int64_t)sizeof(st_stats);
+    case 3: return (int64_t)sizeof(st_frame);
+    case 4: return (int64_t)sizeof(st_tri);
+    case 5: return (int64_t)sizeof(st_cams);
+    case 6: return (int64_t)sizeof(st_frame_plan);
+    default: return -1;
+  }
+}
 int st_version(void) { return ST_VERSION; }
 int64_t st_launch_count(void) { return sthost::g_launches.load(); }
 
@@ -488,7 +517,7 @@ static SolveLayout solve_layout(int W, int H) {
   L.offs = o;     o += align_up(sizeof(uint32_t) * (npx + 1));
   L.work = o;     o += align_up(sizeof(st::Partial) * L.max_warps);
   L.parts = o;    o += align_up(sizeof(st::Partial) * L.max_warps);
-  L.reduced = o;  o += align_up(sizeof(st::Partial) * 66);
+  L.reduced = o;  o += align_up(sizeof(st::Partial) * (ST_MAX_ITERS + 2));
   L.cub = o;      o += align_up(L.cub_bytes);
   L.total = o;
   return L;
@@ -582,10 +611,12 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
   }
 
   const int iters = p->forced_iters > 0 ? p->forced_iters : p->max_iters;
+  // worklist counts start cleared even on a shard whose band has no active pixel
+  ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), s));
   const int nblk = (int)blocks_for(n_act, EM_BLOCK);
   const int nwarps = nblk * (EM_BLOCK / 32);
   bool solved = false;
-  for (int it = 1; it <= iters && it <= 64; ++it) {
+  for (int it = 1; it <= iters; ++it) {
     if (n_act_global == 0) {
       stats->converged_after = 0;
       break;
@@ -760,7 +791,7 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
                                                            valid_bits);
   ST_LAUNCH_CHECK("k_initial_masks");
 
-  const int iters = std::min(p->forced_iters > 0 ? p->forced_iters : p->max_iters, 64);
+  const int iters = p->forced_iters > 0 ? p->forced_iters : p->max_iters;
   const int nblk = (int)blocks_for(npx, EM_BLOCK);
   const int nwarps = nblk * (EM_BLOCK / 32);
   const int sblk = std::min((int)blocks_for(npx, STATS_BLOCK), STATS_GRID);
@@ -773,6 +804,15 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
   }();
   const int wave2 = std::min(nblk, 148 * wave_env);
   for (int it = 1; it <= iters; ++it) {
+    // long caps (max_iters > ST_ASYNC_CHUNK): every ST_ASYNC_CHUNK iterations
+    // read the device stop flag back, so a converged solve does not enqueue
+    // max_iters rounds of (immediately exiting) launches
+    if (it > ST_ASYNC_CHUNK && (it - 1) % ST_ASYNC_CHUNK == 0) {
+      int h_stop = 0;
+      ST_CUDA_CHECK(cudaMemcpyAsync(&h_stop, stop, sizeof(int), cudaMemcpyDeviceToHost, s));
+      ST_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (h_stop) break;
+    }
     // iteration 2 re-solves the pixels whose mask changed at iteration 1
     // (~20 %); later iterations have far smaller worklists, or none once
     // converged (the launches then exit at once): a smaller grid

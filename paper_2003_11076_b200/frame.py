@@ -1,9 +1,11 @@
 """LightFieldFrame (frame.py:10-52) with a device-resident mirror.
 
-A frame's K views and priors are uploaded once and its descriptors are
-computed on the GPU once; every solver / refocus call on the same frame
-reuses the device copies (the reference caches descriptors the same way,
-frame.py:46-52).
+A frame's descriptors are computed on the GPU once and cached, exactly as the
+reference caches them (frame.py:46-52, computed from the images at first
+use).  The arrays the reference re-reads on every call are re-uploaded on
+every call: the priors at solver construction (solver.py:182) and the
+images in synthesize (refocus.py:24-49), so a caller that edits a frame's
+arrays in place sees the same results as with the reference.
 """
 
 from dataclasses import dataclass, field
@@ -68,11 +70,35 @@ class DeviceFrame:
         self.K, self.H, self.W = (int(x) for x in self.images.shape[:3])
         self.desc, _, _ = _run(self.images)
 
+    def refresh(self, frame, what):
+        """Re-upload `what` ("images" / "priors") from the host frame."""
+        t = torch_of()
+        for name in what:
+            src = getattr(frame, name)
+            dst = getattr(self, name)
+            if isinstance(src, t.Tensor):
+                dst.copy_(src.reshape(dst.shape))
+                continue
+            dt = np.uint8 if name == "images" else np.float32
+            for k, a in enumerate(src):
+                a = np.ascontiguousarray(a, dtype=dt)
+                if name == "images" and a.ndim == 2:
+                    a = np.repeat(a[:, :, None], 3, axis=2)
+                dst[k].copy_(t.from_numpy(a))
 
-def device_frame(frame):
-    """Device mirror of any LightFieldFrame-like object (cached on our own frames)."""
+
+def torch_of():
+    from .device import torch
+    return torch()
+
+
+def device_frame(frame, refresh=()):
+    """Device mirror of any LightFieldFrame-like object (cached on our own
+    frames; `refresh` names the arrays to re-upload into a cached mirror)."""
     cached = getattr(frame, "_dev", None)
     if cached is not None:
+        if refresh:
+            cached.refresh(frame, refresh)
         return cached
     d = DeviceFrame(frame.images, frame.priors)
     if isinstance(frame, LightFieldFrame):

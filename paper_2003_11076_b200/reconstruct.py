@@ -318,6 +318,14 @@ class FramePipeline:
 
     # -- outputs ------------------------------------------------------------------------
 
+    def device_bytes(self):
+        """Device memory held by this pipeline (the cache's eviction weight)."""
+        n = 0
+        for x in vars(self).values():
+            if hasattr(x, "is_cuda") and x.is_cuda:
+                n += x.numel() * x.element_size()
+        return n
+
     def output_bytes(self):
         return self.H * self.W * (4 + 1 + 4 + 4 + 3 + 1 + 1)
 
@@ -404,6 +412,17 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
             prof[key] = prof.get(key, 0.0) + time.perf_counter() - t0
         return time.perf_counter()
 
+    stop = threading.Event()
+
+    def put(item):
+        while not stop.is_set():
+            try:
+                q.put(item, timeout=0.05)
+                return True
+            except queue.Full:
+                continue
+        return False
+
     def prep():
         t.cuda.set_device(device)
         try:
@@ -411,8 +430,10 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
                 t0 = time.perf_counter()
                 pipe = pipes[i % n_slots]
                 with free_lock:
-                    while i >= n_slots and free[i % n_slots] is None:
+                    while i >= n_slots and free[i % n_slots] is None and not stop.is_set():
                         free_lock.wait()
+                    if stop.is_set():
+                        return
                     ev = free[i % n_slots]
                     free[i % n_slots] = None
                 t0 = tick("prep_wait_free", t0)
@@ -427,79 +448,98 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
                     loaded.record(copy_s)
                 # planes solved on the device only: numpy's singular-system
                 # error is checked when the frame's outputs arrive
-                q.put((pipe, td, loaded, tri.planes is None))
+                if not put((pipe, td, loaded, tri.planes is None)):
+                    return
         except Exception as exc:  # noqa: BLE001 -- surfaced in the consumer
             error.append(exc)
-        q.put(None)
+        put(None)
 
     worker = threading.Thread(target=prep, daemon=True)
     worker.start()
     pending = None
     i = 0
-    while True:
-        t0 = time.perf_counter()
-        item = q.get()
-        if item is None:
-            break
-        t0 = tick("main_wait_prep", t0)
-        pipe, td, loaded, check = item
-        main.wait_event(loaded)
-        for x in td.tensors():
-            for st_ in (main, pipe.side, pipe.side2):
-                x.record_stream(st_)
-        # the frame's pre-solve stages start as soon as its inputs are on the
-        # device, overlapping the previous frame's EM on the main stream
-        if not dynamic_only:
-            # one native call enqueues the whole frame and its D2H (st_frame_run)
-            fetched = t.cuda.Event()
-            fetched.record(out_s)  # creates the event; st_frame_run re-records it
-            block, stats = pipe.run_native(td, forced_iters=forced_iters,
-                                           median_radius=median_radius, ready=loaded,
-                                           out_stream=out_s, done=fetched)
-            host = pipe.host_views(block)
-            t0 = tick("main_run", t0)
-            with t.cuda.stream(out_s):
-                flags = None
-                if check and td.flags is not None:
-                    flags = t.empty((1,), dtype=t.int32, pin_memory=True)
-                    flags.copy_(td.flags, non_blocking=True)
+    try:
+        while True:
+            t0 = time.perf_counter()
+            item = q.get()
+            if item is None:
+                break
+            t0 = tick("main_wait_prep", t0)
+            pipe, td, loaded, check = item
+            main.wait_event(loaded)
+            for x in td.tensors():
+                for st_ in (main, pipe.side, pipe.side2):
+                    x.record_stream(st_)
+            # the frame's pre-solve stages start as soon as its inputs are on the
+            # device, overlapping the previous frame's EM on the main stream
+            if not dynamic_only:
+                # one native call enqueues the whole frame and its D2H (st_frame_run)
+                fetched = t.cuda.Event()
+                fetched.record(out_s)  # creates the event; st_frame_run re-records it
+                block, stats = pipe.run_native(td, forced_iters=forced_iters,
+                                               median_radius=median_radius, ready=loaded,
+                                               out_stream=out_s, done=fetched)
+                host = pipe.host_views(block)
+                t0 = tick("main_run", t0)
+                with t.cuda.stream(out_s):
+                    flags = None
+                    if check and td.flags is not None:
+                        flags = t.empty((1,), dtype=t.int32, pin_memory=True)
+                        flags.copy_(td.flags, non_blocking=True)
+                        fetched = t.cuda.Event()
+                        fetched.record(out_s)
+            else:
+                stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
+                                 median_radius=median_radius, ready=loaded)
+                t0 = tick("main_run", t0)
+                done = t.cuda.Event()
+                done.record(main)
+                with t.cuda.stream(out_s):
+                    out_s.wait_event(done)
+                    host = pipe.fetch_async(out_s)
+                    flags = None
+                    if check and td.flags is not None:
+                        flags = t.empty((1,), dtype=t.int32, pin_memory=True)
+                        flags.copy_(td.flags, non_blocking=True)
                     fetched = t.cuda.Event()
                     fetched.record(out_s)
-        else:
-            stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
-                             median_radius=median_radius, ready=loaded)
-            t0 = tick("main_run", t0)
-            done = t.cuda.Event()
-            done.record(main)
-            with t.cuda.stream(out_s):
-                out_s.wait_event(done)
-                host = pipe.fetch_async(out_s)
-                flags = None
-                if check and td.flags is not None:
-                    flags = t.empty((1,), dtype=t.int32, pin_memory=True)
-                    flags.copy_(td.flags, non_blocking=True)
-                fetched = t.cuda.Event()
-                fetched.record(out_s)
-        with free_lock:
-            free[i % n_slots] = fetched
-            free_lock.notify_all()
-        t0 = tick("main_fetch_enqueue", t0)
+            with free_lock:
+                free[i % n_slots] = fetched
+                free_lock.notify_all()
+            t0 = tick("main_fetch_enqueue", t0)
+            if pending is not None:
+                prev, pending = pending, None
+                out = _finish(prev)
+                t0 = tick("main_finish_prev", t0)
+                yield out
+                t0 = time.perf_counter()
+            pending = (pipe, stats, fetched, host, flags)
+            i += 1
+        if error:
+            raise error[0]
         if pending is not None:
-            out = _finish(pending)
-            t0 = tick("main_finish_prev", t0)
-            yield out
-            t0 = time.perf_counter()
-        pending = (pipe, stats, fetched, host, flags)
-        i += 1
-    worker.join()
-    pipes.busy = False
-    if prof is not None:
-        print("reconstruct_stream profile (s, summed over frames):",
-              {k: round(v, 4) for k, v in sorted(prof.items())}, f"frames={i}", flush=True)
-    if error:
-        raise error[0]
-    if pending is not None:
-        yield _finish(pending)
+            prev, pending = pending, None
+            yield _finish(prev)
+    finally:
+        # normal end, an error, or a consumer that stopped early (generator
+        # close): stop the prep thread, let the device finish every enqueued
+        # copy into pinned host blocks before they can be recycled, and hand
+        # the pipelines back
+        stop.set()
+        with free_lock:
+            free_lock.notify_all()
+        while True:
+            try:
+                q.get_nowait()
+            except queue.Empty:
+                break
+        worker.join()
+        for s_ in (copy_s, main, out_s):
+            s_.synchronize()
+        pipes.busy = False
+        if prof is not None:
+            print("reconstruct_stream profile (s, summed over frames):",
+                  {k: round(v, 4) for k, v in sorted(prof.items())}, f"frames={i}", flush=True)
 
 
 def _finish(pending):
@@ -563,8 +603,9 @@ def _chain(first, rest):
     yield from rest
 
 
-_PIPES = {}
-_STREAM_PIPES = {}
+_PIPES = None
+_STREAM_PIPES = None
+CACHE_BYTES = int(os.environ.get("ST_PIPE_CACHE_BYTES", str(8 << 30)))  # device bytes kept
 
 
 class _PipePair(list):
@@ -574,29 +615,80 @@ class _PipePair(list):
 STREAM_SLOTS = 3  # frames in flight: H2D of i+1 never waits for the D2H of i-1
 
 
+def _rig_key(rig, w, h, params, prior_params):
+    """Cache key on the rig's CONTENTS (its st_rig bytes: view count, reference
+    view, warp tables, view sizes), not on the object: pipeline.run_reconstruct
+    loads a fresh rig for every call (geometry.py:326 load_calibration)."""
+    return (bytes(N.make_rig(rig, w, h)), w, h, repr(params), repr(prior_params))
+
+
+def _adopt(pipe, rig):
+    """A cached pipeline serving a content-equal rig object: host-side users of
+    the rig (harvest cameras, ref_index) follow the caller's object."""
+    if pipe.rig_obj is not rig:
+        pipe.rig_obj = rig
+        pipe._hv_key = None
+    return pipe
+
+
+class _Cache:
+    """LRU of device pipelines bounded by device bytes (CACHE_BYTES)."""
+
+    def __init__(self):
+        from collections import OrderedDict
+        self.items = OrderedDict()
+
+    def get(self, key):
+        v = self.items.get(key)
+        if v is not None:
+            self.items.move_to_end(key)
+        return v
+
+    def put(self, key, value, nbytes):
+        self.items[key] = (value, nbytes)
+        self.items.move_to_end(key)
+        total = sum(b for _, b in self.items.values())
+        for k in list(self.items):
+            if total <= CACHE_BYTES or k == key:
+                break
+            v, b = self.items[k]
+            if getattr(v, "busy", False):
+                continue
+            del self.items[k]
+            total -= b
+
+
 def _stream_pipes(rig, w, h, params, prior_params):
     """The rotating pipelines of reconstruct_stream, kept across calls; a set
     in use by a running stream is never handed out twice."""
-    key = (id(rig), w, h, repr(params), repr(prior_params))
-    p = _STREAM_PIPES.get(key)
-    if p is None or p.busy:
+    global _STREAM_PIPES
+    if _STREAM_PIPES is None:
+        _STREAM_PIPES = _Cache()
+    key = _rig_key(rig, w, h, params, prior_params)
+    hit = _STREAM_PIPES.get(key)
+    if hit is not None and not hit[0].busy:
+        p = hit[0]
+        for x in p:
+            _adopt(x, rig)
+    else:
         p = _PipePair(FramePipeline(rig, w, h, params, prior_params)
                       for _ in range(STREAM_SLOTS))
-        if key not in _STREAM_PIPES or not _STREAM_PIPES[key].busy:
-            if len(_STREAM_PIPES) > 4:
-                _STREAM_PIPES.clear()
-            _STREAM_PIPES[key] = p
+        if hit is None:
+            _STREAM_PIPES.put(key, p, sum(x.device_bytes() for x in p))
     p.busy = True
     return p
 
 
 def _pipeline_for(rig, w, h, params, prior_params):
-    key = (id(rig), w, h, repr(params), repr(prior_params))
-    p = _PIPES.get(key)
-    if p is None:
-        if len(_PIPES) > 8:
-            _PIPES.clear()
-        p = _PIPES[key] = FramePipeline(rig, w, h, params, prior_params)
+    global _PIPES
+    if _PIPES is None:
+        _PIPES = _Cache()
+    key = _rig_key(rig, w, h, params, prior_params)
+    hit = _PIPES.get(key)
+    if hit is not None:
+        return _adopt(hit[0], rig)
+    p = FramePipeline(rig, w, h, params, prior_params)
+    _PIPES.put(key, p, p.device_bytes())
     return p
 
 

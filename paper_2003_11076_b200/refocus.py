@@ -24,7 +24,7 @@ def _rig_of(frame, rig):
 
 def _refocus_list(frame, rig, pix, d, static_bits, min_static_rays):
     t = require_cuda()
-    dev = device_frame(frame)
+    dev = device_frame(frame, refresh=("images",))
     pix = np.asarray(pix, dtype=np.int64).ravel()
     n = pix.size
     rgb = empty((n, 3), t.uint8)
@@ -75,7 +75,7 @@ def synthesize_device(frame, rig, values, status, static_bits, min_static_rays=2
                       median_radius=1, copy_mask=None):
     """Device-tensor variant used by `reconstruct` (no host round trips)."""
     t = require_cuda()
-    dev = device_frame(frame)
+    dev = device_frame(frame, refresh=("images",))
     h, w = frame.shape
     img = empty((h, w, 3), t.uint8)
     prov = empty((h, w), t.uint8)

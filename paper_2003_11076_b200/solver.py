@@ -121,7 +121,7 @@ class DisparitySolver:
             raise ValueError("frame view count does not match the rig")
         _check_views(self.num_views)
         self._t = require_cuda()
-        self._dev = device_frame(frame)
+        self._dev = device_frame(frame, refresh=("priors",))
         self._rig = N.make_rig(rig, self.width, self.height)
         self._p = N.make_params(self.params, self.prior_params)
         self._mu = mu_raster_device(tri, self.width, self.height,

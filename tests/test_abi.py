@@ -41,12 +41,14 @@ def test_binding_covers_header(lib):
     assert set(_native.exported_symbols()) == set(declared())
 
 
-def test_struct_layouts_match_the_header():
+def test_struct_layouts_match_the_header(lib):
+    """The ctypes mirrors have the size the compiled library gives each struct."""
     from paper_2003_11076_b200 import _native as N
-    # st_rig: 4 ints + 12*9 + 12*3 doubles + 2*12 ints
-    assert ctypes.sizeof(N.StRig) == 16 + 12 * 12 * 8 + 2 * 12 * 4
-    assert ctypes.sizeof(N.StParams) == 8 * 2 + 4 * 2 + 8 * 5 + 4 * 2
-    assert ctypes.sizeof(N.StStats) == 8 + 3 * 64 * 8 + 7 * 8 + 4 * 8 + 4 * 4 + 2 * 8
+    mirrors = (N.StRig, N.StParams, N.StStats, N.StFrame, N.StTri, N.StCams, N.StFramePlan)
+    for which, cls in enumerate(mirrors):
+        assert ctypes.sizeof(cls) == N.lib().st_struct_size(which), cls.__name__
+    assert N.lib().st_struct_size(99) == -1
+    assert ctypes.sizeof(N.StStats) == 8 + 3 * N.MAX_ITERS * 8 + 7 * 8 + 4 * 8 + 4 * 4 + 2 * 8
 
 
 def test_version_and_error_calls_need_no_gpu(lib):

@@ -258,7 +258,33 @@ def test_full_solve_matches_reference(st, name):
         assert stats.converged_after == ref["converged_after"]
         assert np.allclose(stats.mean_energy, ref["mean_energy"], rtol=1e-9)
         assert np.allclose(stats.prev_energy, ref["prev_energy"], rtol=1e-9)
-        assert np.allclose(stats.changed_fraction, ref["changed_fraction"], atol=2e-4)
+        assert list(stats.changed_fraction) == list(ref["changed_fraction"])
+        _differences_are_low_margin(g, dyn, dmap.values, seg.static_bits, seg.valid_bits,
+                                    want_v, g[f"{tag}_static"], g[f"{tag}_valid"])
+
+
+def _differences_are_low_margin(g, dyn, values, sbits, vbits, want_v, want_s, want_b):
+    """north_star: exact wherever the reference's decision margin exceeds
+    1e-5.  Any pixel that differs must have a final-iteration M-step margin
+    (values) or E-step margin (bits) <= 1e-5, recomputed with the oracle on
+    the final-iteration state."""
+    dv = (values != want_v).ravel()
+    db = ((sbits != want_s) | (vbits != want_b)).ravel()
+    if not (dv.any() or db.any()):
+        return
+    o = oracle_solver(g)
+    trace = []
+    o.solve(dynamic_only=dyn, trace=trace)
+    before, d, _, status = trace[-1]
+    act = o.active_set(dyn)
+    _, _, mm = o.m_margins(act, before)
+    m_marg = np.full(values.size, np.inf)
+    m_marg[act] = mm
+    e_marg = np.full(values.size, np.inf)
+    ok = status != oracle.STATUS_LOW_TEXTURE
+    e_marg[act[ok]] = o.e_margins(act[ok], d[ok])
+    assert not (dv & (m_marg > MARGIN)).any(), np.flatnonzero(dv & (m_marg > MARGIN))[:10]
+    assert not (db & (e_marg > MARGIN) & (m_marg > MARGIN)).any()
 
 
 @pytest.mark.parametrize("name", SCENES)
@@ -293,7 +319,7 @@ def test_reconstruct_end_to_end(st, name):
         assert r.stats.converged_after == ref["converged_after"]
         assert np.allclose(r.stats.mean_energy, ref["mean_energy"], rtol=1e-9)
         assert np.allclose(r.stats.prev_energy, ref["prev_energy"], rtol=1e-9)
-        assert np.allclose(r.stats.changed_fraction, ref["changed_fraction"], atol=2e-4)
+        assert list(r.stats.changed_fraction) == list(ref["changed_fraction"])
 
 
 def test_solver_errors(st):
