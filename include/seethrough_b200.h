@@ -309,6 +309,50 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
              st_stats* stats, void* workspace, int64_t workspace_bytes,
              st_reduce_fn reduce, void* reduce_user, void* stream);
 
+/* ---- row bands (BASELINE C3/C4) ------------------------ */
+
+/* Per-iteration exchange of the row-band shards' statistics records
+ * (solver.py:473-485's GLOBAL convergence rule, EMStats means): gather
+ * every shard's record (st_band_record_bytes bytes, at rec_send) into
+ * rec_recv (world records, rank order), stream-ordered on `stream` (e.g.
+ * ncclAllGather; torch.distributed all_gather_into_tensor).  0 = success. */
+typedef int (*st_exchange_fn)(void* stream, void* user);
+int64_t st_band_record_bytes(void);
+
+/* st_solve_async for one row band of a frame split across shards: pixels
+ * of rows [ext0, ext1) are solved (the band [row0, row1) plus the halo rows
+ * the median reads; halo pixels are pure per-pixel functions, so they equal
+ * the neighbour's own), only rows [row0, row1) enter the statistics, and
+ * after each iteration's statistics the record exchange + k_band_control
+ * apply the reference's global stop rule on every shard (the host reads the
+ * stop flag back once per iteration instead of enqueueing max_iters rounds
+ * of exchanges).  Outputs are full-frame arrays of which rows [ext0, ext1)
+ * are written.  dynamic_only: active = ref prior < threshold within the
+ * rows (solver.py:449-452; one host read-back for the list size).  With
+ * world == 1 and exchange == NULL this is the single-device solve of rows
+ * [row0, row1) (the dynamic_only path of reconstruct_stream). */
+int st_solve_rows(const st_frame* f, const st_rig* rig, const st_params* p,
+                  int32_t dynamic_only, int32_t row0, int32_t row1, int32_t ext0, int32_t ext1,
+                  float* values, uint8_t* status, uint32_t* static_bits, uint32_t* valid_bits,
+                  st_stats* stats_dev, void* workspace, int64_t workspace_bytes,
+                  st_exchange_fn exchange, void* user, int32_t world, void* rec_send,
+                  void* rec_recv, void* stream);
+
+/* features.py:81-104 for rows [row0, row1) of K RGB views only (row bands:
+ * the images must hold rows [row0 - 3, row1 + 3) of the frame, clipped). */
+int st_descriptors_rows(const uint8_t* images, int32_t K, int32_t H, int32_t W,
+                        uint8_t* desc_out, int32_t row0, int32_t row1, void* stream);
+
+/* st_synthesize restricted to a row band: the refocus of rows [ext0, ext1)
+ * and the median rewrite of rows [row0, row1) (ext must cover row0 - r and
+ * row1 + r, clipped to the frame). */
+int st_synthesize_rows(const uint8_t* images, const st_rig* rig, const float* values,
+                       const uint8_t* status, const uint32_t* static_bits,
+                       int32_t min_static_rays, int32_t median_radius,
+                       const uint8_t* copy_mask, uint8_t* image_out, uint8_t* prov_out,
+                       uint8_t* n_rays_out, uint8_t* scratch, int32_t row0, int32_t row1,
+                       int32_t ext0, int32_t ext1, void* stream);
+
 /* ---- refocus (refocus.py:24-148) ------------------------------------- */
 
 /* synthesize: Eq. 2 static-ray average + provenance + n_rays, then the

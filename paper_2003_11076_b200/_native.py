@@ -88,6 +88,7 @@ class StFramePlan(C.Structure):
 
 
 REDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int32, C.c_void_p)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)  # st_exchange_fn(stream, user)
 
 _P = C.c_void_p
 _I32 = C.c_int32
@@ -136,6 +137,13 @@ _SIGS = {
     "st_solve_workspace": (C.c_int64, [_I32, _I32, _I32]),
     "st_solve": (C.c_int, [C.POINTER(StFrame), C.POINTER(StRig), C.POINTER(StParams), _I32, _P,
                            _P, _P, _P, _P, C.POINTER(StStats), _P, _I64, REDUCE_FN, _P, _P]),
+    "st_band_record_bytes": (C.c_int64, []),
+    "st_solve_rows": (C.c_int, [C.POINTER(StFrame), C.POINTER(StRig), C.POINTER(StParams), _I32,
+                                _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _I64,
+                                EXCHANGE_FN, _P, _I32, _P, _P, _P]),
+    "st_descriptors_rows": (C.c_int, [_P, _I32, _I32, _I32, _P, _I32, _I32, _P]),
+    "st_synthesize_rows": (C.c_int, [_P, C.POINTER(StRig), _P, _P, _P, _I32, _I32, _P, _P, _P,
+                                     _P, _P, _I32, _I32, _I32, _I32, _P]),
     "st_synthesize": (C.c_int, [_P, C.POINTER(StRig), _P, _P, _P, _I32, _I32, _P, _P, _P, _P,
                                 _P, _P]),
     "st_refocus_pixels": (C.c_int, [_P, C.POINTER(StRig), _P, _P, _P, _I64, _I32, _P, _P, _P,

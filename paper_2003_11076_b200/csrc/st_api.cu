@@ -583,7 +583,7 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
   if (!dense) {
     const float* ref_prior = f->priors + (size_t)rig->ref_index * npx;
     st::k_flag_active<<<blocks_for(npx, 256), 256, 0, s>>>(ref_prior, active_mask, npx,
-                                                          p->threshold, flags);
+                                                          p->threshold, flags, 0, npx);
     ST_LAUNCH_CHECK("k_flag_active");
     ST_CUDA_CHECK(cudaMemsetAsync(flags + npx, 0, sizeof(uint32_t), s));
     size_t tb = L.cub_bytes;
@@ -631,7 +631,7 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), s));
       ev.record(0, s);
       if (it > 1) {
-        st::k_flag_mstep<<<nblk, EM_BLOCK, 0, s>>>(act_ptr, n_act, static_bits, mask_in, e_act,
+        st::k_flag_mstep<<<nblk, EM_BLOCK, 0, s>>>(act_ptr, n_act, 0, static_bits, mask_in, e_act,
                                                    pe_act, chg, mlist, counts);
         ST_LAUNCH_CHECK("k_flag_mstep");
       }
@@ -724,13 +724,13 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
   // outputs (solver.py:491-500)
   if (dense) {
     st::k_pack_outputs<<<blocks_for(npx, 256), 256, 0, s>>>(
-        f->mu, npx, nullptr, npx, solved ? d_act : nullptr, st_act, values, status, 1);
+        f->mu, npx, 0, nullptr, npx, solved ? d_act : nullptr, st_act, values, status, 1);
     ST_LAUNCH_CHECK("k_pack_outputs");
   } else {
     st::k_fill_mu<<<blocks_for(npx, 256), 256, 0, s>>>(f->mu, npx, values, status);
     ST_LAUNCH_CHECK("k_fill_mu");
     if (solved && n_act > 0) {
-      st::k_pack_outputs<<<blocks_for(n_act, 256), 256, 0, s>>>(f->mu, npx, active, n_act, d_act,
+      st::k_pack_outputs<<<blocks_for(n_act, 256), 256, 0, s>>>(f->mu, npx, 0, active, n_act, d_act,
                                                                 st_act, values, status, 0);
       ST_LAUNCH_CHECK("k_pack_outputs");
     }
@@ -738,32 +738,29 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
   return ST_OK;
 }
 
-// st_solve for a dense solve on one device with no host synchronisation: the
-// convergence test (solver.py:483-485) and the statistics run on the device
-// (k_solve_control), and every kernel of the iterations after convergence
-// exits at once on the device stop flag.  Results are identical to st_solve.
-int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, float* values,
-                   uint8_t* status, uint32_t* static_bits, uint32_t* valid_bits,
-                   st_stats* stats_dev, void* workspace, int64_t workspace_bytes,
-                   void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  st::EmCtx c;
-  int rc = make_ctx(f, rig, p, c);
-  if (rc) return rc;
-  if ((rc = prepare_estep_kernels())) return rc;
-  const int W = c.W, H = c.H;
+// The asynchronous EM driver behind st_solve_async and st_solve_rows.
+// Slots: i -> pixel pix0 + i (dense) or active[i] (a sorted list); slots
+// [cnt_lo, cnt_hi) are this shard's own pixels (the statistics count only
+// them; row bands also solve a halo of neighbour rows for the median).
+struct AsyncSolve {
+  int64_t pix0;
+  const int64_t* active;
+  int64_t n;
+  int64_t cnt_lo, cnt_hi;
+  int64_t init_pix0, init_n;   // initial masks: pixels [init_pix0, init_pix0 + init_n)
+  bool band;                   // per-iteration record exchange + k_band_control
+  st_exchange_fn exchange;     // nullable when world == 1
+  void* user;
+  int world;
+  void* rec_send;
+  void* rec_recv;
+};
+
+static int solve_async_core(const st_frame* f, const st_rig* rig, const st_params* p,
+                            st::EmCtx& c, const AsyncSolve& A, float* values, uint8_t* status,
+                            uint32_t* static_bits, uint32_t* valid_bits, st_stats* stats_dev,
+                            char* ws, const SolveLayout& L, cudaStream_t s) {
   const int64_t npx = c.HW;
-  const SolveLayout L = solve_layout(W, H);
-  if ((int64_t)L.total > workspace_bytes) {
-    sthost::set_error("solve workspace too small (%lld < %lld)", (long long)workspace_bytes,
-                      (long long)L.total);
-    return ST_ENOMEM;
-  }
-  if (!stats_dev) {
-    sthost::set_error("st_solve_async: stats_dev is required");
-    return ST_EINVAL;
-  }
-  char* ws = (char*)workspace;
   double* d_act = (double*)(ws + L.d);
   double* e_act = (double*)(ws + L.e);
   double* pe_act = (double*)(ws + L.pe);
@@ -777,24 +774,30 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
   st::Partial* work = (st::Partial*)(ws + L.work);
   st::Partial* parts = (st::Partial*)(ws + L.parts);
   st::Partial* reduced = (st::Partial*)(ws + L.reduced);
+  const int64_t n = A.n;
+  const int64_t n_cnt = A.cnt_hi - A.cnt_lo;
 
   ST_CUDA_CHECK(cudaMemsetAsync(stats_dev, 0, sizeof(st_stats), s));
   ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t) + sizeof(int), s));
   // E-step fallback count (byte 48) and the stats kernel's block counter (52)
   ST_CUDA_CHECK(cudaMemsetAsync(counts + 12, 0, 4 * sizeof(uint32_t), s));
-  st::k_stats_init<<<1, 32, 0, s>>>(stats_dev, npx);
+  st::k_stats_init<<<1, 32, 0, s>>>(stats_dev, n_cnt);
   ST_LAUNCH_CHECK("k_stats_init");
   double* eps_logs = (double*)(counts + 4);
   st::k_eps_logs<<<1, 32, 0, s>>>(p->epsilon_prior, eps_logs);
   ST_LAUNCH_CHECK("k_eps_logs");
-  st::k_initial_masks<<<blocks_for(npx, 128), 128, 0, s>>>(c, nullptr, npx, static_bits,
-                                                           valid_bits);
-  ST_LAUNCH_CHECK("k_initial_masks");
+  {
+    st::EmCtx ci = c;
+    ci.pix0 = A.init_pix0;
+    st::k_initial_masks<<<blocks_for(A.init_n, 128), 128, 0, s>>>(ci, nullptr, A.init_n,
+                                                                  static_bits, valid_bits);
+    ST_LAUNCH_CHECK("k_initial_masks");
+  }
+  c.pix0 = A.active ? 0 : A.pix0;
 
   const int iters = p->forced_iters > 0 ? p->forced_iters : p->max_iters;
-  const int nblk = (int)blocks_for(npx, EM_BLOCK);
-  const int nwarps = nblk * (EM_BLOCK / 32);
-  const int sblk = std::min((int)blocks_for(npx, STATS_BLOCK), STATS_GRID);
+  const int nblk = std::max(1, (int)blocks_for(n, EM_BLOCK));
+  const int sblk = std::max(1, std::min((int)blocks_for(n_cnt, STATS_BLOCK), STATS_GRID));
   // iterations >= 2 work on device-counted worklists (a fraction of the
   // pixels) and do nothing once converged: a fixed grid of grid-stride
   // blocks (16 per SM measured best: the worklists' items are latency-bound)
@@ -803,11 +806,14 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     return e ? atoi(e) : 16;
   }();
   const int wave2 = std::min(nblk, 148 * wave_env);
-  for (int it = 1; it <= iters; ++it) {
-    // long caps (max_iters > ST_ASYNC_CHUNK): every ST_ASYNC_CHUNK iterations
-    // read the device stop flag back, so a converged solve does not enqueue
-    // max_iters rounds of (immediately exiting) launches
-    if (it > ST_ASYNC_CHUNK && (it - 1) % ST_ASYNC_CHUNK == 0) {
+  // a row band with no active pixel still takes part in every exchange
+  for (int it = 1; it <= iters && (n > 0 || A.band); ++it) {
+    // long caps (max_iters > ST_ASYNC_CHUNK) and row bands: read the device
+    // stop flag back before enqueueing more iterations, so a converged solve
+    // does not enqueue max_iters rounds of (immediately exiting) launches and
+    // exchanges (row bands check every iteration)
+    const int chunk = A.band ? 1 : ST_ASYNC_CHUNK;
+    if (it > chunk && (it - 1) % chunk == 0) {
       int h_stop = 0;
       ST_CUDA_CHECK(cudaMemcpyAsync(&h_stop, stop, sizeof(int), cudaMemcpyDeviceToHost, s));
       ST_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -817,13 +823,15 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     // (~20 %); later iterations have far smaller worklists, or none once
     // converged (the launches then exit at once): a smaller grid
     const int wave = it <= 2 ? wave2 : std::min(nblk, 148 * 4);
+    if (n > 0) {
     if (it > 1) {
-      st::k_flag_mstep<<<wave, EM_BLOCK, 0, s>>>(nullptr, npx, static_bits, mask_in, e_act,
-                                                 pe_act, chg, mlist, counts, stop);
+      st::k_flag_mstep<<<wave, EM_BLOCK, 0, s>>>(A.active, n, c.pix0, static_bits, mask_in,
+                                                 e_act, pe_act, chg, mlist, counts, stop);
       ST_LAUNCH_CHECK("k_flag_mstep");
     }
     st::MStepArgs a = {};
-    a.n = npx;
+    a.active = A.active;
+    a.n = n;
     a.list = it > 1 ? mlist : nullptr;
     a.list_count = counts;
     a.static_all = static_bits;
@@ -841,7 +849,8 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     st::k_m_step<<<it > 1 ? wave : nblk, EM_BLOCK, 0, s>>>(c, a);
     ST_LAUNCH_CHECK("k_m_step");
     st::EStepArgs e = {};
-    e.n = npx;
+    e.pix = A.active;
+    e.n = n;
     e.list = elist;
     e.list_count = counts + 1;
     e.d = d_act;
@@ -854,9 +863,10 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     e.flist_count = (uint32_t*)(eps_logs + 4);
     e.stop = stop;
     launch_e_step(rig->num_views,
-                  it == 1 ? npx : std::min<int64_t>(npx, 148 * (it == 2 ? 8 : 4) * 128), s, c, e,
+                  it == 1 ? n : std::min<int64_t>(n, 148 * (it == 2 ? 8 : 4) * 128), s, c, e,
                   true);
     ST_LAUNCH_CHECK("k_e_step_at");
+    }  // n > 0
     // statistics, their fixed-order reduction and the control in one launch
     // (the last block folds the partials; it also clears the fallback count)
     st::StatsTail tail = {};
@@ -865,20 +875,157 @@ int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, flo
     tail.done = counts + 13;
     tail.reduced = reduced;
     tail.counts = counts;
-    tail.n_act = npx;
+    tail.n_act = n_cnt;
     tail.forced_iters = p->forced_iters;
     tail.stats = stats_dev;
     tail.stop_rw = stop;
-    tail.flist_count = e.flist_count;
-    st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(npx, it > 1, e_act, pe_act, chg, work,
+    tail.flist_count = (uint32_t*)(eps_logs + 4);
+    tail.record_only = A.band ? 1 : 0;
+    tail.record_n_act = n_cnt;
+    tail.record_slots = n;
+    st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(n_cnt, it > 1, e_act + A.cnt_lo,
+                                                pe_act + A.cnt_lo, chg + A.cnt_lo, work,
                                                 (it > 1 ? wave : nblk) * (EM_BLOCK / 32),
                                                 parts, stop, tail);
     ST_LAUNCH_CHECK("k_em_stats");
+    if (A.band) {
+      const st::Partial* recs = reduced + it;
+      if (A.exchange) {
+        ST_CUDA_CHECK(cudaMemcpyAsync(A.rec_send, reduced + it, sizeof(st::Partial),
+                                      cudaMemcpyDeviceToDevice, s));
+        if (A.exchange(s, A.user)) {
+          sthost::set_error("row-band record exchange failed");
+          return ST_EINVAL;
+        }
+        recs = (const st::Partial*)A.rec_recv;
+      }
+      st::k_band_control<<<1, 32, 0, s>>>(it, recs, A.exchange ? A.world : 1, p->forced_iters,
+                                          stats_dev, stop);
+      ST_LAUNCH_CHECK("k_band_control");
+    }
   }
-  st::k_pack_outputs<<<blocks_for(npx, 256), 256, 0, s>>>(f->mu, npx, nullptr, npx, d_act,
+  if (A.active) {
+    st::k_fill_mu<<<blocks_for(A.init_n, 256), 256, 0, s>>>(f->mu + A.init_pix0, A.init_n,
+                                                             values + A.init_pix0,
+                                                             status + A.init_pix0);
+    ST_LAUNCH_CHECK("k_fill_mu");
+    if (n > 0) {
+      st::k_pack_outputs<<<blocks_for(n, 256), 256, 0, s>>>(f->mu, npx, 0, A.active, n, d_act,
+                                                            st_act, values, status, 0);
+      ST_LAUNCH_CHECK("k_pack_outputs");
+    }
+  } else {
+    st::k_pack_outputs<<<blocks_for(n, 256), 256, 0, s>>>(f->mu, n, A.pix0, nullptr, n, d_act,
                                                           st_act, values, status, 1);
-  ST_LAUNCH_CHECK("k_pack_outputs");
+    ST_LAUNCH_CHECK("k_pack_outputs");
+  }
   return ST_OK;
+}
+
+static int solve_prologue(const st_frame* f, const st_rig* rig, const st_params* p,
+                          st::EmCtx& c, int64_t workspace_bytes, SolveLayout& L) {
+  int rc = make_ctx(f, rig, p, c);
+  if (rc) return rc;
+  if ((rc = prepare_estep_kernels())) return rc;
+  L = solve_layout(c.W, c.H);
+  if ((int64_t)L.total > workspace_bytes) {
+    sthost::set_error("solve workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                      (long long)L.total);
+    return ST_ENOMEM;
+  }
+  return ST_OK;
+}
+
+// st_solve for a dense solve on one device with no host synchronisation: the
+// convergence test (solver.py:483-485) and the statistics run on the device
+// (k_solve_control), and every kernel of the iterations after convergence
+// exits at once on the device stop flag.  Results are identical to st_solve.
+int st_solve_async(const st_frame* f, const st_rig* rig, const st_params* p, float* values,
+                   uint8_t* status, uint32_t* static_bits, uint32_t* valid_bits,
+                   st_stats* stats_dev, void* workspace, int64_t workspace_bytes,
+                   void* stream) {
+  st::EmCtx c;
+  SolveLayout L;
+  int rc = solve_prologue(f, rig, p, c, workspace_bytes, L);
+  if (rc) return rc;
+  if (!stats_dev) {
+    sthost::set_error("st_solve_async: stats_dev is required");
+    return ST_EINVAL;
+  }
+  AsyncSolve A = {};
+  A.n = c.HW;
+  A.cnt_hi = c.HW;
+  A.init_n = c.HW;
+  A.world = 1;
+  return solve_async_core(f, rig, p, c, A, values, status, static_bits, valid_bits, stats_dev,
+                          (char*)workspace, L, (cudaStream_t)stream);
+}
+
+int64_t st_band_record_bytes(void) { return (int64_t)sizeof(st::Partial); }
+
+int st_solve_rows(const st_frame* f, const st_rig* rig, const st_params* p,
+                  int32_t dynamic_only, int32_t row0, int32_t row1, int32_t ext0, int32_t ext1,
+                  float* values, uint8_t* status, uint32_t* static_bits, uint32_t* valid_bits,
+                  st_stats* stats_dev, void* workspace, int64_t workspace_bytes,
+                  st_exchange_fn exchange, void* user, int32_t world, void* rec_send,
+                  void* rec_recv, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  st::EmCtx c;
+  SolveLayout L;
+  int rc = solve_prologue(f, rig, p, c, workspace_bytes, L);
+  if (rc) return rc;
+  const int W = c.W, H = c.H;
+  if (!stats_dev || !(0 <= ext0 && ext0 <= row0 && row0 <= row1 && row1 <= ext1 && ext1 <= H) ||
+      world < 1 || (world > 1 && (!exchange || !rec_send || !rec_recv))) {
+    sthost::set_error("st_solve_rows: need 0 <= ext0 <= row0 <= row1 <= ext1 <= H (%d), "
+                      "stats_dev, and an exchange with its buffers when world > 1", H);
+    return ST_EINVAL;
+  }
+  char* ws = (char*)workspace;
+  AsyncSolve A = {};
+  A.band = true;
+  A.exchange = world > 1 || exchange ? exchange : nullptr;
+  A.user = user;
+  A.world = world;
+  A.rec_send = rec_send;
+  A.rec_recv = rec_recv;
+  A.init_pix0 = (int64_t)ext0 * W;
+  A.init_n = (int64_t)(ext1 - ext0) * W;
+  if (!dynamic_only) {
+    A.pix0 = A.init_pix0;
+    A.n = A.init_n;
+    A.cnt_lo = (int64_t)(row0 - ext0) * W;
+    A.cnt_hi = (int64_t)(row1 - ext0) * W;
+  } else {
+    // active = ref prior < threshold inside the solved rows (solver.py:449-452):
+    // one host read-back for the list size and this band's counted slots
+    const int64_t npx = c.HW;
+    uint32_t* flags = (uint32_t*)(ws + L.flags);
+    uint32_t* offs = (uint32_t*)(ws + L.offs);
+    int64_t* active = (int64_t*)(ws + L.active);
+    const float* ref_prior = f->priors + (size_t)rig->ref_index * npx;
+    st::k_flag_active<<<blocks_for(npx, 256), 256, 0, s>>>(ref_prior, nullptr, npx, p->threshold,
+                                                          flags, A.init_pix0,
+                                                          A.init_pix0 + A.init_n);
+    ST_LAUNCH_CHECK("k_flag_active");
+    ST_CUDA_CHECK(cudaMemsetAsync(flags + npx, 0, sizeof(uint32_t), s));
+    size_t tb = L.cub_bytes;
+    ST_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws + L.cub, tb, flags, offs, (int)(npx + 1), s));
+    sthost::count_launch();
+    st::k_scatter_active<<<blocks_for(npx, 256), 256, 0, s>>>(flags, offs, npx, active);
+    ST_LAUNCH_CHECK("k_scatter_active");
+    uint32_t h[3] = {0, 0, 0};
+    ST_CUDA_CHECK(cudaMemcpyAsync(&h[0], offs + npx, 4, cudaMemcpyDeviceToHost, s));
+    ST_CUDA_CHECK(cudaMemcpyAsync(&h[1], offs + (int64_t)row0 * W, 4, cudaMemcpyDeviceToHost, s));
+    ST_CUDA_CHECK(cudaMemcpyAsync(&h[2], offs + (int64_t)row1 * W, 4, cudaMemcpyDeviceToHost, s));
+    ST_CUDA_CHECK(cudaStreamSynchronize(s));
+    A.active = active;
+    A.n = h[0];
+    A.cnt_lo = h[1];
+    A.cnt_hi = h[2];
+  }
+  return solve_async_core(f, rig, p, c, A, values, status, static_bits, valid_bits, stats_dev,
+                          ws, L, s);
 }
 
 }  // extern "C"

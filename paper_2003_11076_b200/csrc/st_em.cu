@@ -345,7 +345,7 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
   bool want_e = false;
 
   if (live) {
-    const int64_t pix = a.active ? a.active[i] : i;
+    const int64_t pix = a.active ? a.active[i] : c.pix0 + i;
     const int x = (int)(pix % c.W), y = (int)(pix / c.W);
     const double u = (double)x, v = (double)y;
     const double mu = c.mu[pix];
@@ -467,7 +467,7 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
 // Iteration >= 2: which slots need a new M-step (mask changed since their
 // last one).  The others carry their previous-disparity energy (= their E)
 // and changed = 0 into the statistics.
-__global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n,
+__global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n, int64_t pix0,
                              const uint32_t* __restrict__ static_all,
                              const uint32_t* __restrict__ mask_in, const double* __restrict__ e,
                              double* __restrict__ pe, uint8_t* __restrict__ chg,
@@ -479,7 +479,7 @@ __global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n,
     const int64_t i = base + threadIdx.x;
     bool want = false;
     if (i < n) {
-      const int64_t pix = active ? active[i] : i;
+      const int64_t pix = active ? active[i] : pix0 + i;
       want = static_all[pix] != mask_in[i];
       if (!want) {
         pe[i] = e[i];
@@ -586,6 +586,18 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ 
   __threadfence();
   reduce_partials_block(parts, gridDim.x, tail.reduced + tail.it);
   __syncthreads();
+  if (threadIdx.x == 0 && tail.record_only) {
+    __threadfence();
+    *tail.done = 0u;
+    Partial* rec = tail.reduced + tail.it;
+    rec->n_act = tail.record_n_act;
+    rec->n_mwork = tail.it > 1 ? (long long)tail.counts[0] : tail.record_slots;
+    rec->n_ework = (long long)tail.counts[1];
+    tail.counts[0] = 0;  // next iteration's worklists
+    tail.counts[1] = 0;
+    if (tail.flist_count) *tail.flist_count = 0u;
+    return;
+  }
   if (threadIdx.x == 0) {
     __threadfence();
     *tail.done = 0u;
@@ -1146,7 +1158,7 @@ __global__ void __launch_bounds__(ESTEP_TAPS_BLOCK, ESTEP_MIN_BLOCKS) k_e_step_t
        t += (int64_t)gridDim.x * blockDim.x) {
   const int64_t i = a.list ? (int64_t)a.list[t] : t;
   if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) continue;  // solver.py:476-478
-  const int64_t pix = a.pix ? a.pix[i] : i;
+  const int64_t pix = a.pix ? a.pix[i] : c.pix0 + i;
   const double u = (double)(pix % c.W), v = (double)(pix / c.W);
   const double d = a.d[i];
   int idx[KT];
@@ -1238,7 +1250,7 @@ __global__ void __launch_bounds__(ESTEP_CERT_BLOCK, ESTEP_CERT_MIN_BLOCKS)
     if (t < n_work) {
       i = a.list ? (int64_t)a.list[t] : t;
       if (!(a.status && a.status[i] == ST_STATUS_LOW_TEXTURE)) {  // solver.py:476-478
-        const int64_t pix = a.pix ? a.pix[i] : i;
+        const int64_t pix = a.pix ? a.pix[i] : c.pix0 + i;
         const double u = (double)(pix % c.W), v = (double)(pix / c.W);
         const double d = a.d[i];
         int idx[KT];
@@ -1387,7 +1399,7 @@ __global__ void __launch_bounds__(CERT_BIG_BLOCK, 4) k_e_step_cert_big(EmCtx c, 
     if (t < n_work) {
       i = a.list ? (int64_t)a.list[t] : t;
       if (!(a.status && a.status[i] == ST_STATUS_LOW_TEXTURE)) {  // solver.py:476-478
-        const int64_t pix = a.pix ? a.pix[i] : i;
+        const int64_t pix = a.pix ? a.pix[i] : c.pix0 + i;
         const double u = (double)(pix % c.W), v = (double)(pix / c.W);
         const double d = a.d[i];
         int idx[ST_MAX_VIEWS];
@@ -1556,7 +1568,7 @@ __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a)
        t += (int64_t)gridDim.x * blockDim.x) {
   const int64_t i = a.list ? (int64_t)a.list[t] : t;
   if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) continue;  // solver.py:476-478
-  const int64_t pix = a.pix ? a.pix[i] : i;
+  const int64_t pix = a.pix ? a.pix[i] : c.pix0 + i;
   const double u = (double)(pix % c.W), v = (double)(pix / c.W);
   const double d = a.d[i];
   double* f = sh_f + threadIdx.x;
@@ -1594,7 +1606,7 @@ __global__ void k_initial_masks(EmCtx c, const int64_t* __restrict__ pix_list, i
                                 uint32_t* __restrict__ valid_out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int64_t pix = pix_list ? pix_list[i] : i;
+  const int64_t pix = pix_list ? pix_list[i] : c.pix0 + i;
   const double u = (double)(pix % c.W), v = (double)(pix / c.W);
   const double d = c.mu[pix];
   uint32_t sb = 0, vb = 0;
@@ -1722,7 +1734,8 @@ __global__ void k_masked_variance(const double* __restrict__ desc, const uint8_t
 }
 
 // solve() output packing (solver.py:491-500).
-__global__ void k_pack_outputs(const double* __restrict__ mu, int64_t npx,
+// dense: slots 0..npx-1 are pixels pix0 + i.
+__global__ void k_pack_outputs(const double* __restrict__ mu, int64_t npx, int64_t pix0,
                                const int64_t* __restrict__ active, int64_t n_active,
                                const double* __restrict__ d_act,
                                const uint8_t* __restrict__ st_act, float* __restrict__ values,
@@ -1730,13 +1743,14 @@ __global__ void k_pack_outputs(const double* __restrict__ mu, int64_t npx,
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (dense) {
     if (i >= npx) return;
+    const int64_t p = pix0 + i;
     if (d_act) {
       const double d = d_act[i];
-      values[i] = isnan(d) ? 0.0f : (float)d;
-      status[i] = st_act[i];
+      values[p] = isnan(d) ? 0.0f : (float)d;
+      status[p] = st_act[i];
     } else {
-      values[i] = (float)mu[i];
-      status[i] = ST_STATUS_VALID;
+      values[p] = (float)mu[p];
+      status[p] = ST_STATUS_VALID;
     }
     return;
   }
@@ -1798,7 +1812,7 @@ __device__ void reduce_partials_block(const Partial* __restrict__ parts, int npa
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    Partial r;
+    Partial r = {};
     r.sum_e = sd[0][0];
     r.sum_pe = sd[1][0];
     r.n_fin = si[0][0];
@@ -1821,11 +1835,14 @@ __global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
 // dynamic_only / explicit active-set compaction: count then scatter, in
 // pixel order (the reference's `active` is ascending).
 __global__ void k_flag_active(const float* __restrict__ ref_prior, const uint8_t* __restrict__ mask,
-                              int64_t npx, double threshold, uint32_t* __restrict__ flags) {
+                              int64_t npx, double threshold, uint32_t* __restrict__ flags,
+                              int64_t lo, int64_t hi) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npx) return;
-  // numpy compares the float32 prior against the Python float in float32 (NEP 50)
-  flags[i] = mask ? (mask[i] ? 1u : 0u) : (ref_prior[i] < (float)threshold ? 1u : 0u);
+  // numpy compares the float32 prior against the Python float in float32 (NEP 50);
+  // [lo, hi): the pixel window of a row band (the whole frame otherwise)
+  const bool on = mask ? mask[i] != 0 : ref_prior[i] < (float)threshold;
+  flags[i] = (on && i >= lo && i < hi) ? 1u : 0u;
 }
 
 __global__ void k_scatter_active(const uint32_t* __restrict__ flags,
@@ -1844,15 +1861,15 @@ __global__ void k_stats_init(st_stats* stats, int64_t n_act) {
   }
 }
 
-// Device-side EM control (solver.py:463-485): one thread.
-__device__ void solve_control(int it, const Partial* __restrict__ reduced,
-                              uint32_t* __restrict__ counts, int64_t n_act, int forced_iters,
-                              st_stats* __restrict__ stats, int* __restrict__ stop) {
-  const Partial r = reduced[it];
+// Device-side EM control (solver.py:463-485): one thread.  `r` is the
+// iteration's (all-shard) record, n_act the (global) active count.
+__device__ void control_step(int it, const Partial& r, int64_t n_act, long long mwork,
+                             long long ework, int forced_iters, st_stats* __restrict__ stats,
+                             int* __restrict__ stop) {
   stats->iterations_run = it;
-  stats->msteps += it > 1 ? (int64_t)counts[0] : n_act;
-  stats->esteps += counts[1];
-  if (it > 1) stats->prev_evals += counts[0];
+  stats->msteps += mwork;
+  stats->esteps += ework;
+  if (it > 1) stats->prev_evals += mwork;
   stats->kernel_launches[0] += 1;
   stats->kernel_launches[1] += 1;
   stats->kernel_launches[3] += it > 1 ? 3 : 2;
@@ -1872,8 +1889,45 @@ __device__ void solve_control(int it, const Partial* __restrict__ reduced,
       *stop = 1;
     }
   }
+}
+
+__device__ void solve_control(int it, const Partial* __restrict__ reduced,
+                              uint32_t* __restrict__ counts, int64_t n_act, int forced_iters,
+                              st_stats* __restrict__ stats, int* __restrict__ stop) {
+  const Partial r = reduced[it];
+  control_step(it, r, n_act, it > 1 ? (long long)counts[0] : (long long)n_act,
+               (long long)counts[1], forced_iters, stats, stop);
   counts[0] = 0;  // next iteration's worklists
   counts[1] = 0;
+}
+
+__global__ void k_band_control(int it, const Partial* __restrict__ gathered, int world,
+                               int forced_iters, st_stats* __restrict__ stats,
+                               int* __restrict__ stop) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || *stop) return;
+  Partial r = gathered[0];
+  for (int w = 1; w < world; ++w) {  // rank order: identical on every shard
+    const Partial& g = gathered[w];
+    r.sum_e += g.sum_e;
+    r.sum_pe += g.sum_pe;
+    r.n_fin += g.n_fin;
+    r.n_pfin += g.n_pfin;
+    r.n_changed += g.n_changed;
+    r.n_cand += g.n_cand;
+    r.n_eval += g.n_eval;
+    r.n_hopeless += g.n_hopeless;
+    r.n_samples += g.n_samples;
+    r.n_act += g.n_act;
+    r.n_mwork += g.n_mwork;
+    r.n_ework += g.n_ework;
+  }
+  if (it == 1) stats->active_pixels = r.n_act;
+  if (r.n_act == 0) {  // solver.py:486-488: no active pixel anywhere
+    stats->converged_after = 0;
+    *stop = 1;
+    return;
+  }
+  control_step(it, r, r.n_act, r.n_mwork, r.n_ework, forced_iters, stats, stop);
 }
 
 __global__ void k_solve_control(int it, const Partial* __restrict__ reduced,

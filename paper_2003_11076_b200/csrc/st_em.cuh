@@ -58,6 +58,7 @@ struct EmCtx {
   double recip[ST_MAX_VIEWS + 1];  // RN(1/n), n = 1..12, for div_small
   uint32_t view_bits;   // (1 << K) - 1
   int exhaustive;       // M-step: no pruning, every candidate evaluated (cross-check)
+  int64_t pix0;         // dense slots: slot i -> pixel pix0 + i (row bands; 0 otherwise)
 };
 
 struct Partial {
@@ -65,6 +66,9 @@ struct Partial {
   long long n_fin, n_pfin, n_changed, n_cand, n_eval;
   long long n_hopeless;  // M-step pixels with fewer static views than min_static_rays
   long long n_samples;   // M-step descriptor samples (static in-margin rays of real candidates)
+  // row-band record (st_solve_rows): the shard's counted active pixels and its
+  // M/E worklist sizes, summed over shards by k_band_control
+  long long n_act, n_mwork, n_ework;
 };
 
 // Slots are the rows of the active set (slot i -> pixel active[i], or i when
@@ -106,7 +110,8 @@ struct EStepArgs {
 };
 
 __global__ void k_m_step(EmCtx c, MStepArgs a);
-__global__ void k_flag_mstep(const int64_t* active, int64_t n, const uint32_t* static_all,
+__global__ void k_flag_mstep(const int64_t* active, int64_t n, int64_t pix0,
+                             const uint32_t* static_all,
                              const uint32_t* mask_in, const double* e, double* pe, uint8_t* chg,
                              int32_t* list, uint32_t* count, const int* stop = nullptr);
 // st_solve_async: k_em_stats' last block also reduces the partials and runs
@@ -122,6 +127,12 @@ struct StatsTail {
   st_stats* stats;
   int* stop_rw;
   uint32_t* flist_count;   // nullable: the E-step fallback count, cleared for the next E-step
+  // row bands: the last block only writes this shard's record into
+  // reduced[it] (+ n_act = record_n_act, the worklist sizes) and clears the
+  // worklist counts; k_band_control runs the control after the exchange
+  int record_only;
+  long long record_n_act;
+  long long record_slots;  // iteration 1's M-step count (every slot)
 };
 __global__ void k_em_stats(int64_t n, int with_prev, const double* e, const double* pe,
                            const uint8_t* chg, const Partial* work, int n_work_parts,
@@ -143,7 +154,7 @@ __global__ void k_e_step_rays(const double* desc, const uint8_t* valid, const do
                               int64_t n, int K, st_params p, uint32_t* out);
 __global__ void k_masked_variance(const double* desc, const uint8_t* mask, int64_t n, int K,
                                   double* out);
-__global__ void k_pack_outputs(const double* mu, int64_t npx, const int64_t* active,
+__global__ void k_pack_outputs(const double* mu, int64_t npx, int64_t pix0, const int64_t* active,
                                int64_t n_active, const double* d_act, const uint8_t* st_act,
                                float* values, uint8_t* status, int dense);
 __global__ void k_fill_mu(const double* mu, int64_t npx, float* values, uint8_t* status);
@@ -155,11 +166,15 @@ __global__ void k_reduce_partials(const Partial* parts, int nparts, Partial* out
 __global__ void k_solve_control(int it, const Partial* reduced, uint32_t* counts, int64_t n_act,
                                 int forced_iters, st_stats* stats, int* stop);
 __global__ void k_stats_init(st_stats* stats, int64_t n_act);
+// Row bands: sum the shards' records (rank order, deterministic) and run the
+// iteration's control exactly as k_solve_control does for one device.
+__global__ void k_band_control(int it, const Partial* gathered, int world, int forced_iters,
+                               st_stats* stats, int* stop);
 // log(eps), log(1 - eps), log(1 - (1 - eps)) with the device log: the E-step
 // reuses them for rays whose prior is clamped (identical values).
 __global__ void k_eps_logs(double eps, double* out);
 __global__ void k_flag_active(const float* ref_prior, const uint8_t* mask, int64_t npx,
-                              double threshold, uint32_t* flags);
+                              double threshold, uint32_t* flags, int64_t lo, int64_t hi);
 __global__ void k_scatter_active(const uint32_t* flags, const uint32_t* offs, int64_t npx,
                                  int64_t* active);
 

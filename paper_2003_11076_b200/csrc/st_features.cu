@@ -125,14 +125,16 @@ __global__ void __launch_bounds__(256) k_descriptors_wide(const uint8_t* __restr
                                                           int H, int W, size_t total_bytes,
                                                           uint4* __restrict__ desc,
                                                           uint8_t* __restrict__ gray_out,
-                                                          uint8_t* __restrict__ sobel_out) {
+                                                          uint8_t* __restrict__ sobel_out,
+                                                          int row0, int row1) {
   __shared__ __align__(16) uint8_t raw[DW_H + 6][DW_ROWB];
   __shared__ int16_t g[DW_H + 6][DW_W + 6];
   __shared__ uint16_t sxy[DW_H + 4][DW_W + 4];  // gx | gy << 8; 0x8080 off-image
   __shared__ int roff[DW_H + 6];  // byte of pixel 0 of the row, relative to the staged start
   const int k = blockIdx.z;
   const size_t view = (size_t)k * H * W * 3;
-  const int x0 = blockIdx.x * DW_W, y0 = blockIdx.y * DW_H;
+  // rows [row0, row1) only (row bands; the whole frame otherwise)
+  const int x0 = blockIdx.x * DW_W, y0 = row0 + blockIdx.y * DW_H;
   const int tid = threadIdx.x;
   const int cl0 = max(x0 - 3, 0), cl1 = min(x0 + DW_W + 3, W);  // clamped column range
   const uintptr_t buf0 = (uintptr_t)images, buf1 = buf0 + total_bytes;
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(256) k_descriptors_wide(const uint8_t* __restr
   for (int e = 0; e < 8; ++e) {
     const int ty = e * 2 + (tid >> 7), tx = tid & 127;
     const int x = x0 + tx, y = y0 + ty;
-    if (x >= W || y >= H) continue;
+    if (x >= W || y >= row1) continue;
     // descriptor bytes 2i, 2i+1 = (gx, gy) at ring offset i: halfword i
     uint32_t w[4];
 #pragma unroll
@@ -214,7 +216,7 @@ extern "C" int st_descriptors(const uint8_t* images, int32_t K, int32_t H, int32
     dim3 grid((W + DW_W - 1) / DW_W, (H + DW_H - 1) / DW_H, K);
     st::k_descriptors_wide<<<grid, 256, 0, (cudaStream_t)stream>>>(
         images, H, W, (size_t)K * H * W * 3, reinterpret_cast<uint4*>(desc_out), gray_out,
-        sobel_out);
+        sobel_out, 0, H);
     ST_LAUNCH_CHECK("k_descriptors_wide");
     return ST_OK;
   }
@@ -223,5 +225,27 @@ extern "C" int st_descriptors(const uint8_t* images, int32_t K, int32_t H, int32
   st::k_descriptors<<<grid, block, 0, (cudaStream_t)stream>>>(
       images, H, W, channels, reinterpret_cast<uint4*>(desc_out), gray_out, sobel_out);
   ST_LAUNCH_CHECK("k_descriptors");
+  return ST_OK;
+}
+
+extern "C" int st_descriptors_rows(const uint8_t* images, int32_t K, int32_t H, int32_t W,
+                                   uint8_t* desc_out, int32_t row0, int32_t row1,
+                                   void* stream) {
+  row0 = max(row0, 0);
+  row1 = min(row1, H);
+  if (K < 1 || H < 1 || W < 1 || row0 > row1) {
+    sthost::set_error("bad descriptor rows [%d, %d) of %d x %d x %d", row0, row1, K, H, W);
+    return ST_EINVAL;
+  }
+  if (((uintptr_t)images & 3) != 0) {
+    sthost::set_error("st_descriptors_rows needs 4-byte aligned RGB views");
+    return ST_EINVAL;
+  }
+  if (row0 == row1) return ST_OK;
+  dim3 grid((W + DW_W - 1) / DW_W, (row1 - row0 + DW_H - 1) / DW_H, K);
+  st::k_descriptors_wide<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      images, H, W, (size_t)K * H * W * 3, reinterpret_cast<uint4*>(desc_out), nullptr, nullptr,
+      row0, row1);
+  ST_LAUNCH_CHECK("k_descriptors_wide");
   return ST_OK;
 }

@@ -8,6 +8,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "st_common.cuh"
 
 namespace st {
@@ -79,9 +81,10 @@ __global__ void k_refocus(const uint8_t* __restrict__ images, st_rig rig, int W,
                           const uint32_t* __restrict__ static_bits, int min_static_rays,
                           const uint8_t* __restrict__ copy_mask, uint8_t* __restrict__ out,
                           uint8_t* __restrict__ prov, uint8_t* __restrict__ n_rays,
-                          int rectified) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= (int64_t)W * H) return;
+                          int rectified, int64_t p0, int64_t p1) {
+  // pixels [p0, p1) (a row band's rows; the whole frame otherwise)
+  const int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= p1) return;
   const uint8_t* ref = images + (size_t)rig.ref_index * W * H * 3 + (size_t)p * 3;
   uint8_t c0 = ref[0], c1 = ref[1], c2 = ref[2];
   const bool copied = copy_mask && copy_mask[p];
@@ -153,9 +156,10 @@ __device__ __forceinline__ int kth_smallest(const uint8_t* __restrict__ img, int
 }
 
 __global__ void k_median_small(const uint8_t* __restrict__ src, int H, int W, int C, int radius,
-                               const uint8_t* __restrict__ prov, uint8_t* __restrict__ out) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= (int64_t)W * H) return;
+                               const uint8_t* __restrict__ prov, uint8_t* __restrict__ out,
+                               int64_t p0, int64_t p1) {
+  const int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= p1) return;
   const int x = (int)(p % W), y = (int)(p / W);
   if (prov && prov[p] == ST_PROV_COPIED) {
     for (int ch = 0; ch < C; ++ch) out[(size_t)p * C + ch] = src[(size_t)p * C + ch];
@@ -239,9 +243,10 @@ __device__ __forceinline__ void med9(int (&v)[9]) {
 
 __global__ void __launch_bounds__(MT_W * MT_H) k_median_rgb_tile(
     const uint8_t* __restrict__ src, int H, int W, const uint8_t* __restrict__ prov,
-    uint8_t* __restrict__ out) {
+    uint8_t* __restrict__ out, int row0, int row1) {
+  // output rows [row0, row1); the staged halo rows must hold refocused pixels
   __shared__ uint8_t tile[MT_H + 2][(MT_W + 2) * 3 + 2];
-  const int x0 = blockIdx.x * MT_W, y0 = blockIdx.y * MT_H;
+  const int x0 = blockIdx.x * MT_W, y0 = row0 + blockIdx.y * MT_H;
   const int tid = threadIdx.y * MT_W + threadIdx.x;
   for (int i = tid; i < (MT_H + 2) * (MT_W + 2) * 3; i += MT_W * MT_H) {
     const int r = i / ((MT_W + 2) * 3), cb = i % ((MT_W + 2) * 3);
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(MT_W * MT_H) k_median_rgb_tile(
   }
   __syncthreads();
   const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
-  if (x >= W || y >= H) return;
+  if (x >= W || y >= row1) return;
   const size_t p = (size_t)y * W + x;
   if (prov && prov[p] == ST_PROV_COPIED) {
 #pragma unroll
@@ -303,20 +308,19 @@ extern "C" int st_median(const uint8_t* image, int32_t H, int32_t W, int32_t C, 
     return ST_OK;
   }
   st::k_median_small<<<(unsigned)((npx + 255) / 256), 256, 0, s>>>(image, H, W, C, radius,
-                                                                   nullptr, out);
+                                                                   nullptr, out, 0, npx);
   ST_LAUNCH_CHECK("k_median_small");
   return ST_OK;
 }
 
-extern "C" int st_synthesize(const uint8_t* images, const st_rig* rig, const float* values,
-                             const uint8_t* status, const uint32_t* static_bits,
-                             int32_t min_static_rays, int32_t median_radius,
-                             const uint8_t* copy_mask, uint8_t* image_out, uint8_t* prov_out,
-                             uint8_t* n_rays_out, uint8_t* scratch, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+static int synthesize_rows(const uint8_t* images, const st_rig* rig, const float* values,
+                           const uint8_t* status, const uint32_t* static_bits,
+                           int32_t min_static_rays, int32_t median_radius,
+                           const uint8_t* copy_mask, uint8_t* image_out, uint8_t* prov_out,
+                           uint8_t* n_rays_out, uint8_t* scratch, int row0, int row1, int ext0,
+                           int ext1, cudaStream_t s) {
   const int W = rig->width, H = rig->height;
-  const int64_t npx = (int64_t)W * H;
-  const unsigned blocks = (unsigned)((npx + 127) / 128);
+  const int64_t e0 = (int64_t)ext0 * W, e1 = (int64_t)ext1 * W;
   uint8_t* stage = median_radius > 0 ? scratch : image_out;
   int rectified = 1;
   for (int k = 0; k < rig->num_views; ++k) {
@@ -327,20 +331,56 @@ extern "C" int st_synthesize(const uint8_t* images, const st_rig* rig, const flo
           b[2] == 0.0 && fabs(b[0]) < 1e300))
       rectified = 0;
   }
-  st::k_refocus<<<blocks, 128, 0, s>>>(images, *rig, W, H, values, status, static_bits,
-                                       min_static_rays, copy_mask, stage, prov_out, n_rays_out,
-                                       rectified);
-  ST_LAUNCH_CHECK("k_refocus");
+  if (e1 > e0) {
+    st::k_refocus<<<(unsigned)((e1 - e0 + 127) / 128), 128, 0, s>>>(
+        images, *rig, W, H, values, status, static_bits, min_static_rays, copy_mask, stage,
+        prov_out, n_rays_out, rectified, e0, e1);
+    ST_LAUNCH_CHECK("k_refocus");
+  }
+  if (median_radius <= 0 || row1 <= row0) return ST_OK;
   if (median_radius == 1) {
-    dim3 grid((W + MT_W - 1) / MT_W, (H + MT_H - 1) / MT_H);
-    st::k_median_rgb_tile<<<grid, dim3(MT_W, MT_H), 0, s>>>(scratch, H, W, prov_out, image_out);
+    dim3 grid((W + MT_W - 1) / MT_W, (row1 - row0 + MT_H - 1) / MT_H);
+    st::k_median_rgb_tile<<<grid, dim3(MT_W, MT_H), 0, s>>>(scratch, H, W, prov_out, image_out,
+                                                            row0, row1);
     ST_LAUNCH_CHECK("k_median_rgb_tile");
-  } else if (median_radius > 0) {
-    st::k_median_small<<<(unsigned)((npx + 255) / 256), 256, 0, s>>>(
-        scratch, H, W, 3, median_radius, prov_out, image_out);
+  } else {
+    const int64_t p0 = (int64_t)row0 * W, p1 = (int64_t)row1 * W;
+    st::k_median_small<<<(unsigned)((p1 - p0 + 255) / 256), 256, 0, s>>>(
+        scratch, H, W, 3, median_radius, prov_out, image_out, p0, p1);
     ST_LAUNCH_CHECK("k_median_small");
   }
   return ST_OK;
+}
+
+extern "C" int st_synthesize(const uint8_t* images, const st_rig* rig, const float* values,
+                             const uint8_t* status, const uint32_t* static_bits,
+                             int32_t min_static_rays, int32_t median_radius,
+                             const uint8_t* copy_mask, uint8_t* image_out, uint8_t* prov_out,
+                             uint8_t* n_rays_out, uint8_t* scratch, void* stream) {
+  return synthesize_rows(images, rig, values, status, static_bits, min_static_rays,
+                         median_radius, copy_mask, image_out, prov_out, n_rays_out, scratch, 0,
+                         rig->height, 0, rig->height, (cudaStream_t)stream);
+}
+
+extern "C" int st_synthesize_rows(const uint8_t* images, const st_rig* rig, const float* values,
+                                  const uint8_t* status, const uint32_t* static_bits,
+                                  int32_t min_static_rays, int32_t median_radius,
+                                  const uint8_t* copy_mask, uint8_t* image_out,
+                                  uint8_t* prov_out, uint8_t* n_rays_out, uint8_t* scratch,
+                                  int32_t row0, int32_t row1, int32_t ext0, int32_t ext1,
+                                  void* stream) {
+  const int H = rig->height;
+  const int r = median_radius > 0 ? median_radius : 0;
+  if (!(0 <= ext0 && ext0 <= row0 && row0 <= row1 && row1 <= ext1 && ext1 <= H) ||
+      ext0 > std::max(row0 - r, 0) || ext1 < std::min(row1 + r, H)) {
+    sthost::set_error("st_synthesize_rows: rows [%d, %d) need the refocused rows [%d, %d) "
+                      "(got [%d, %d))", row0, row1, std::max(row0 - r, 0),
+                      std::min(row1 + r, H), ext0, ext1);
+    return ST_EINVAL;
+  }
+  return synthesize_rows(images, rig, values, status, static_bits, min_static_rays,
+                         median_radius, copy_mask, image_out, prov_out, n_rays_out, scratch,
+                         row0, row1, ext0, ext1, (cudaStream_t)stream);
 }
 
 extern "C" int st_refocus_pixels(const uint8_t* images, const st_rig* rig, const int64_t* pix,
