@@ -370,6 +370,11 @@ int st_refocus_pixels(const uint8_t* images, const st_rig* rig, const int64_t* p
                       const double* d, const uint32_t* bits, int64_t n, int32_t min_static_rays,
                       uint8_t* rgb, int32_t* count, uint8_t* prov, double* totals, void* stream);
 
+/* pipeline.py:254-255 (dynamic_only): copy_mask = ref prior >= threshold,
+ * compared in float32 like numpy; out (n) u8. */
+int st_copy_mask(const float* ref_prior, int64_t n, double threshold, uint8_t* out,
+                 void* stream);
+
 /* refocus.py:68-106 median_filter on an (H,W,C) uint8 image. */
 int st_median(const uint8_t* image, int32_t H, int32_t W, int32_t C, int32_t radius,
               uint8_t* out, void* stream);

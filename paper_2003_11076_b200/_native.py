@@ -148,6 +148,7 @@ _SIGS = {
                                 _P, _P]),
     "st_refocus_pixels": (C.c_int, [_P, C.POINTER(StRig), _P, _P, _P, _I64, _I32, _P, _P, _P,
                                     _P, _P]),
+    "st_copy_mask": (C.c_int, [_P, _I64, _D, _P, _P]),
     "st_median": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P]),
 }
 

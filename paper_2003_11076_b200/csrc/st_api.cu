@@ -812,7 +812,7 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     // stop flag back before enqueueing more iterations, so a converged solve
     // does not enqueue max_iters rounds of (immediately exiting) launches and
     // exchanges (row bands check every iteration)
-    const int chunk = A.band ? 1 : ST_ASYNC_CHUNK;
+    const int chunk = A.band && A.exchange ? 1 : ST_ASYNC_CHUNK;
     if (it > chunk && (it - 1) % chunk == 0) {
       int h_stop = 0;
       ST_CUDA_CHECK(cudaMemcpyAsync(&h_stop, stop, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -383,6 +383,24 @@ extern "C" int st_synthesize_rows(const uint8_t* images, const st_rig* rig, cons
                          row0, row1, ext0, ext1, (cudaStream_t)stream);
 }
 
+namespace st {
+// pipeline.py:254-255: copy_mask = ref prior >= threshold (float32 compare, NEP 50)
+__global__ void k_copy_mask(const float* __restrict__ prior, int64_t n, float thr,
+                            uint8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = prior[i] >= thr ? 1 : 0;
+}
+}  // namespace st
+
+extern "C" int st_copy_mask(const float* ref_prior, int64_t n, double threshold, uint8_t* out,
+                            void* stream) {
+  if (n <= 0) return ST_OK;
+  st::k_copy_mask<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      ref_prior, n, (float)threshold, out);
+  ST_LAUNCH_CHECK("k_copy_mask");
+  return ST_OK;
+}
+
 extern "C" int st_refocus_pixels(const uint8_t* images, const st_rig* rig, const int64_t* pix,
                                  const double* d, const uint32_t* bits, int64_t n,
                                  int32_t min_static_rays, uint8_t* rgb, int32_t* count,

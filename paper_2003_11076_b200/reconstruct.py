@@ -183,7 +183,9 @@ class FramePipeline:
         if self.sup_ws.numel() < need:
             self.sup_ws = empty((need,), t.uint8)
         # no host round trip unless a diagnostic path wants the record count
+        # (dynamic_only: st_solve_rows reads the active-list size back once)
         run_async = not dynamic_only and reduce is None and not timing
+        run_rows = bool(dynamic_only) and reduce is None and not timing
         rec = N.C.c_int64(-1)
         with t.cuda.stream(self.side2):
             self.side2.wait_event(ready)
@@ -192,7 +194,8 @@ class FramePipeline:
             else:
                 N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
             N.invoke("st_support_build", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W, H, p,
-                     self.frame, self.sup_ws, self.sup_ws.numel(), None if run_async else rec)
+                     self.frame, self.sup_ws, self.sup_ws.numel(),
+                     None if (run_async or run_rows) else rec)
             pre_done = self._event(timing=False)
         self._desc_ready = False
         main.wait_event(pre_done)
@@ -204,6 +207,12 @@ class FramePipeline:
             N.invoke("st_solve_async", self.frame, self.rig, p, self.values, self.status,
                      self.sbits, self.vbits, self.stats_dev, self.solve_ws,
                      self.solve_ws.numel())
+        elif run_rows:
+            N.check(N.lib().st_solve_rows(
+                self.frame, self.rig, p, 1, 0, H, 0, H, N.ptr(self.values), N.ptr(self.status),
+                N.ptr(self.sbits), N.ptr(self.vbits), N.ptr(self.stats_dev),
+                N.ptr(self.solve_ws), self.solve_ws.numel(), N.EXCHANGE_FN(), None, 1, None,
+                None, N.stream_handle()))
         else:
             cb = N.REDUCE_FN(reduce) if reduce is not None else N.REDUCE_FN()
             N.invoke("st_solve", self.frame, self.rig, p, int(bool(dynamic_only)), None,
@@ -214,14 +223,14 @@ class FramePipeline:
         copy = None
         if dynamic_only:
             # pipeline.py:254-255: copy_mask = ref prior >= threshold (float32 compare)
-            thr = self.t.tensor(np.float32(self.params.threshold), device=self.priors.device)
-            self.copy.copy_(self.priors[self.rig_obj.ref_index] >= thr)
+            N.invoke("st_copy_mask", self.priors[self.rig.ref_index], H * W,
+                     float(self.params.threshold), self.copy)
             copy = self.copy
         N.invoke("st_synthesize", self.images, self.rig, self.values, self.status, self.sbits,
                  int(self.params.min_static_rays), int(median_radius), copy, self.image,
                  self.prov, self.n_rays, self.scratch)
         mark()
-        if run_async:
+        if run_async or run_rows:
             return AsyncStats(rec.value)
         out = _stats_of(stats)
         if timing:

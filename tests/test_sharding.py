@@ -1,5 +1,6 @@
-"""Row-band sharding host logic across 2 processes (gloo, CPU): band split,
-the st_solve reduce callback, and band gathering."""
+"""Row-band sharding (sharding.py): band split and halos, the per-iteration
+record exchange and the band gather across 2-3 processes (gloo, CPU), and on
+the GPU the banded reconstruction against the single-device one."""
 
 import os
 import socket
@@ -30,52 +31,155 @@ def _free_port():
     return port
 
 
+def test_band_extents_cover_the_frame_with_halos():
+    from paper_2003_11076_b200.sharding import DESC_HALO, band_extents
+    for h in (5, 120, 1080):
+        for world in (1, 2, 3, 8):
+            for mr in (0, 1, 2):
+                own = []
+                for r in range(world):
+                    e = band_extents(h, world, r, mr, rectified=True)
+                    r0, r1 = e["rows"]
+                    own.append((r0, r1))
+                    e0, e1 = e["solve"]
+                    assert e0 == max(0, r0 - mr) and e1 == min(h, r1 + mr)
+                    d0, d1 = e["desc"]
+                    assert d0 <= e0 and d1 >= e1
+                    i0, i1 = e["images"]
+                    assert i0 == max(0, d0 - DESC_HALO) and i1 == min(h, d1 + DESC_HALO)
+                    assert e["priors"] == e["desc"]
+                    g = band_extents(h, world, r, mr, rectified=False)
+                    assert g["images"] == (0, h) and g["priors"] == (0, h)
+                assert own[0][0] == 0 and own[-1][1] == h
+                assert all(a[1] == b[0] for a, b in zip(own, own[1:]))
+
+
 def _worker(rank, world, port, q):
-    import ctypes
+    import torch
     import torch.distributed as dist
-    from paper_2003_11076_b200.sharding import CollectiveReduce, gather_bands
+    from paper_2003_11076_b200.sharding import RecordExchange, gather_rows
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        # the callback sums per-iteration statistics in place, like st_solve calls it
-        red = CollectiveReduce()
-        vals = (ctypes.c_double * 7)(*[rank + 1.0 + i for i in range(7)])
-        rc = red(vals, 7, None)
-        summed = [vals[i] for i in range(7)]
-        # every rank fills only its band rows; the gather rebuilds the frame
+        # the per-iteration record exchange st_solve_rows calls (rank order)
+        rec = 96
+        send = torch.arange(rec, dtype=torch.uint8) + rank
+        recv = torch.zeros(world * rec, dtype=torch.uint8)
+        ex = RecordExchange(send, recv, None)
+        rc = ex._call(None, None)
+        gathered = recv.numpy().reshape(world, rec)
+        ok_x = rc == 0 and all(np.array_equal(gathered[r], np.arange(rec) + r)
+                               for r in range(world))
+        # every rank fills only its band rows; rank 0 gathers the frame
         h, w = 13, 5
-        full = (np.arange(h * w * 3, dtype=np.float32).reshape(h, w, 3) * 0.5)
-        local = np.full_like(full, -1.0)
+        full = np.arange(h * w * 3, dtype=np.float32).reshape(h, w, 3) * 0.5
+        bits = (np.arange(h * w, dtype=np.int64).reshape(h, w) * 7919).astype(np.int32)
+        a = torch.full((h, w, 3), -1.0)
+        b = torch.zeros((h, w), dtype=torch.int32)
         r0, r1 = band_rows(h, world, rank)
-        local[r0:r1] = full[r0:r1]
-        got = gather_bands(local, h, world, rank)
-        bits = np.arange(h * w, dtype=np.uint32).reshape(h, w) * 7919
-        lb = np.zeros_like(bits)
-        lb[r0:r1] = bits[r0:r1]
-        gb = gather_bands(lb, h, world, rank)
-        q.put((rank, rc, summed, bool(np.array_equal(got, full)), bool(np.array_equal(gb, bits))))
+        a[r0:r1] = torch.from_numpy(full[r0:r1])
+        b[r0:r1] = torch.from_numpy(bits[r0:r1])
+        gather_rows([a, b], h, world, rank, dst=0)
+        ok_g = rank != 0 or (np.array_equal(a.numpy(), full) and np.array_equal(b.numpy(), bits))
+        q.put((rank, bool(ok_x), bool(ok_g)))
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_two_ranks():
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ranks_exchange_and_gather(world):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    want = [(1.0 + i) + (2.0 + i) for i in range(7)]
-    for rank, rc, summed, ok_f, ok_b in res:
-        assert rc == 0
-        assert summed == want
-        assert ok_f and ok_b
+    for rank, ok_x, ok_g in res:
+        assert ok_x and ok_g, rank
+
+
+def _band_gpu_worker(rank, world, port, q, dynamic_only):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2003_11076_b200 as st
+        from paper_2003_11076_b200.sharding import reconstruct_band, solve_band
+        from golden_io import load
+        from test_gpu_parity import _Rig, _Tri, _frame, _params
+        g = load("occ320_noisy")
+        sp, pp = _params(st, g)
+        frame, rig, tri = _frame(st, g), _Rig(g), _Tri(g)
+        r = reconstruct_band(frame, rig, tri, sp, pp, dynamic_only=dynamic_only)
+        out = None
+        if r is not None:
+            out = dict(values=r.disparity.values, status=r.disparity.status,
+                       static=r.segmentation.static_bits, valid=r.segmentation.valid_bits,
+                       image=r.image, prov=r.provenance, n_rays=r.n_rays,
+                       stats=(r.stats.iterations_run, r.stats.converged_after,
+                              list(r.stats.mean_energy), list(r.stats.prev_energy),
+                              list(r.stats.changed_fraction), r.stats.active_pixels))
+        solver = st.DisparitySolver(frame, rig, tri, sp, pp)
+        d, s, stats = solve_band(solver, dynamic_only=dynamic_only)
+        q.put((rank, out, (d.values, s.static_bits, stats.iterations_run)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,dynamic_only", [(2, False), (3, False), (2, True)])
+def test_row_bands_match_single_device(world, dynamic_only):
+    """`reconstruct_band` over 2-3 processes (gloo collectives, one GPU; no
+    kernel waits on another process) reproduces the single-device
+    `reconstruct` bit for bit: disparity, status, bits, refocused image
+    (median halo rows included), provenance, n_rays; EMStats iterations,
+    changed fractions exact, energies to 1e-12 (a different summation
+    order).  solve_band likewise."""
+    import torch.multiprocessing as mp
+
+    import paper_2003_11076_b200 as st
+    from golden_io import load
+    from test_gpu_parity import _Rig, _Tri, _frame, _params
+    g = load("occ320_noisy")
+    sp, pp = _params(st, g)
+    ref = st.reconstruct(_frame(st, g), _Rig(g), _Tri(g), sp, pp, dynamic_only=dynamic_only)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_gpu_worker, args=(r, world, port, q, dynamic_only))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out = res[0][1]
+    assert all(x[1] is None for x in res[1:])
+    for key, want in (("values", ref.disparity.values), ("status", ref.disparity.status),
+                      ("static", ref.segmentation.static_bits),
+                      ("valid", ref.segmentation.valid_bits), ("image", ref.image),
+                      ("prov", ref.provenance), ("n_rays", ref.n_rays)):
+        assert np.array_equal(out[key], want), key
+    it, conv, me, pe, cf, act = out["stats"]
+    assert (it, conv) == (ref.stats.iterations_run, ref.stats.converged_after)
+    assert cf == list(ref.stats.changed_fraction)
+    assert act == ref.stats.active_pixels
+    np.testing.assert_allclose(me, ref.stats.mean_energy, rtol=1e-12)
+    np.testing.assert_allclose(pe, ref.stats.prev_energy, rtol=1e-12)
+    for rank, _, (vals, sbits, iters) in res:
+        assert np.array_equal(vals, ref.disparity.values), rank
+        assert np.array_equal(sbits, ref.segmentation.static_bits), rank
+        assert iters == ref.stats.iterations_run
 
 
 @pytest.mark.gpu
