@@ -358,38 +358,98 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def oracle_frame(frame, rig, tri, cfg):
+    """One WHOLE frame through the CPU oracle (the numpy restatement of the
+    reference): descriptors, surface raster, initial masks, EM with the
+    reference's convergence rule, refocus + median -- the timed unit of
+    SURVEY.md §8(d) (solver.py:436-502 + refocus.py:109-148), descriptors
+    included as for a fresh LightFieldFrame.  Returns seconds."""
+    import oracle
+    w, h, k, dmax, iters = CONFIGS[cfg]
+    sp, pp = params_for(cfg)
+    p = oracle.OracleParams(beta=sp.beta, threshold=sp.threshold, max_iters=sp.max_iters,
+                            min_static_rays=sp.min_static_rays, epsilon_prior=sp.epsilon_prior,
+                            sigma=pp.sigma, gamma=pp.gamma, d_max=pp.d_max,
+                            neighborhood_radius=pp.neighborhood_radius)
+    a = np.stack([rig.warp_coefficients(i)[0] for i in range(k)])
+    b = np.stack([rig.warp_coefficients(i)[1] for i in range(k)])
+    sup_uv, sup_d = tri.support_points()
+    t0 = time.perf_counter()
+    desc = [oracle.descriptors_of(im) for im in frame.images]
+    mu = oracle.mu_raster(tri.points, tri.disparities, tri.triangles, tri.planes, w, h)
+    s = oracle.OracleSolver(frame.images, frame.priors, a, b, rig.ref_index, mu, sup_uv, sup_d,
+                            params=p, descriptors=desc)
+    res = s.solve()
+    oracle.synthesize(frame.images, a, b, rig.ref_index, res["values"], res["status"],
+                      res["static_bits"], sp.min_static_rays, 1)
+    return time.perf_counter() - t0
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def blas_threads(n):
+    """Context manager limiting BLAS (OpenBLAS) threads to n (None = all)."""
+    import contextlib
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(n if n is not None else cpu_cores(), user_api="blas")
+    except Exception:  # noqa: BLE001
+        return contextlib.nullcontext()
+
+
+def cpu_baseline_block(frame, rig, tri, cfg):
+    """cpu_baseline of the GPU arm (rank 0, N = 1): whole frames through the
+    oracle on the box's host cores -- the bench config once with all cores
+    (`value`), and C1 (the configuration the CPU reference runs,
+    BASELINE configs[0]) with one BLAS thread and with all cores."""
+    with blas_threads(None):
+        t_cfg = oracle_frame(frame, rig, tri, cfg)
+    f1, r1, t1, _ = load_inputs("C1")
+    with blas_threads(1):
+        t_c1_one = oracle_frame(f1, r1, t1, "C1")
+    with blas_threads(None):
+        t_c1_all = oracle_frame(f1, r1, t1, "C1")
+    return {"value": 1.0 / t_cfg, "unit": "frames/s", "cores": cpu_cores(), "kind": "port",
+            "sample": f"one whole {cfg} frame (descriptors, surface raster, EM with the "
+                      f"reference convergence rule, refocus + median) through the numpy "
+                      f"oracle, all cores for BLAS ({t_cfg:.1f} s)",
+            "cpu_model": cpu_model(),
+            "c1_whole_frame": {"one_thread_s": t_c1_one, "all_cores_s": t_c1_all,
+                               "one_thread_fps": 1.0 / t_c1_one,
+                               "all_cores_fps": 1.0 / t_c1_all,
+                               "note": "C1 = 640x480, K=5, d_max 32 (BASELINE configs[0]); "
+                                       "OPENBLAS threads 1 vs all (threadpoolctl)"}}
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle, rank 0 only."""
+    """--impl reference: the CPU oracle (numpy restatement of the reference,
+    which is pure Python and cannot travel to the GPU box) on WHOLE frames of
+    the same config, rank 0 only, all host cores available to BLAS.  Warm-up
+    steps run on a 1/16 row band (import and cache warm-up only); every timed
+    step is one whole frame."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    try:
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(cpu_cores())
-    except Exception:  # noqa: BLE001
-        pass
     cfg = args.config
     w, h, k, dmax, iters = CONFIGS[cfg]
     frame, rig, tri, exact = load_inputs(cfg)
-    # calibrate the band so the whole run stays within ~args.budget seconds
-    probe = oracle_sample(frame, rig, tri, cfg, rows=8)
-    per_row = probe["t_band"] / 8
-    n_runs = args.steps + args.warmup
-    avail = max(1.0, args.budget / n_runs - probe["t_full"])
-    rows = int(max(8, min(h, avail / max(per_row, 1e-6))))
-    log(f"reference arm: {rows} rows per step (per-row {per_row:.3f}s, full parts "
-        f"{probe['t_full']:.2f}s)")
-    for _ in range(args.warmup):
-        oracle_sample(frame, rig, tri, cfg, rows=max(8, rows // 4))
-    times = []
-    for _ in range(args.steps):
-        r = oracle_sample(frame, rig, tri, cfg, rows=rows)
-        times.append(r["t_frame"])
+    with blas_threads(None):
+        for _ in range(args.warmup):
+            oracle_sample(frame, rig, tri, cfg, rows=max(8, h // 16))
+        times = [oracle_frame(frame, rig, tri, cfg) for _ in range(args.steps)]
     t = float(np.mean(times))
     fps = 1.0 / t
-    sample = (f"{rows} of {h} rows per step ({rows * w} px); descriptors + mu raster timed "
-              f"for the full frame, the per-pixel EM/refocus/median on the band, "
-              f"extrapolated by row fraction; numpy oracle")
+    sample = (f"whole {w}x{h} frames, one per step: descriptors, surface raster, EM "
+              f"(reference convergence rule), refocus + median through the numpy oracle; "
+              f"{cpu_cores()} host cores available to BLAS")
     out = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -397,7 +457,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(cfg, args, exact),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cpu_cores(),
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample, "cpu_model": cpu_model(),
+                         "step_s": times},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpix_plane_per_s": w * h * dmax * fps / 1e9,
@@ -416,6 +477,142 @@ def config_block(cfg, args, exact):
             "l2": "flushed between steps (256 MiB write)",
             "parallelism": f"frame-parallel x{args.gpus}" if args.gpus > 1 else "1 GPU",
             "forced_iters": args.forced_iters or None}
+
+
+# -- row bands (BASELINE C3/C4: one frame split across the ranks) -------------------------
+
+def measure_row_bands(cfg, steps, warmup, dist, rank, world, flush):
+    """One frame per step split into `world` row bands (sharding.BandPipeline):
+    per-rank band descriptors, whole-frame surface raster + support groups,
+    the banded EM with its per-iteration record all-gather (NCCL), the band
+    refocus + median, and the NCCL gather of the artefact bands to rank 0.
+    `value`: device-resident inputs (CUDA events, max over ranks); `e2e`:
+    each rank's band rows from pinned host memory + the Qhull tables, and
+    rank 0's full-frame artefacts back to the host (wall clock, max over
+    ranks).  Strong scaling: the frame is fixed, the ranks share it."""
+    import torch
+    import paper_2003_11076_b200 as st
+    from paper_2003_11076_b200.prior import TriDevice
+    from paper_2003_11076_b200.sharding import BandPipeline
+    w, h, k, dmax, iters = CONFIGS[cfg]
+    sp, pp = params_for(cfg)
+    frame, rig, tri, exact = load_inputs(cfg)
+    bp = BandPipeline(rig, w, h, sp, pp)
+    pin_imgs = [st.device.pinned_empty(im.shape, np.uint8) for im in frame.images]
+    pin_pris = [st.device.pinned_empty(q.shape, np.float32) for q in frame.priors]
+    for d_, s_ in zip(pin_imgs, frame.images):
+        d_[...] = s_
+    for d_, s_ in zip(pin_pris, frame.priors):
+        d_[...] = s_
+    bp.load(pin_imgs, pin_pris)
+    td = TriDevice(tri)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_ranks(x):
+        if dist is not None:
+            tt = torch.tensor([x], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            x = float(tt.item())
+        return x
+
+    for _ in range(warmup):
+        bp.run(td)
+        bp.gather()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(i & 0xff)
+        ev[i][0].record(stream)
+        bp.run(td)
+        bp.gather()
+        ev[i][1].record(stream)
+    barrier()
+    total = max_ranks(float(sum(a.elapsed_time(b) for a, b in ev)))
+    stats = bp.stats()
+    # e2e: band rows H2D (pinned), Qhull tables H2D, compute, gather, rank-0 D2H
+    host = None
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        bp.load(pin_imgs, pin_pris)
+        tdi = TriDevice(tri)
+        bp.run(tdi)
+        bp.gather()
+        if rank == 0:
+            host = bp.pipe.fetch()
+        else:
+            stream.synchronize()
+    torch.cuda.synchronize()
+    e2e_ms = max_ranks((time.perf_counter() - t0) * 1e3)
+    h2d = max_ranks(float(bp.h2d_bytes() + td.nbytes))
+    return {
+        "config": cfg, "value": steps / (total / 1e3), "unit": "frames/s", "n_gpus": world,
+        "ms_per_step": total / steps, "scaling": "strong",
+        "e2e": {"value": steps / (e2e_ms / 1e3), "unit": "frames/s",
+                "h2d_bytes_per_step_max_rank": int(h2d),
+                "d2h_bytes_per_step": int(bp.pipe.output_bytes()) if host is not None else None,
+                "ms_per_step": e2e_ms / steps},
+        "band_rows": list(bp.ext["rows"]), "solved_rows": list(bp.ext["solve"]),
+        "input_rows": list(bp.ext["images"]),
+        "iterations_run": stats.iterations_run, "converged_after": stats.converged_after,
+        "inputs_match_reference_digest": bool(exact),
+        "replicated_per_rank": "surface raster (Qhull walk replay) and support groups "
+                               "over the whole frame",
+        "collectives": "per EM iteration all_gather of 96-byte records (NCCL, "
+                       "stream-ordered); artefact band gather to rank 0 (NCCL p2p group)",
+    }
+
+
+def run_rows(args):
+    """--shard rows: the row-band line (BASELINE configs[2]: C3 at 1/2/4/8)."""
+    import torch
+    from paper_2003_11076_b200 import _native as N
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import datetime
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(seconds=300))
+    cfg = args.config
+    w, h, k, dmax, iters = CONFIGS[cfg]
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    lib = N.lib()
+    l0 = lib.st_launch_count()
+    with ClockSampler(local) as clocks:
+        r = measure_row_bands(cfg, args.steps, args.warmup, dist, rank, world, flush)
+    launches = lib.st_launch_count() - l0
+    if rank == 0:
+        peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        peak = float(json.load(open(peaks_path))["hbm_gbs"]) if os.path.exists(peaks_path) \
+            else 6650.0
+        out = {
+            "metric": METRIC, "value": r["value"], "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference renderer, reference support harvest)",
+            "config": dict(config_block(cfg, args, r["inputs_match_reference_digest"]),
+                           parallelism=f"row bands x{world}"),
+            "e2e": {"value": r["e2e"]["value"], "unit": "frames/s",
+                    "h2d_bytes_per_step": r["e2e"]["h2d_bytes_per_step_max_rank"],
+                    "d2h_bytes_per_step": r["e2e"]["d2h_bytes_per_step"]},
+            "gpu_launches": int(launches), "clocks": clocks.summary(),
+            "row_bands": r,
+            "roofline": None, "cpu_baseline": None,
+        }
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
 
 
 # -- GPU arm ------------------------------------------------------------------------------
@@ -542,6 +739,56 @@ def run_ours(args):
             ms = float(tt.item())
         return ms
 
+    def e2e_dropin(n):
+        # the reference's own entry points (solver.py:505-508 em_solve,
+        # refocus.py:109 synthesize) on pageable numpy frames, a fresh
+        # LightFieldFrame per step (descriptors recomputed, as the reference
+        # computes them per frame), numpy artefacts back
+        imgs = [np.array(x) for x in frame.images]
+        pris = [np.array(x) for x in frame.priors]
+
+        def one():
+            f = st.LightFieldFrame(images=imgs, priors=pris)
+            dmap, seg, _ = st.em_solve(f, rig, tri, sp, pp)
+            st.synthesize(f, rig, dmap, seg, min_static_rays=sp.min_static_rays,
+                          median_radius=1)
+        for _ in range(2):
+            one()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            one()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) * 1e3
+
+    def dyn_stream(n):
+        # dynamic_only (PAPER.md:242 person-only mode, solver.py:449-452,
+        # pipeline.py:250-260) through the pipelined public API
+        for _ in st.reconstruct_stream([(host_frame, tri)] * 4, rig, sp, pp, dynamic_only=True):
+            pass
+        barrier()
+        t0 = time.perf_counter()
+        for _ in st.reconstruct_stream([(host_frame, tri)] * n, rig, sp, pp, dynamic_only=True):
+            pass
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) * 1e3
+
+    dropin_n = 10
+    dropin_ms = max_ranks(e2e_dropin(dropin_n))
+    dyn_n = max(10, e2e_steps // 2)
+    dyn_ms = max_ranks(dyn_stream(dyn_n))
+    # resident dynamic_only frames (CUDA events, L2 flushed between steps)
+    pipe.run(tdev, dynamic_only=True)
+    torch.cuda.synchronize()
+    dyn_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        dyn_ev[i][0].record(stream)
+        pipe.run(tdev, dynamic_only=True)
+        dyn_ev[i][1].record(stream)
+    barrier()
+    dyn_res_ms = max_ranks(float(sum(a.elapsed_time(b) for a, b in dyn_ev)))
     single_ms = max_ranks(e2e_single())
     # host-side throughput is sensitive to host noise: median of five streams,
     # after two untimed ones (the pinned host allocator fills its cache of
@@ -607,6 +854,14 @@ def run_ours(args):
         forced = {"iterations": iters, "fps_per_gpu": args.forced_steps / (fms / 1e3),
                   "ms_per_frame": fms / args.forced_steps}
 
+    # -- BASELINE configs[2]: the C3 frame split into row bands over the same ranks
+    row_bands = None
+    if args.row_band_steps > 0 and not args.forced_iters:
+        try:
+            row_bands = measure_row_bands("C3", args.row_band_steps, 3, dist, rank, world, flush)
+        except Exception as exc:  # noqa: BLE001 -- reported, the frame-parallel line stands
+            row_bands = {"error": f"{type(exc).__name__}: {exc}"}
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -652,14 +907,7 @@ def run_ours(args):
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        rows = args.cpu_rows
-        r = oracle_sample(frame, rig, tri, cfg, rows=rows)
-        cpu = {"value": 1.0 / r["t_frame"], "unit": "frames/s", "cores": cpu_cores(),
-               "kind": "port",
-               "sample": f"{rows} of {h} rows ({rows * w} px) through the numpy oracle "
-                         f"(initial masks, EM, refocus, median), descriptors + mu raster on "
-                         f"the full frame, extrapolated by row fraction "
-                         f"({r['t_frame']:.1f} s/frame)"}
+        cpu = cpu_baseline_block(frame, rig, tri, cfg)
 
     nxt = None
     if world == 1 and not args.no_next_rows:
@@ -699,7 +947,15 @@ def run_ours(args):
                 "api": "reconstruct_stream (pipelined), host wall clock incl. all streams; "
                        "median of 5 streams",
                 "reps_ms_per_step": [x / e2e_steps for x in e2e_reps],
-                "single_call_fps": world * e2e_steps / (single_ms / 1e3)},
+                "single_call_fps": world * e2e_steps / (single_ms / 1e3),
+                "dropin_fps": world * dropin_n / (dropin_ms / 1e3),
+                "dropin_api": "em_solve + synthesize (the reference entry points) on "
+                              "pageable numpy frames, fresh LightFieldFrame per step"},
+        "dynamic_only": {"e2e_stream_fps": world * dyn_n / (dyn_ms / 1e3),
+                         "resident_fps": world * args.steps / (dyn_res_ms / 1e3),
+                         "resident_ms_per_step": dyn_res_ms / args.steps,
+                         "note": "person-only mode (PAPER.md:242; solver.py:449-452): "
+                                 "st_solve_rows (one read-back of the active-list size)"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "em": {"iterations_run": s0.iterations_run, "converged_after": s0.converged_after,
@@ -716,6 +972,7 @@ def run_ours(args):
                             for n in stats[0].stage_ms}},
         "gpix_plane_per_s": w * h * dmax * fps / 1e9,
         "forced_iters_mode": forced,
+        "row_bands_C3": row_bands,
         "next_rows": nxt,
         "pipelined_resident": {"value": pipelined_fps, "unit": "frames/s",
                                "ms_per_frame": pipe_ms / n_pipe, "frames": n_pipe,
@@ -733,25 +990,35 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default C2 (C3 with --shard rows)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--forced-iters", type=int, default=0)
     ap.add_argument("--forced-steps", type=int, default=5)
-    ap.add_argument("--cpu-rows", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="value loop only (profiling)")
     ap.add_argument("--no-next-rows", action="store_true",
                     help="skip the harvest / triangulation / frame-in measurements")
     ap.add_argument("--e2e-frames", type=int, default=60,
                     help="frames per timed e2e stream (steady-state throughput)")
+    ap.add_argument("--shard", default="frames", choices=["frames", "rows"],
+                    help="multi-GPU split: frames (C5 frame-parallel, default) or rows "
+                         "(one frame in row bands, C3/C4)")
+    ap.add_argument("--row-band-steps", type=int, default=10,
+                    help="frame-parallel runs also time C3 row bands over the same ranks "
+                         "(0 = skip)")
     ap.add_argument("--budget", type=float, default=150.0,
                     help="reference arm: seconds for the whole run")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")
         args.warmup = 3
+    if args.config is None:
+        args.config = "C3" if args.shard == "rows" else "C2"
     if args.impl == "reference":
         run_reference(args)
+    elif args.shard == "rows":
+        run_rows(args)
     else:
         run_ours(args)
 

@@ -789,8 +789,9 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
   {
     st::EmCtx ci = c;
     ci.pix0 = A.init_pix0;
-    st::k_initial_masks<<<blocks_for(A.init_n, 128), 128, 0, s>>>(ci, nullptr, A.init_n,
-                                                                  static_bits, valid_bits);
+    // (k_initial_masks writes row i of its outputs: pixel init_pix0 + i)
+    st::k_initial_masks<<<blocks_for(A.init_n, 128), 128, 0, s>>>(
+        ci, nullptr, A.init_n, static_bits + A.init_pix0, valid_bits + A.init_pix0);
     ST_LAUNCH_CHECK("k_initial_masks");
   }
   c.pix0 = A.active ? 0 : A.pix0;

@@ -261,8 +261,23 @@ class DisparitySolver:
         ws = getattr(self, "_solve_ws", None)
         if ws is None or ws.numel() < nbytes:
             ws = self._solve_ws = empty((nbytes,), t.uint8)
-        stats = N.StStats()
         p = N.make_params(self.params, self.prior_params, forced_iters, timing)
+        if reduce is None and active_mask is None and not timing:
+            # no host round trip per iteration: the device-side control of
+            # st_solve_async (dense) / st_solve_rows (dynamic_only)
+            sdev = empty((N.C.sizeof(N.StStats),), t.uint8)
+            if dynamic_only:
+                N.check(N.lib().st_solve_rows(
+                    self._frame, self._rig, p, 1, 0, h, 0, h, N.ptr(values), N.ptr(status),
+                    N.ptr(sbits), N.ptr(vbits), N.ptr(sdev), N.ptr(ws), ws.numel(),
+                    N.EXCHANGE_FN(), None, 1, None, None, N.stream_handle()))
+            else:
+                N.invoke("st_solve_async", self._frame, self._rig, p, values, status, sbits,
+                         vbits, sdev, ws, ws.numel())
+            stats = N.StStats.from_buffer_copy(download(sdev).tobytes())
+            stats.support_records = self._support_records
+            return (values, status, sbits, vbits), _stats_of(stats)
+        stats = N.StStats()
         am = upload(np.asarray(active_mask, dtype=np.uint8).ravel()) if active_mask is not None \
             else None
         cb = N.REDUCE_FN(reduce) if reduce is not None else N.REDUCE_FN()
