@@ -22,5 +22,5 @@ from .em import (  # noqa: F401
     STATUS_LOW_TEXTURE, STATUS_NO_STATIC_EVIDENCE, PROV_FALLBACK, PROV_COPIED,
     PROV_REFOCUSED, OracleParams, warp, bilinear, gray_of, sobel_of,
     descriptors_of, log_prior, e_step, e_step_scores, mask_order,
-    OracleSolver, synthesize, median_filter, mu_raster,
+    OracleSolver, synthesize, median_filter, mu_raster, numpy_sum_order,
 )

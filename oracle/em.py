@@ -49,6 +49,41 @@ class OracleParams:
 
 # -- L1 primitives -----------------------------------------------------------
 
+def numpy_sum_order(values):
+    """np.add.reduce of a contiguous float64 array, restated: 0.0 plus
+    numpy's pairwise_sum (numpy/_core/src/umath/loops_utils.h.src) -- blocks
+    of n <= 128 with eight strided accumulators combined as
+    ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail in order (n < 8: a
+    running sum from 0.0), larger blocks split at n/2 rounded down to a
+    multiple of 8.  This is the order solver.py:466/471 `finite.mean()` sums
+    in; the device statistics (st_mean.cu) replay it.  Pure Python: small n."""
+    a = [float(x) for x in np.asarray(values, dtype=np.float64).ravel()]
+
+    def pw(lo, n):
+        if n < 8:
+            r = 0.0
+            for i in range(n):
+                r += a[lo + i]
+            return r
+        if n <= 128:
+            r = a[lo:lo + 8]
+            i = 8
+            while i < n - (n % 8):
+                for j in range(8):
+                    r[j] += a[lo + i + j]
+                i += 8
+            res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+            while i < n:
+                res += a[lo + i]
+                i += 1
+            return res
+        n2 = n // 2
+        n2 -= n2 % 8
+        return pw(lo, n2) + pw(lo + n2, n - n2)
+
+    return 0.0 + pw(0, len(a))
+
+
 def warp(A, b, u, v, d):
     """geometry.py:204-219: h = A (u, v, 1) + d b, evaluated left to right."""
     u = np.asarray(u, dtype=np.float64)

@@ -488,7 +488,7 @@ int st_masked_variance(const double* desc, const uint8_t* mask, int64_t n, int32
 
 struct SolveLayout {
   size_t d, e, pe, st_act, chg, mask_in, mlist, elist, counts, flist, active, flags, offs,
-      work, parts, reduced, cub, total;
+      work, parts, reduced, cub, pw_part, pw_done, pw_seq, pw_scratch, total;
   size_t cub_bytes;
   int max_warps;
 };
@@ -519,6 +519,10 @@ static SolveLayout solve_layout(int W, int H) {
   L.parts = o;    o += align_up(sizeof(st::Partial) * L.max_warps);
   L.reduced = o;  o += align_up(sizeof(st::Partial) * (ST_MAX_ITERS + 2));
   L.cub = o;      o += align_up(L.cub_bytes);
+  L.pw_part = o;  o += align_up(sizeof(double) * 2 * (1 << ST_PW_MAX_DEPTH));
+  L.pw_done = o;  o += align_up(sizeof(unsigned) * 2);
+  L.pw_seq = o;   o += align_up(32);
+  L.pw_scratch = o; o += align_up(sizeof(double) * 2 * npx);
   L.total = o;
   return L;
 }
@@ -781,6 +785,7 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
   ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t) + sizeof(int), s));
   // E-step fallback count (byte 48) and the stats kernel's block counter (52)
   ST_CUDA_CHECK(cudaMemsetAsync(counts + 12, 0, 4 * sizeof(uint32_t), s));
+  ST_CUDA_CHECK(cudaMemsetAsync(ws + L.pw_done, 0, sizeof(unsigned) * 2, s));
   st::k_stats_init<<<1, 32, 0, s>>>(stats_dev, n_cnt);
   ST_LAUNCH_CHECK("k_stats_init");
   double* eps_logs = (double*)(counts + 4);
@@ -903,6 +908,14 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
       st::k_band_control<<<1, 32, 0, s>>>(it, recs, A.exchange ? A.world : 1, p->forced_iters,
                                           stats_dev, stop);
       ST_LAUNCH_CHECK("k_band_control");
+    }
+    // one device: the iteration's energy means exactly as numpy sums them
+    // (row bands keep the fixed-order record sums, summed over shards)
+    if (!A.exchange && n_cnt > 0) {
+      const int rc = st_pw_means(e_act + A.cnt_lo, pe_act + A.cnt_lo, n_cnt, reduced + it,
+                                 ws + L.pw_scratch, ws + L.pw_seq, (double*)(ws + L.pw_part),
+                                 (unsigned*)(ws + L.pw_done), it, stats_dev, s);
+      if (rc) return rc;
     }
   }
   if (A.active) {

@@ -179,3 +179,10 @@ __global__ void k_scatter_active(const uint32_t* flags, const uint32_t* offs, in
                                  int64_t* active);
 
 }  // namespace st
+
+// numpy-exact EM statistics means (st_mean.cu): the finite values of e / pe
+// (slot order) -> stats->mean_energy[it-1] / prev_energy[it-2].
+#define ST_PW_MAX_DEPTH 12
+int st_pw_means(const double* e, const double* pe, int64_t n, const void* rec, void* scratch,
+                void* seq, double* partial, unsigned* done, int it, st_stats* stats,
+                cudaStream_t s);

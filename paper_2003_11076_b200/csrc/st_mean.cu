@@ -1,0 +1,281 @@
+// numpy's float64 mean, bit for bit, for the EM statistics (solver.py:466
+// `finite.mean()` of the M-step energies and :471 of the previous-disparity
+// energies; written to em_stats.txt by pipeline.py:292-302 with repr()).
+//
+// np.add.reduce over a contiguous float64 array evaluates
+//     0.0 + pairwise_sum(a, n)
+// (numpy loops_utils.h.src): a block of n <= 128 values is summed with
+// eight strided accumulators r[j] += a[8i + j] combined as
+// ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)), then the n % 8 tail in
+// order (n < 8: a plain running sum from 0.0); a larger block splits at
+// n2 = n/2 rounded down to a multiple of 8 and adds the two halves' sums.
+// The mean is that sum / n (IEEE division).  The identity start and the
+// split rule are pinned against numpy itself in tests/test_oracle.py.
+//
+// Device form: the top D levels of the recursion assign one node (~4k
+// values) per block; a block enumerates its node's leaves, sums them in
+// parallel (one thread per leaf), then replays the node's additions in
+// recursion order; the last block to finish replays the top D levels over
+// the blocks' sums.  The sequence is the FINITE values in slot order: when
+// a value is non-finite (never for d_max >= 1: the coarse sweep always has
+// a finite candidate) one block first compacts them into scratch.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <cub/block/block_scan.cuh>
+
+#include "st_common.cuh"
+#include "st_em.cuh"
+
+namespace st {
+
+#define PW_LEAF 128
+#define PW_MAX_LEAVES 256
+#define PW_THREADS 256
+
+__device__ __forceinline__ int64_t pw_split(int64_t n) {
+  const int64_t h = n / 2;
+  return h - h % 8;
+}
+
+__device__ double pw_leaf(const double* __restrict__ a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r = dadd(r, a[i]);
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = dadd(r[j], a[i + j]);
+  }
+  double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+  for (; i < n; ++i) res = dadd(res, a[i]);
+  return res;
+}
+
+// The recursion over a node of size n whose leaves (size <= PW_LEAF, or
+// depth == max_depth) have sums leaf[k], k in DFS order: one thread.
+__device__ double pw_combine(int64_t n, int max_depth, const double* leaf) {
+  int64_t sz[64];
+  double acc[64];
+  uint8_t st[64];
+  int sp = 0, k = 0;
+  sz[0] = n;
+  for (;;) {
+    while (sz[sp] > PW_LEAF && sp < max_depth) {
+      st[sp] = 0;
+      sz[sp + 1] = pw_split(sz[sp]);
+      ++sp;
+    }
+    double ret = leaf[k++];
+    for (;;) {
+      if (sp == 0) return ret;
+      --sp;
+      if (st[sp] == 0) {  // left child done: its right sibling next
+        acc[sp] = ret;
+        st[sp] = 1;
+        sz[sp + 1] = sz[sp] - pw_split(sz[sp]);
+        ++sp;
+        break;
+      }
+      ret = dadd(acc[sp], ret);
+    }
+  }
+}
+
+struct PwSeq {
+  const double* src;
+  int64_t m;
+};
+
+// Rare path: compact the finite values (slot order) into scratch when the
+// statistics found a non-finite one; otherwise point at the input.
+__global__ void __launch_bounds__(1024) k_pw_prepare(const double* __restrict__ e,
+                                                     const double* __restrict__ pe, int64_t n,
+                                                     const Partial* __restrict__ rec,
+                                                     double* __restrict__ scratch, PwSeq* seq,
+                                                     int with_prev) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int64_t base;
+  for (int y = 0; y < 1 + with_prev; ++y) {
+    const double* x = y ? pe : e;
+    const int64_t m = y ? rec->n_pfin : rec->n_fin;
+    if (m == n) {
+      if (threadIdx.x == 0) seq[y] = PwSeq{x, n};
+      continue;
+    }
+    double* out = scratch + (size_t)y * n;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    for (int64_t c = 0; c < n; c += 1024) {
+      const int64_t i = c + threadIdx.x;
+      const int f = (i < n && isfinite(x[i])) ? 1 : 0;
+      int off, tot;
+      Scan(tmp).ExclusiveSum(f, off, tot);
+      if (f) out[base + off] = x[i];
+      __syncthreads();
+      if (threadIdx.x == 0) base += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) seq[y] = PwSeq{out, base};
+    __syncthreads();
+  }
+}
+
+// gridDim.x = 2^D nodes, gridDim.y = 1 (E) or 2 (E and previous E).
+__global__ void __launch_bounds__(PW_THREADS) k_pw_mean(const PwSeq* __restrict__ seq, int D,
+                                                        int it, double* __restrict__ partial,
+                                                        unsigned* __restrict__ done,
+                                                        st_stats* __restrict__ stats) {
+  if (stats->iterations_run != it) return;  // the iteration did not run (converged before)
+  const int y = blockIdx.y;
+  const PwSeq q = seq[y];
+  const int nb = gridDim.x;
+  __shared__ int64_t leaf_s[PW_MAX_LEAVES], leaf_n[PW_MAX_LEAVES];
+  __shared__ double leaf_v[PW_MAX_LEAVES];
+  __shared__ int n_leaves;
+  __shared__ int64_t node_s, node_n;
+  __shared__ int node_depth;
+  __shared__ bool owner;
+  if (threadIdx.x == 0) {
+    // descend the top D levels along this block's path; an early leaf
+    // (size <= PW_LEAF) belongs to the path whose remaining bits are zero
+    int64_t s = 0, n = q.m;
+    int d = 0;
+    bool own = true;
+    while (d < D && n > PW_LEAF) {
+      const int bit = (blockIdx.x >> (D - 1 - d)) & 1;
+      const int64_t n2 = pw_split(n);
+      if (bit) {
+        s += n2;
+        n -= n2;
+      } else {
+        n = n2;
+      }
+      ++d;
+    }
+    if (d < D && (blockIdx.x & ((1u << (D - d)) - 1u)) != 0) own = false;
+    owner = own;
+    node_s = s;
+    node_n = n;
+    node_depth = d;
+    // enumerate the node's leaves in DFS order
+    int cnt = 0;
+    if (own) {
+      int64_t st_s[64], st_n[64];
+      int sp = 0;
+      st_s[0] = s;
+      st_n[0] = n;
+      while (sp >= 0) {
+        const int64_t a = st_s[sp], b = st_n[sp];
+        --sp;
+        if (b > PW_LEAF) {
+          const int64_t b2 = pw_split(b);
+          ++sp;  // right child below the left one: the left pops first
+          st_s[sp] = a + b2;
+          st_n[sp] = b - b2;
+          ++sp;
+          st_s[sp] = a;
+          st_n[sp] = b2;
+        } else if (cnt < PW_MAX_LEAVES) {
+          leaf_s[cnt] = a;
+          leaf_n[cnt] = b;
+          ++cnt;
+        }
+      }
+    }
+    n_leaves = cnt;
+  }
+  __syncthreads();
+  if (owner) {
+    for (int l = threadIdx.x; l < n_leaves; l += blockDim.x)
+      leaf_v[l] = q.m > 0 ? pw_leaf(q.src + leaf_s[l], leaf_n[l]) : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    partial[(size_t)y * nb + blockIdx.x] =
+        owner ? pw_combine(node_n, 64, leaf_v) : 0.0;
+    (void)node_s;
+    (void)node_depth;
+    __threadfence();
+  }
+  // the last block of this sequence replays the top D levels
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(done + y, 1u) == (unsigned)nb - 1;
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  done[y] = 0u;
+  // top-level leaves in DFS order = the owning blocks in increasing path order
+  // (a node that became a leaf early owns the lowest path under it)
+  double* part = partial + (size_t)y * nb;
+  int64_t sz[64];
+  int path[64];
+  double acc[64];
+  uint8_t stt[64];
+  int sp = 0;
+  sz[0] = q.m;
+  path[0] = 0;
+  double total;
+  for (;;) {
+    while (sp < D && sz[sp] > PW_LEAF) {
+      stt[sp] = 0;
+      sz[sp + 1] = pw_split(sz[sp]);
+      path[sp + 1] = path[sp] << 1;
+      ++sp;
+    }
+    double ret = part[(int64_t)path[sp] << (D - sp)];
+    bool finished = false;
+    for (;;) {
+      if (sp == 0) {
+        finished = true;
+        break;
+      }
+      --sp;
+      if (stt[sp] == 0) {
+        acc[sp] = ret;
+        stt[sp] = 1;
+        sz[sp + 1] = sz[sp] - pw_split(sz[sp]);
+        path[sp + 1] = (path[sp] << 1) | 1;
+        ++sp;
+        break;
+      }
+      ret = dadd(acc[sp], ret);
+    }
+    if (finished) {
+      total = ret;
+      break;
+    }
+  }
+  const double sum = dadd(0.0, total);
+  const double mean = q.m > 0 ? ddiv(sum, (double)q.m) : NAN;
+  if (y == 0)
+    stats->mean_energy[it - 1] = mean;
+  else
+    stats->prev_energy[it - 2] = mean;
+}
+
+}  // namespace st
+
+// Host launcher used by the asynchronous solve (st_api.cu).
+int st_pw_means(const double* e, const double* pe, int64_t n, const void* rec, void* scratch,
+                void* seq, double* partial, unsigned* done, int it, st_stats* stats,
+                cudaStream_t s) {
+  if (n <= 0) return ST_OK;
+  const int with_prev = it > 1 ? 1 : 0;
+  st::k_pw_prepare<<<1, 1024, 0, s>>>(e, pe, n, (const st::Partial*)rec, (double*)scratch,
+                                       (st::PwSeq*)seq, with_prev);
+  ST_LAUNCH_CHECK("k_pw_prepare");
+  int D = 0;
+  while (D < ST_PW_MAX_DEPTH && (n >> D) > 4096) ++D;
+  st::k_pw_mean<<<dim3(1u << D, 1 + with_prev), PW_THREADS, 0, s>>>(
+      (const st::PwSeq*)seq, D, it, partial, done, stats);
+  ST_LAUNCH_CHECK("k_pw_mean");
+  return ST_OK;
+}

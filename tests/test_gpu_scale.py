@@ -133,10 +133,13 @@ def test_async_solve_equals_sync(st, forced):
                  (a.segmentation.static_bits, b.segmentation.static_bits),
                  (a.segmentation.valid_bits, b.segmentation.valid_bits), (a.image, b.image)):
         assert np.array_equal(x, y)
-    for f in ("iterations_run", "converged_after", "mean_energy", "prev_energy",
-              "changed_fraction", "candidates_total", "energy_evals", "msteps", "esteps",
-              "prev_evals", "active_pixels"):
+    for f in ("iterations_run", "converged_after", "changed_fraction", "candidates_total",
+              "energy_evals", "msteps", "esteps", "prev_evals", "active_pixels"):
         assert getattr(a.stats, f) == getattr(b.stats, f), f
+    # the synchronous path sums the energies in a fixed order, the
+    # asynchronous one replays numpy's pairwise order (st_mean.cu)
+    for f in ("mean_energy", "prev_energy"):
+        np.testing.assert_allclose(getattr(a.stats, f), getattr(b.stats, f), rtol=1e-12)
 
 
 @pytest.mark.slow

@@ -103,3 +103,17 @@ def test_oracle_matches_live_reference(reference):
     assert np.array_equal(r["static_bits"], seg.static_bits)
     assert np.array_equal(r["valid_bits"], seg.valid_bits)
     assert r["stats"]["mean_energy"] == stats.mean_energy
+
+
+def test_numpy_sum_order_is_numpys():
+    """The summation order the device statistics replay (st_mean.cu) is
+    numpy's own: identity start + pairwise blocks (discriminated against the
+    first-element start on arrays where the two differ)."""
+    import oracle
+    rng = np.random.default_rng(7)
+    for n in list(range(0, 40)) + [127, 128, 129, 255, 256, 257, 1000, 4097, 20011]:
+        x = rng.standard_normal(n) * 10.0 ** rng.integers(-6, 6, n)
+        assert oracle.numpy_sum_order(x) == np.add.reduce(x), n
+        if n:
+            assert oracle.numpy_sum_order(x) / n == x.mean(), n
+    assert str(oracle.numpy_sum_order(np.array([-0.0]))) == str(np.add.reduce(np.array([-0.0])))

@@ -211,20 +211,14 @@ def _check_run(run_dir, case):
            for f in sorted(os.listdir(run_dir)) if f != "timings.txt"}
     want = case["artefacts"]
     assert sorted(got) == sorted(want)
-    # em_stats.txt: the statistics are fixed-order device sums, numpy uses a
-    # pairwise tree -- compared as numbers, every other artefact as bytes
+    # every artefact byte for byte, em_stats.txt included (the device means
+    # replay numpy's pairwise summation, st_mean.cu)
     for f in want:
-        if f != "em_stats.txt":
-            assert got[f] == want[f], f
+        assert got[f] == want[f], f
     text = open(os.path.join(run_dir, "em_stats.txt")).read()
     vals = dict(line.split(" = ", 1) for line in text.strip().splitlines())
     es = case["em_stats"]
     assert int(vals["iterations_run"]) == es["iterations_run"]
-    conv = vals["converged_after"]
-    assert (None if conv == "none" else int(conv)) == es["converged_after"]
-    for key in ("mean_energy", "prev_energy", "changed_fraction"):
-        v = [float(x) for x in vals[key].split(",") if x.strip()]
-        assert np.allclose(v, es[key], rtol=1e-12, atol=0), key
 
 
 @pytest.mark.gpu
