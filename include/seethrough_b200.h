@@ -309,6 +309,15 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
              st_stats* stats, void* workspace, int64_t workspace_bytes,
              st_reduce_fn reduce, void* reduce_user, void* stream);
 
+/* solver.py:466 `finite.mean()`: the mean of the finite values of x (n
+ * float64, device) in numpy's own summation order (0.0 + pairwise_sum over
+ * the compacted array, then / count; NaN when none is finite), into
+ * out[0] (device).  The EM statistics of the single-device solves use the
+ * same kernels. */
+int st_numpy_mean(const double* x, int64_t n, double* out, void* workspace,
+                  int64_t workspace_bytes, void* stream);
+int64_t st_numpy_mean_workspace(int64_t n);
+
 /* ---- row bands (BASELINE C3/C4) ------------------------ */
 
 /* Per-iteration exchange of the row-band shards' statistics records

@@ -138,6 +138,8 @@ _SIGS = {
     "st_solve": (C.c_int, [C.POINTER(StFrame), C.POINTER(StRig), C.POINTER(StParams), _I32, _P,
                            _P, _P, _P, _P, C.POINTER(StStats), _P, _I64, REDUCE_FN, _P, _P]),
     "st_band_record_bytes": (C.c_int64, []),
+    "st_numpy_mean": (C.c_int, [_P, _I64, _P, _P, _I64, _P]),
+    "st_numpy_mean_workspace": (C.c_int64, [_I64]),
     "st_solve_rows": (C.c_int, [C.POINTER(StFrame), C.POINTER(StRig), C.POINTER(StParams), _I32,
                                 _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _I64,
                                 EXCHANGE_FN, _P, _I32, _P, _P, _P]),

@@ -234,6 +234,26 @@ void launch_e_step(int K, int64_t n, cudaStream_t s, const st::EmCtx& c,
   }
 }
 
+// M-step launch: the 4-lanes-per-slot kernel on rectified rigs (same
+// outputs), the one-thread-per-slot kernel otherwise or with
+// ST_MSTEP_SCALAR set.  `grid_slots`: slots the grid must cover (a wave of
+// grid-stride blocks for worklists).  Returns the grid used.
+bool mstep_g4(const st::EmCtx& c) {
+  static const bool scalar = getenv("ST_MSTEP_SCALAR") != nullptr;
+  return c.rectified && !scalar;
+}
+
+unsigned mstep_blocks(const st::EmCtx& c, int64_t grid_slots) {
+  return blocks_for(std::max<int64_t>(grid_slots, 1), mstep_g4(c) ? EM_BLOCK / 4 : EM_BLOCK);
+}
+
+void launch_m_step(const st::EmCtx& c, const st::MStepArgs& a, unsigned grid, cudaStream_t s) {
+  if (mstep_g4(c))
+    st::k_m_step_g4<<<grid, EM_BLOCK, 0, s>>>(c, a);
+  else
+    st::k_m_step<<<grid, EM_BLOCK, 0, s>>>(c, a);
+}
+
 }  // namespace
 
 namespace st {
@@ -436,7 +456,7 @@ int st_m_step(const st_frame* f, const st_rig* rig, const st_params* p, const in
   a.d = d_out;
   a.e = e_out;
   a.status = status_out;
-  st::k_m_step<<<blocks_for(n, EM_BLOCK), EM_BLOCK, 0, (cudaStream_t)stream>>>(c, a);
+  launch_m_step(c, a, mstep_blocks(c, n), (cudaStream_t)stream);
   ST_LAUNCH_CHECK("k_m_step");
   return ST_OK;
 }
@@ -496,7 +516,7 @@ struct SolveLayout {
 static SolveLayout solve_layout(int W, int H) {
   SolveLayout L;
   const int64_t npx = (int64_t)W * H;
-  L.max_warps = (int)blocks_for(npx, EM_BLOCK) * (EM_BLOCK / 32);
+  L.max_warps = (int)blocks_for(npx, EM_BLOCK / 4) * (EM_BLOCK / 32);  // k_m_step_g4's grid
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                 (int)(npx + 1));
@@ -618,7 +638,6 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
   // worklist counts start cleared even on a shard whose band has no active pixel
   ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), s));
   const int nblk = (int)blocks_for(n_act, EM_BLOCK);
-  const int nwarps = nblk * (EM_BLOCK / 32);
   bool solved = false;
   for (int it = 1; it <= iters; ++it) {
     if (n_act_global == 0) {
@@ -655,7 +674,7 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       a.elist = elist;
       a.elist_count = counts + 1;
       a.partials = work;
-      st::k_m_step<<<nblk, EM_BLOCK, 0, s>>>(c, a);
+      launch_m_step(c, a, mstep_blocks(c, n_act), s);
       ST_LAUNCH_CHECK("k_m_step");
       ev.record(1, s);
       st::EStepArgs e = {};
@@ -675,7 +694,8 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       ST_LAUNCH_CHECK("k_e_step_at");
       ev.record(2, s);
       const int sblk = std::min((int)blocks_for(n_act, STATS_BLOCK), STATS_GRID);
-      st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(n_act, it > 1, e_act, pe_act, chg, work, nwarps,
+      st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(n_act, it > 1, e_act, pe_act, chg, work,
+                                                  (int)mstep_blocks(c, n_act) * (EM_BLOCK / 32),
                                                   parts);
       ST_LAUNCH_CHECK("k_em_stats");
       st::k_reduce_partials<<<1, 256, 0, s>>>(parts, sblk, reduced + it);
@@ -812,6 +832,8 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     return e ? atoi(e) : 16;
   }();
   const int wave2 = std::min(nblk, 148 * wave_env);
+  const int mblk = (int)mstep_blocks(c, n);
+  const int mwave2 = std::min(mblk, 148 * wave_env);
   // a row band with no active pixel still takes part in every exchange
   for (int it = 1; it <= iters && (n > 0 || A.band); ++it) {
     // long caps (max_iters > ST_ASYNC_CHUNK) and row bands: read the device
@@ -852,7 +874,8 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     a.elist_count = counts + 1;
     a.partials = work;
     a.stop = stop;
-    st::k_m_step<<<it > 1 ? wave : nblk, EM_BLOCK, 0, s>>>(c, a);
+    const int mgrid = it == 1 ? mblk : it == 2 ? mwave2 : std::min(mblk, 148 * 4);
+    launch_m_step(c, a, mgrid, s);
     ST_LAUNCH_CHECK("k_m_step");
     st::EStepArgs e = {};
     e.pix = A.active;
@@ -889,10 +912,11 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     tail.record_only = A.band ? 1 : 0;
     tail.record_n_act = n_cnt;
     tail.record_slots = n;
-    st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(n_cnt, it > 1, e_act + A.cnt_lo,
-                                                pe_act + A.cnt_lo, chg + A.cnt_lo, work,
-                                                (it > 1 ? wave : nblk) * (EM_BLOCK / 32),
-                                                parts, stop, tail);
+    st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(
+        n_cnt, it > 1, e_act + A.cnt_lo, pe_act + A.cnt_lo, chg + A.cnt_lo, work,
+        (n > 0 ? (it == 1 ? mblk : it == 2 ? mwave2 : std::min(mblk, 148 * 4)) : 0) *
+            (EM_BLOCK / 32),
+        parts, stop, tail);
     ST_LAUNCH_CHECK("k_em_stats");
     if (A.band) {
       const st::Partial* recs = reduced + it;

@@ -23,6 +23,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include <cub/block/block_scan.cuh>
 
 #include "st_common.cuh"
@@ -277,5 +279,57 @@ int st_pw_means(const double* e, const double* pe, int64_t n, const void* rec, v
   st::k_pw_mean<<<dim3(1u << D, 1 + with_prev), PW_THREADS, 0, s>>>(
       (const st::PwSeq*)seq, D, it, partial, done, stats);
   ST_LAUNCH_CHECK("k_pw_mean");
+  return ST_OK;
+}
+
+namespace st {
+__global__ void k_count_finite(const double* __restrict__ x, int64_t n, Partial* rec,
+                               st_stats* stats) {
+  long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += isfinite(x[i]) ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long*)&rec->n_fin, (unsigned long long)c);
+  if (blockIdx.x == 0 && threadIdx.x == 0) stats->iterations_run = 1;
+}
+}  // namespace st
+
+extern "C" int64_t st_numpy_mean_workspace(int64_t n) {
+  return (int64_t)(1024 + sizeof(st_stats) + sizeof(double) * 2 * (1 << ST_PW_MAX_DEPTH) +
+                   sizeof(double) * (n > 0 ? n : 1) + 256 * 4);
+}
+
+// np.mean of the finite values of x (n float64, device), bit for bit: the
+// device form of solver.py:466 `finite.mean()` (NaN when none is finite).
+extern "C" int st_numpy_mean(const double* x, int64_t n, double* out, void* workspace,
+                             int64_t workspace_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (workspace_bytes < st_numpy_mean_workspace(n)) {
+    sthost::set_error("st_numpy_mean: workspace too small");
+    return ST_ENOMEM;
+  }
+  char* ws = (char*)workspace;
+  st::Partial* rec = (st::Partial*)ws;                     // 0..255
+  void* seq = ws + 256;                                     // 256..511
+  unsigned* done = (unsigned*)(ws + 512);                   // 512..767
+  st_stats* stats = (st_stats*)(ws + 1024);
+  double* partial = (double*)(ws + 1024 + ((sizeof(st_stats) + 255) & ~(size_t)255));
+  double* scratch = partial + 2 * (1 << ST_PW_MAX_DEPTH);
+  ST_CUDA_CHECK(cudaMemsetAsync(ws, 0, 1024, s));
+  ST_CUDA_CHECK(cudaMemsetAsync(stats, 0, sizeof(st_stats), s));
+  if (n > 0) {
+    st::k_count_finite<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
+        x, n, rec, stats);
+    ST_LAUNCH_CHECK("k_count_finite");
+    int rc = st_pw_means(x, x, n, rec, scratch, seq, partial, done, 1, stats, s);
+    if (rc) return rc;
+    ST_CUDA_CHECK(cudaMemcpyAsync(out, &stats->mean_energy[0], sizeof(double),
+                                  cudaMemcpyDeviceToDevice, s));
+  } else {
+    const double nan = NAN;
+    ST_CUDA_CHECK(cudaMemcpyAsync(out, &nan, sizeof(double), cudaMemcpyHostToDevice, s));
+    ST_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
   return ST_OK;
 }
