@@ -234,24 +234,14 @@ void launch_e_step(int K, int64_t n, cudaStream_t s, const st::EmCtx& c,
   }
 }
 
-// M-step launch: the 4-lanes-per-slot kernel on rectified rigs (same
-// outputs), the one-thread-per-slot kernel otherwise or with
-// ST_MSTEP_SCALAR set.  `grid_slots`: slots the grid must cover (a wave of
-// grid-stride blocks for worklists).  Returns the grid used.
-bool mstep_g4(const st::EmCtx& c) {
-  static const bool scalar = getenv("ST_MSTEP_SCALAR") != nullptr;
-  return c.rectified && !scalar;
-}
-
-unsigned mstep_blocks(const st::EmCtx& c, int64_t grid_slots) {
-  return blocks_for(std::max<int64_t>(grid_slots, 1), mstep_g4(c) ? EM_BLOCK / 4 : EM_BLOCK);
+// M-step launch: one thread per slot (`grid_slots`: slots the grid must
+// cover; a wave of grid-stride blocks for worklists).
+unsigned mstep_blocks(const st::EmCtx&, int64_t grid_slots) {
+  return blocks_for(std::max<int64_t>(grid_slots, 1), EM_BLOCK);
 }
 
 void launch_m_step(const st::EmCtx& c, const st::MStepArgs& a, unsigned grid, cudaStream_t s) {
-  if (mstep_g4(c))
-    st::k_m_step_g4<<<grid, EM_BLOCK, 0, s>>>(c, a);
-  else
-    st::k_m_step<<<grid, EM_BLOCK, 0, s>>>(c, a);
+  st::k_m_step<<<grid, EM_BLOCK, 0, s>>>(c, a);
 }
 
 }  // namespace
@@ -516,7 +506,7 @@ struct SolveLayout {
 static SolveLayout solve_layout(int W, int H) {
   SolveLayout L;
   const int64_t npx = (int64_t)W * H;
-  L.max_warps = (int)blocks_for(npx, EM_BLOCK / 4) * (EM_BLOCK / 32);  // k_m_step_g4's grid
+  L.max_warps = (int)blocks_for(npx, EM_BLOCK) * (EM_BLOCK / 32);
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                 (int)(npx + 1));
@@ -935,7 +925,8 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     }
     // one device: the iteration's energy means exactly as numpy sums them
     // (row bands keep the fixed-order record sums, summed over shards)
-    if (!A.exchange && n_cnt > 0) {
+    static const bool no_exact = getenv("ST_NO_EXACT_MEANS") != nullptr;  // (diagnostics)
+    if (!A.exchange && n_cnt > 0 && !no_exact) {
       const int rc = st_pw_means(e_act + A.cnt_lo, pe_act + A.cnt_lo, n_cnt, reduced + it,
                                  ws + L.pw_scratch, ws + L.pw_seq, (double*)(ws + L.pw_part),
                                  (unsigned*)(ws + L.pw_done), it, stats_dev, s);

@@ -467,218 +467,6 @@ __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
 // Iteration >= 2: which slots need a new M-step (mask changed since their
 // last one).  The others carry their previous-disparity energy (= their E)
 // and changed = 0 into the statistics.
-// ---------------------------------------------------------------------------
-// M-step, cooperative form for rectified rigs: a group of 4 lanes per slot.
-//
-// Same decisions and outputs as k_m_step, bit for bit (the winner is the
-// order-independent lexicographic (E, d) minimum; only the pruning order,
-// hence the energy_evals / energy_samples diagnostics, may differ):
-//   * lane q owns channels {2q, 2q+1, 2q+8, 2q+9} of every sample, so it
-//     forms r_{2q} = t_{2q} + t_{2q+8} and r_{2q+1}; numpy's 16-wide tree
-//     ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) (solver.py:253-256 `sum(axis=1)`)
-//     is then two xor-shuffles (IEEE addition is commutative, so every lane
-//     ends with the same bits): 4 channel sums per lane instead of 16, no
-//     shared-memory tap cache, 4x the resident warps of k_m_step;
-//   * candidates are screened 4 at a time, one per lane (radius test and the
-//     fp64 log prior, solver.py:341-347), and the survivors' energies are
-//     evaluated by the whole group in candidate order.
-#define G4 4
-__global__ void __launch_bounds__(EM_BLOCK, MSTEP_G4_MIN_BLOCKS) k_m_step_g4(EmCtx c, MStepArgs a) {
-  if (a.stop && *a.stop) return;  // converged (st_solve_async)
-  const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
-  const int lane = threadIdx.x & 31;
-  const int q = lane & (G4 - 1);
-  const int gbase = lane & ~(G4 - 1);
-  const unsigned gmask = 0xFu << gbase;
-  long long n_cand = 0, n_eval = 0, n_hopeless = 0, n_samples = 0;
-  const double pen = dmul(c.p.beta, variance_ceiling());
-  const int K = c.rig.num_views;
-  const int slots_per_block = EM_BLOCK / G4;
-  // this lane's two descriptor words and halfword
-  const int wlo = q >> 1;
-  const uint32_t sel = (q & 1) ? 0x7632u : 0x5410u;  // halfword 1 / 0 of each word
-  for (int64_t base = (int64_t)blockIdx.x * slots_per_block; base < n_work;
-       base += (int64_t)gridDim.x * slots_per_block) {
-  const int64_t t = base + (threadIdx.x >> 2);
-  const bool live = t < n_work;
-  const int64_t i = live ? (a.list ? (int64_t)a.list[t] : t) : 0;
-  bool want_e = false;
-  if (live) {
-    const int64_t pix = a.active ? a.active[i] : c.pix0 + i;
-    const int x = (int)(pix % c.W), y = (int)(pix / c.W);
-    const double u = (double)x, v = (double)y;
-    const double mu = c.mu[pix];
-    const uint32_t bits = a.static_all[pix];
-    const double dmax = c.p.d_max;
-    const bool hopeless = __popc(bits & c.view_bits) < c.p.min_static_rays;
-    if (q == 0) n_hopeless += hopeless;
-    const uint32_t row = (uint32_t)y * (uint32_t)c.W;
-    // exact energy of candidate d (group-uniform result)
-    auto energy = [&](double d, double lp, double& e, bool& real) {
-      if (hopeless) {
-        real = false;
-        e = dsub(pen, lp);
-        return;
-      }
-      int cnt = 0;
-      for (int k = 0; k < K; ++k) {
-        if (!((bits >> k) & 1u)) continue;
-        if (in_margin(c.rig, k, warp_ctx(c, k, u, v, d))) ++cnt;
-      }
-      real = cnt >= c.p.min_static_rays;
-      if (!real) {
-        e = dsub(pen, lp);
-        return;
-      }
-      if (q == 0) n_samples += cnt;
-      double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int k = 0; k < K; ++k) {
-        if (!((bits >> k) & 1u)) continue;
-        const WarpOut w = warp_ctx(c, k, u, v, d);
-        if (!in_margin(c.rig, k, w)) continue;
-        const double fl = floor(w.pu);
-        const double fu = dsub(w.pu, fl);
-        const uint4* pl = c.desc + ((uint32_t)k * (uint32_t)c.HW + row + (uint32_t)(int)fl);
-        const uint4 ta = __ldg(pl), tb = __ldg(pl + 1);
-        // this lane's bytes 2q, 2q+1, 2q+8, 2q+9 packed in channel order
-        const uint32_t wa = __byte_perm(wlo ? ta.y : ta.x, wlo ? ta.w : ta.z, sel);
-        const uint32_t wb = __byte_perm(wlo ? tb.y : tb.x, wlo ? tb.w : tb.z, sel);
-        double f[4];
-        lerp_word(wa, wb, fu, f);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          s1[j] = dadd(s1[j], f[j]);
-          s2[j] = dadd(s2[j], dmul(f[j], f[j]));
-        }
-      }
-      const double nn = (double)cnt;
-      const double rn = c.recip[cnt];
-      double tt[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) tt[j] = dsub(s2[j], div_small(dmul(s1[j], s1[j]), nn, rn));
-      // r_{2q} = t_{2q} + t_{2q+8}, r_{2q+1} = t_{2q+1} + t_{2q+9}
-      const double pr = dadd(dadd(tt[0], tt[2]), dadd(tt[1], tt[3]));
-      const double h1 = dadd(pr, __shfl_xor_sync(gmask, pr, 1));
-      const double sum = dadd(h1, __shfl_xor_sync(gmask, h1, 2));
-      const double var = fmax(div_small(sum, nn, rn), 0.0);
-      e = dsub(dmul(c.p.beta, var), lp);
-    };
-    auto radius = [&](double best) -> double {
-      if (c.exhaustive) return INFINITY;
-      if (!hopeless) return prune_radius(best, c.sigma_f, c.gamma_f);
-      return prune_radius(dadd(dsub(best, pen), 1e-12 * (1.0 + fabs(pen))), c.sigma_f,
-                          c.gamma_f);
-    };
-    double be = INFINITY, bd = INFINITY;
-    bool br = false;
-    double lim = INFINITY;
-    double dp = NAN, pe = NAN;
-    if (!a.first) {
-      dp = a.d[i];
-      if (!isnan(dp)) {
-        double e;
-        bool real;
-        energy(dp, log_prior(dp, mu, c.p.sigma, c.p.gamma, c.inv_sigma), e, real);
-        pe = e;
-        be = e;
-        bd = dp;
-        br = real;
-        lim = radius(be);
-      }
-    }
-    // four candidates at once: lane q screens d_q, then the group evaluates
-    // the survivors in candidate order
-    auto offer4 = [&](double dq, bool valid) {
-      n_cand += valid;
-      bool pass = false;
-      double lp = 0.0;
-      if (valid && !(fabs(dq - mu) > lim) && dq != bd) {
-        lp = log_prior(dq, mu, c.p.sigma, c.p.gamma, c.inv_sigma);
-        pass = (-lp <= be) || c.exhaustive;
-      }
-      unsigned m = (__ballot_sync(gmask, pass) >> gbase) & 0xFu;
-      while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        const double d = __shfl_sync(gmask, dq, gbase + j);
-        const double l = __shfl_sync(gmask, lp, gbase + j);
-        if (fabs(d - mu) > lim || d == bd) continue;
-        if (!(-l <= be) && !c.exhaustive) continue;
-        if (q == 0) ++n_eval;
-        double e;
-        bool real;
-        energy(d, l, e, real);
-        if (e < be || (e == be && d < bd)) {
-          be = e;
-          bd = d;
-          br = real;
-          lim = radius(be);
-        }
-      }
-    };
-    // band mu + 0.5 j, nearest first (solver.py:187-191, 360-363)
-    for (int j0 = 0; j0 < c.n_band; j0 += G4) {
-      const int j = j0 + q;
-      const double d = j < c.n_band ? dadd(mu, c.band[j]) : 0.0;
-      offer4(d, j < c.n_band && d > 0.0 && d <= dmax);
-    }
-    // coarse sweep 1, 5, 9, ... (solver.py:192, 364-365)
-    for (int j0 = 0; j0 < c.n_coarse; j0 += G4) {
-      const int j = j0 + q;
-      offer4(dadd(1.0, dmul(4.0, (double)j)), j < c.n_coarse);
-    }
-    // support disparities within the radius (solver.py:286-321, 373-400)
-    if (c.sup_tile_start) {
-      const int tile = (y / ST_TH) * c.tiles_x + (x / ST_TW);
-      const uint32_t g0 = __ldg(c.sup_tile_start + tile), g1 = __ldg(c.sup_tile_start + tile + 1);
-      const int srow = y % ST_TH, scol = x % ST_TW;
-      for (uint32_t gs = g0; gs < g1; gs += G4) {
-        const uint32_t g = gs + q;
-        const bool on = g < g1 && ((__ldg(c.sup_mask + (size_t)g * ST_TH + srow) >> scol) & 1u);
-        offer4(on ? (double)__ldg(c.sup_value + g) : 0.0, on);
-      }
-    }
-    uint8_t status = ST_STATUS_VALID;
-    if (!isfinite(be)) {
-      status = ST_STATUS_LOW_TEXTURE;
-      bd = NAN;
-    } else if (!br) {
-      status = ST_STATUS_NO_STATIC_EVIDENCE;
-    }
-    if (!a.first) {
-      want_e = status != ST_STATUS_LOW_TEXTURE &&
-               __double_as_longlong(bd) != __double_as_longlong(dp);
-    } else {
-      want_e = status != ST_STATUS_LOW_TEXTURE;
-    }
-    if (q == 0) {
-      if (!a.first) {
-        a.pe[i] = pe;
-        a.chg[i] = fabs(bd - dp) > 0.5 ? 1 : 0;  // NaN -> False (solver.py:472-475)
-      }
-      a.d[i] = bd;
-      a.e[i] = be;
-      a.status[i] = status;
-      if (a.mask_in) a.mask_in[i] = bits;
-    }
-  }
-  if (a.elist) list_append(want_e && q == 0, (int32_t)i, a.elist, a.elist_count);
-  }
-  if (a.partials) {
-    const long long c_cand = warp_sum(n_cand);
-    const long long c_eval = warp_sum(n_eval);
-    const long long c_hopeless = warp_sum(n_hopeless);
-    const long long c_samples = warp_sum(n_samples);
-    if (lane == 0) {
-      Partial& P = a.partials[(blockIdx.x * blockDim.x + threadIdx.x) >> 5];
-      P.n_cand = c_cand;
-      P.n_eval = c_eval;
-      P.n_hopeless = c_hopeless;
-      P.n_samples = c_samples;
-    }
-  }
-}
-
 __global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n, int64_t pix0,
                              const uint32_t* __restrict__ static_all,
                              const uint32_t* __restrict__ mask_in, const double* __restrict__ e,

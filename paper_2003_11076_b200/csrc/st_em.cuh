@@ -15,9 +15,6 @@
 #define MSTEP_MIN_BLOCKS 5
 #endif
 #define MSTEP_BOUNDS __launch_bounds__(EM_BLOCK, MSTEP_MIN_BLOCKS)
-#ifndef MSTEP_G4_MIN_BLOCKS
-#define MSTEP_G4_MIN_BLOCKS 6  // <= 80 registers
-#endif
 #define STATS_BLOCK 256
 #ifndef STATS_GRID
 #define STATS_GRID (148 * 2)  // fixed grid of k_em_stats: deterministic sums (measured best)
@@ -113,8 +110,6 @@ struct EStepArgs {
 };
 
 __global__ void k_m_step(EmCtx c, MStepArgs a);
-// rectified rigs: 4 lanes per slot (same outputs as k_m_step)
-__global__ void k_m_step_g4(EmCtx c, MStepArgs a);
 __global__ void k_flag_mstep(const int64_t* active, int64_t n, int64_t pix0,
                              const uint32_t* static_all,
                              const uint32_t* mask_in, const double* e, double* pe, uint8_t* chg,

@@ -33,7 +33,6 @@
 namespace st {
 
 #define PW_LEAF 128
-#define PW_MAX_LEAVES 256
 #define PW_THREADS 256
 
 __device__ __forceinline__ int64_t pw_split(int64_t n) {
@@ -60,36 +59,6 @@ __device__ double pw_leaf(const double* __restrict__ a, int64_t n) {
   return res;
 }
 
-// The recursion over a node of size n whose leaves (size <= PW_LEAF, or
-// depth == max_depth) have sums leaf[k], k in DFS order: one thread.
-__device__ double pw_combine(int64_t n, int max_depth, const double* leaf) {
-  int64_t sz[64];
-  double acc[64];
-  uint8_t st[64];
-  int sp = 0, k = 0;
-  sz[0] = n;
-  for (;;) {
-    while (sz[sp] > PW_LEAF && sp < max_depth) {
-      st[sp] = 0;
-      sz[sp + 1] = pw_split(sz[sp]);
-      ++sp;
-    }
-    double ret = leaf[k++];
-    for (;;) {
-      if (sp == 0) return ret;
-      --sp;
-      if (st[sp] == 0) {  // left child done: its right sibling next
-        acc[sp] = ret;
-        st[sp] = 1;
-        sz[sp + 1] = sz[sp] - pw_split(sz[sp]);
-        ++sp;
-        break;
-      }
-      ret = dadd(acc[sp], ret);
-    }
-  }
-}
-
 struct PwSeq {
   const double* src;
   int64_t m;
@@ -101,7 +70,9 @@ __global__ void __launch_bounds__(1024) k_pw_prepare(const double* __restrict__ 
                                                      const double* __restrict__ pe, int64_t n,
                                                      const Partial* __restrict__ rec,
                                                      double* __restrict__ scratch, PwSeq* seq,
-                                                     int with_prev) {
+                                                     int with_prev, int it,
+                                                     const st_stats* __restrict__ stats) {
+  if (stats->iterations_run != it) return;  // the iteration did not run (converged before)
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int64_t base;
@@ -130,31 +101,80 @@ __global__ void __launch_bounds__(1024) k_pw_prepare(const double* __restrict__ 
   }
 }
 
+// Node (s, n) at depth t along the t low bits of `path` (MSB first) below
+// (s0, n0); false when an ancestor is already a leaf (size <= PW_LEAF).
+__device__ __forceinline__ bool pw_descend(int64_t s0, int64_t n0, int t, unsigned path,
+                                           int64_t& s, int64_t& n) {
+  s = s0;
+  n = n0;
+  for (int d = 0; d < t; ++d) {
+    if (n <= PW_LEAF) return false;
+    const int64_t n2 = pw_split(n);
+    if ((path >> (t - 1 - d)) & 1u) {
+      s += n2;
+      n -= n2;
+    } else {
+      n = n2;
+    }
+  }
+  return true;
+}
+
+#define PW_MAX_LEVELS 11  // node depth below a block root / top depth D: <= 10
+
+// The recursion below (s0, n0) evaluated level by level, deepest first: node
+// (t, p) = val[2^t - 1 + p] is a leaf sum when its size is <= PW_LEAF (or
+// when t == cut, with its value from `cut_val(p)`), else the sum of its two
+// children.  Every addition is the recursion's own (left + right).
+template <typename CutVal>
+__device__ double pw_levels(const double* __restrict__ a, int64_t s0, int64_t n0, int cut,
+                            CutVal cut_val, double* val) {
+  int depth = 0;  // deepest level with a node
+  {
+    int64_t n = n0;
+    while (n > PW_LEAF && depth < cut) {
+      n = n - pw_split(n);  // the right child is the larger half
+      ++depth;
+    }
+  }
+  for (int t = depth; t >= 0; --t) {
+    const unsigned cnt = 1u << t;
+    for (unsigned p = threadIdx.x; p < cnt; p += blockDim.x) {
+      int64_t s, n;
+      if (!pw_descend(s0, n0, t, p, s, n)) continue;
+      double v;
+      if (t == cut)
+        v = cut_val(p);
+      else if (n <= PW_LEAF)
+        v = a ? pw_leaf(a + s, n) : cut_val(p << (cut - t));
+      else
+        v = dadd(val[(2u << t) - 1 + 2 * p], val[(2u << t) + 2 * p]);
+      val[cnt - 1 + p] = v;
+    }
+    __syncthreads();
+  }
+  return val[0];
+}
+
 // gridDim.x = 2^D nodes, gridDim.y = 1 (E) or 2 (E and previous E).
 __global__ void __launch_bounds__(PW_THREADS) k_pw_mean(const PwSeq* __restrict__ seq, int D,
                                                         int it, double* __restrict__ partial,
                                                         unsigned* __restrict__ done,
                                                         st_stats* __restrict__ stats) {
   if (stats->iterations_run != it) return;  // the iteration did not run (converged before)
+  __shared__ double val[(1 << PW_MAX_LEVELS) - 1];
   const int y = blockIdx.y;
   const PwSeq q = seq[y];
   const int nb = gridDim.x;
-  __shared__ int64_t leaf_s[PW_MAX_LEAVES], leaf_n[PW_MAX_LEAVES];
-  __shared__ double leaf_v[PW_MAX_LEAVES];
-  __shared__ int n_leaves;
-  __shared__ int64_t node_s, node_n;
-  __shared__ int node_depth;
-  __shared__ bool owner;
-  if (threadIdx.x == 0) {
-    // descend the top D levels along this block's path; an early leaf
-    // (size <= PW_LEAF) belongs to the path whose remaining bits are zero
-    int64_t s = 0, n = q.m;
+  // this block's node: D levels down along its index; an early leaf belongs
+  // to the lowest path under it
+  int64_t s = 0, n = q.m;
+  bool own = true;
+  {
     int d = 0;
-    bool own = true;
     while (d < D && n > PW_LEAF) {
-      const int bit = (blockIdx.x >> (D - 1 - d)) & 1;
       const int64_t n2 = pw_split(n);
-      if (bit) {
+      if ((blockIdx.x >> (D - 1 - d)) & 1u) {
         s += n2;
         n -= n2;
       } else {
@@ -163,104 +183,34 @@ __global__ void __launch_bounds__(PW_THREADS) k_pw_mean(const PwSeq* __restrict_
       ++d;
     }
     if (d < D && (blockIdx.x & ((1u << (D - d)) - 1u)) != 0) own = false;
-    owner = own;
-    node_s = s;
-    node_n = n;
-    node_depth = d;
-    // enumerate the node's leaves in DFS order
-    int cnt = 0;
-    if (own) {
-      int64_t st_s[64], st_n[64];
-      int sp = 0;
-      st_s[0] = s;
-      st_n[0] = n;
-      while (sp >= 0) {
-        const int64_t a = st_s[sp], b = st_n[sp];
-        --sp;
-        if (b > PW_LEAF) {
-          const int64_t b2 = pw_split(b);
-          ++sp;  // right child below the left one: the left pops first
-          st_s[sp] = a + b2;
-          st_n[sp] = b - b2;
-          ++sp;
-          st_s[sp] = a;
-          st_n[sp] = b2;
-        } else if (cnt < PW_MAX_LEAVES) {
-          leaf_s[cnt] = a;
-          leaf_n[cnt] = b;
-          ++cnt;
-        }
-      }
-    }
-    n_leaves = cnt;
   }
-  __syncthreads();
-  if (owner) {
-    for (int l = threadIdx.x; l < n_leaves; l += blockDim.x)
-      leaf_v[l] = q.m > 0 ? pw_leaf(q.src + leaf_s[l], leaf_n[l]) : 0.0;
+  if (own) {
+    const double v = q.m > 0 ? pw_levels(q.src, s, n, PW_MAX_LEVELS - 1,
+                                         [&](unsigned) { return 0.0; }, val)
+                             : 0.0;
+    if (threadIdx.x == 0) partial[(size_t)y * nb + blockIdx.x] = v;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    partial[(size_t)y * nb + blockIdx.x] =
-        owner ? pw_combine(node_n, 64, leaf_v) : 0.0;
-    (void)node_s;
-    (void)node_depth;
-    __threadfence();
-  }
-  // the last block of this sequence replays the top D levels
   __shared__ bool last;
-  if (threadIdx.x == 0) last = atomicAdd(done + y, 1u) == (unsigned)nb - 1;
-  __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  __threadfence();
-  done[y] = 0u;
-  // top-level leaves in DFS order = the owning blocks in increasing path order
-  // (a node that became a leaf early owns the lowest path under it)
-  double* part = partial + (size_t)y * nb;
-  int64_t sz[64];
-  int path[64];
-  double acc[64];
-  uint8_t stt[64];
-  int sp = 0;
-  sz[0] = q.m;
-  path[0] = 0;
-  double total;
-  for (;;) {
-    while (sp < D && sz[sp] > PW_LEAF) {
-      stt[sp] = 0;
-      sz[sp + 1] = pw_split(sz[sp]);
-      path[sp + 1] = path[sp] << 1;
-      ++sp;
-    }
-    double ret = part[(int64_t)path[sp] << (D - sp)];
-    bool finished = false;
-    for (;;) {
-      if (sp == 0) {
-        finished = true;
-        break;
-      }
-      --sp;
-      if (stt[sp] == 0) {
-        acc[sp] = ret;
-        stt[sp] = 1;
-        sz[sp + 1] = sz[sp] - pw_split(sz[sp]);
-        path[sp + 1] = (path[sp] << 1) | 1;
-        ++sp;
-        break;
-      }
-      ret = dadd(acc[sp], ret);
-    }
-    if (finished) {
-      total = ret;
-      break;
-    }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done + y, 1u) == (unsigned)nb - 1;
   }
-  const double sum = dadd(0.0, total);
-  const double mean = q.m > 0 ? ddiv(sum, (double)q.m) : NAN;
-  if (y == 0)
-    stats->mean_energy[it - 1] = mean;
-  else
-    stats->prev_energy[it - 2] = mean;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // the top D levels over the blocks' sums (a top-level leaf at depth t, path
+  // p, was written by block p << (D - t))
+  const double* part = partial + (size_t)y * nb;
+  const double total = pw_levels(nullptr, 0, q.m, D,
+                                 [&](unsigned p) { return part[p]; }, val);
+  if (threadIdx.x == 0) {
+    done[y] = 0u;
+    const double mean = q.m > 0 ? ddiv(dadd(0.0, total), (double)q.m) : NAN;
+    if (y == 0)
+      stats->mean_energy[it - 1] = mean;
+    else
+      stats->prev_energy[it - 2] = mean;
+  }
 }
 
 }  // namespace st
@@ -272,10 +222,10 @@ int st_pw_means(const double* e, const double* pe, int64_t n, const void* rec, v
   if (n <= 0) return ST_OK;
   const int with_prev = it > 1 ? 1 : 0;
   st::k_pw_prepare<<<1, 1024, 0, s>>>(e, pe, n, (const st::Partial*)rec, (double*)scratch,
-                                       (st::PwSeq*)seq, with_prev);
+                                       (st::PwSeq*)seq, with_prev, it, stats);
   ST_LAUNCH_CHECK("k_pw_prepare");
-  int D = 0;
-  while (D < ST_PW_MAX_DEPTH && (n >> D) > 4096) ++D;
+  int D = 0;  // <= 10 top levels: nodes of ~4k values (<= 128 k up to 2^27 values)
+  while (D < 10 && (n >> D) > 4096) ++D;
   st::k_pw_mean<<<dim3(1u << D, 1 + with_prev), PW_THREADS, 0, s>>>(
       (const st::PwSeq*)seq, D, it, partial, done, stats);
   ST_LAUNCH_CHECK("k_pw_mean");

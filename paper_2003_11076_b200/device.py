@@ -71,6 +71,37 @@ def download(x, out=None):
     return host.numpy()
 
 
+def upload_views(views, np_dtype):
+    """A list of equally shaped host arrays -> one (K, ...) CUDA tensor, each
+    view copied straight into its slice (no host-side np.stack)."""
+    t = torch()
+    first = np.asarray(views[0])
+    out = t.empty((len(views),) + first.shape, dtype=_TORCH_OF[np.dtype(np_dtype)], device=dev())
+    for k, v in enumerate(views):
+        a = np.ascontiguousarray(v, dtype=np_dtype)
+        out[k].copy_(t.from_numpy(a), non_blocking=False)
+    return out
+
+
+def download_many(xs):
+    """Several CUDA tensors -> numpy arrays through ONE pinned block, one
+    synchronisation (the arrays are views of distinct parts of the block)."""
+    t = torch()
+    sizes = [x.numel() * x.element_size() for x in xs]
+    offs, total = [], 0
+    for n in sizes:
+        offs.append(total)
+        total += (n + 255) & ~255
+    block = t.empty((max(total, 1),), dtype=t.uint8, pin_memory=True)
+    outs = []
+    for x, o, n in zip(xs, offs, sizes):
+        h = block[o:o + n].view(x.dtype).view(x.shape)
+        h.copy_(x, non_blocking=True)
+        outs.append(h)
+    t.cuda.current_stream().synchronize()
+    return [h.numpy() for h in outs]
+
+
 def _torch_dtypes():
     t = torch()
     return {np.dtype(np.uint8): t.uint8, np.dtype(np.int32): t.int32,

@@ -62,9 +62,11 @@ class DeviceFrame:
 
     def __init__(self, images, priors):
         t = require_cuda()
-        self.images = upload(images if isinstance(images, t.Tensor) else np.stack(images), np.uint8)
-        self.priors = upload(priors if isinstance(priors, t.Tensor) else np.stack(priors),
-                             np.float32)
+        from .device import upload_views
+        self.images = (upload(images, np.uint8) if isinstance(images, t.Tensor)
+                       else upload_views(images, np.uint8))
+        self.priors = (upload(priors, np.float32) if isinstance(priors, t.Tensor)
+                       else upload_views(priors, np.float32))
         if self.images.dim() == 3:
             self.images = self.images.unsqueeze(-1).expand(-1, -1, -1, 3).contiguous()
         self.K, self.H, self.W = (int(x) for x in self.images.shape[:3])

@@ -99,4 +99,6 @@ def synthesize(frame, rig, disparity, seg, min_static_rays=2, median_radius=1, c
     bits = upload(np.asarray(seg.static_bits, dtype=np.uint32).view(np.int32))
     img, prov, nr = synthesize_device(frame, rig, values, status, bits, min_static_rays,
                                       median_radius, copy_mask)
-    return download(img), download(prov), download(nr)
+    from .device import download_many
+    img, prov, nr = download_many((img, prov, nr))
+    return img, prov, nr

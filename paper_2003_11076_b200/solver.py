@@ -288,10 +288,12 @@ class DisparitySolver:
         return (values, status, sbits, vbits), _stats_of(stats)
 
     def solve(self, dynamic_only=False):
+        from .device import download_many
         (values, status, sbits, vbits), stats = self.solve_device(dynamic_only)
-        disparity = DisparityMap(values=download(values), status=download(status))
-        seg = SegmentationState(static_bits=download(sbits).view(np.uint32),
-                                valid_bits=download(vbits).view(np.uint32))
+        values, status, sbits, vbits = download_many((values, status, sbits, vbits))
+        disparity = DisparityMap(values=values, status=status)
+        # the E-step only sets static bits of valid rays (no host subset scan)
+        seg = SegmentationState._device_result(sbits.view(np.uint32), vbits.view(np.uint32))
         return disparity, seg, stats
 
 

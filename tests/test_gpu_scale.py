@@ -112,34 +112,6 @@ def test_screened_em_equals_exhaustive(st, monkeypatch, cfg):
     assert list(a.stats.mean_energy) == list(b.stats.mean_energy)
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3"])
-def test_mstep_group_kernel_equals_scalar(st, monkeypatch, cfg):
-    """k_m_step_g4 (4 lanes per pixel, rectified rigs) decides exactly what
-    the one-thread-per-pixel k_m_step decides, whole frame, 5 forced
-    iterations."""
-    frame, rig, tri, sp, pp = _inputs(cfg)
-    a = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=5)
-    monkeypatch.setenv("ST_MSTEP_SCALAR", "1")
-    import subprocess
-    import sys
-    import json
-    code = (
-        "import sys, json, numpy as np; sys.path.insert(0, '.'); import bench, "
-        "paper_2003_11076_b200 as st; "
-        f"f, r, t, _ = bench.load_inputs('{cfg}'); sp, pp = bench.params_for('{cfg}'); "
-        "x = st.reconstruct(f, r, t, sp, pp, forced_iters=5); "
-        "np.savez('/tmp/_mstep_scalar.npz', v=x.disparity.values, s=x.segmentation.static_bits, "
-        "i=x.image); print(json.dumps(list(x.stats.mean_energy)))")
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
-                         env=dict(__import__("os").environ, ST_MSTEP_SCALAR="1"), check=True)
-    me = json.loads(out.stdout.strip().splitlines()[-1])
-    z = np.load("/tmp/_mstep_scalar.npz")
-    assert np.array_equal(a.disparity.values, z["v"])
-    assert np.array_equal(a.segmentation.static_bits, z["s"])
-    assert np.array_equal(a.image, z["i"])
-    assert list(a.stats.mean_energy) == me
-
-
 @pytest.mark.parametrize("forced", [0, 5])
 def test_async_solve_equals_sync(st, forced):
     """st_solve_async (device-side convergence test and statistics, no host
