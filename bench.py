@@ -905,6 +905,20 @@ def run_ours(args):
             pipes = dict(pipes, source=tj.get("source"),
                          note="the bound that binds: FP64 issue + latency, not HBM")
 
+    # the bound that binds k_m_step: FP64 issue.  The device's DFMA peak is
+    # measured here; the kernel's FP64 flops per launch come from the ncu
+    # capture summarised in profiles/traffic_<cfg>.json
+    fp64_peak = N.C.c_double(0.0)
+    N.check(lib.st_fp64_peak(N.C.byref(fp64_peak), N.stream_handle()))
+    fp64 = {"peak_tflops": fp64_peak.value, "peak_source": "measured (st_fp64_peak: 8 "
+            "independent DFMA chains per thread)"}
+    if prof and os.path.exists(prof):
+        tj = json.load(open(prof))
+        fl = tj.get("k_m_step_fp64_flops_per_launch")
+        if fl:
+            fp64["k_m_step_flops_per_launch"] = fl
+            fp64["k_m_step_tflops"] = fl / (ms_m / max(1, n_m) / 1e3) / 1e12
+            fp64["frac"] = fp64["k_m_step_tflops"] / fp64_peak.value
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_block(frame, rig, tri, cfg)
@@ -923,7 +937,7 @@ def run_ours(args):
         "config": config_block(cfg, args, exact),
         "roofline": {"bound": "hbm", "kernel": "k_m_step", "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "pipes": pipes,
+                     "traffic": traffic, "pipes": pipes, "fp64": fp64,
                      "algorithmic_bytes_per_launch": bytes_m / max(1, n_m),
                      "unit_note": "16 B per descriptor sample the kernel takes: (pixel, "
                                   "evaluated real candidate, static in-margin view), "

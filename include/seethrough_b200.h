@@ -114,6 +114,10 @@ int64_t st_launch_count(void);
  * returns the number of bit mismatches (expected 0). */
 int st_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* mismatches, void* stream);
 
+/* Diagnostics: measured FP64 (DFMA) throughput of this device in TFLOP/s
+ * (8 independent FMA chains per thread, best of 5; synchronises). */
+int st_fp64_peak(double* tflops, void* stream);
+
 /* ---- L1 primitives ---------------------------------------------------- */
 
 /* features.py:81-104 compute_descriptors (with rgb_to_gray :29-36 and

@@ -100,6 +100,7 @@ _SIGS = {
     "st_device_count": (C.c_int, []),
     "st_launch_count": (C.c_int64, []),
     "st_struct_size": (C.c_int64, [_I32]),
+    "st_fp64_peak": (C.c_int, [C.POINTER(C.c_double), _P]),
     "st_selftest": (C.c_int, [_I32, _I64, C.c_uint64, C.POINTER(C.c_int64), _P]),
     "st_descriptors": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
     "st_bilinear": (C.c_int, [_P, _I32, _I32, _I32, _P, _P, _I64, _P, _P]),

@@ -318,9 +318,59 @@ __global__ void k_selftest_div(int64_t n, unsigned long long seed,
   }
 }
 
+// FP64 throughput probe: 8 independent DFMA chains per thread (the pipe's
+// latency hidden), 2 flops per DFMA.  Output kept live through `sink`.
+__global__ void __launch_bounds__(256) k_fp64_peak(int iters, double seed, double* sink) {
+  double a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = seed + threadIdx.x * 1e-9 + j;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = __fma_rn(a[j], m, c);
+  }
+  double t = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) t += a[j];
+  if (t == 12345.678) *sink = t;
+}
+
 }  // namespace st
 
 extern "C" {
+
+int st_fp64_peak(double* tflops, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  double* sink = nullptr;
+  ST_CUDA_CHECK(cudaMallocAsync(&sink, sizeof(double), s));
+  cudaEvent_t e0, e1;
+  ST_CUDA_CHECK(cudaEventCreate(&e0));
+  ST_CUDA_CHECK(cudaEventCreate(&e1));
+  int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  st::k_fp64_peak<<<blocks, threads, 0, s>>>(64, 1.0, sink);  // warm-up
+  ST_LAUNCH_CHECK("k_fp64_peak");
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0, s);
+    st::k_fp64_peak<<<blocks, threads, 0, s>>>(iters, 1.0 + r, sink);
+    ST_LAUNCH_CHECK("k_fp64_peak");
+    cudaEventRecord(e1, s);
+    ST_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ST_CUDA_CHECK(cudaFreeAsync(sink, s));
+  ST_CUDA_CHECK(cudaStreamSynchronize(s));
+  *tflops = 2.0 * 8.0 * (double)iters * blocks * threads / (best * 1e-3) / 1e12;
+  return ST_OK;
+}
 
 int st_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* mismatches, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
@@ -498,7 +548,7 @@ int st_masked_variance(const double* desc, const uint8_t* mask, int64_t n, int32
 
 struct SolveLayout {
   size_t d, e, pe, st_act, chg, mask_in, mlist, elist, counts, flist, active, flags, offs,
-      work, parts, reduced, cub, pw_part, pw_done, pw_seq, pw_scratch, total;
+      work, parts, reduced, cub, pw_scratch, pw_val, total;
   size_t cub_bytes;
   int max_warps;
 };
@@ -529,10 +579,8 @@ static SolveLayout solve_layout(int W, int H) {
   L.parts = o;    o += align_up(sizeof(st::Partial) * L.max_warps);
   L.reduced = o;  o += align_up(sizeof(st::Partial) * (ST_MAX_ITERS + 2));
   L.cub = o;      o += align_up(L.cub_bytes);
-  L.pw_part = o;  o += align_up(sizeof(double) * 2 * (1 << ST_PW_MAX_DEPTH));
-  L.pw_done = o;  o += align_up(sizeof(unsigned) * 2);
-  L.pw_seq = o;   o += align_up(32);
-  L.pw_scratch = o; o += align_up(sizeof(double) * 2 * npx);
+  L.pw_scratch = o; o += align_up(sizeof(double) * npx);
+  L.pw_val = o;   o += align_up(sizeof(double) * st::pw_val_size(npx));
   L.total = o;
   return L;
 }
@@ -579,6 +627,8 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
   memset(stats, 0, sizeof(*stats));
   stats->converged_after = -1;
   EventSet ev(p->timing != 0);
+  // the stats kernel's block counter (word 13) starts at zero
+  ST_CUDA_CHECK(cudaMemsetAsync(counts + 12, 0, 4 * sizeof(uint32_t), s));
   double* eps_logs = (double*)(counts + 4);
   st::k_eps_logs<<<1, 32, 0, s>>>(p->epsilon_prior, eps_logs);
   ST_LAUNCH_CHECK("k_eps_logs");
@@ -683,13 +733,25 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
       launch_e_step(rig->num_views, n_act, s, c, e);
       ST_LAUNCH_CHECK("k_e_step_at");
       ev.record(2, s);
-      const int sblk = std::min((int)blocks_for(n_act, STATS_BLOCK), STATS_GRID);
-      st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(n_act, it > 1, e_act, pe_act, chg, work,
-                                                  (int)mstep_blocks(c, n_act) * (EM_BLOCK / 32),
-                                                  parts);
+      // statistics in numpy's summation order, folded by the last block into
+      // reduced[it] (the host loop reads the worklist counts itself)
+      st::StatsTail tail = {};
+      tail.on = 1;
+      tail.it = it;
+      tail.done = counts + 13;
+      tail.reduced = reduced;
+      tail.counts = counts;
+      tail.record_only = 1;
+      tail.keep_counts = 1;
+      tail.record_n_act = n_act;
+      tail.record_slots = n_act;
+      tail.pw_depth = st::stats_depth(n_act);
+      tail.pw_scratch = (double*)(ws + L.pw_scratch);
+      tail.pw_val = (double*)(ws + L.pw_val);
+      st::k_em_stats<<<1 << tail.pw_depth, STATS_BLOCK, 0, s>>>(
+          n_act, it > 1, e_act, pe_act, chg, work,
+          (int)mstep_blocks(c, n_act) * (EM_BLOCK / 32), parts, nullptr, tail);
       ST_LAUNCH_CHECK("k_em_stats");
-      st::k_reduce_partials<<<1, 256, 0, s>>>(parts, sblk, reduced + it);
-      ST_LAUNCH_CHECK("k_reduce_partials");
       ev.record(3, s);
       stats->kernel_launches[0] += 1;
       stats->kernel_launches[1] += 1;
@@ -795,7 +857,6 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
   ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t) + sizeof(int), s));
   // E-step fallback count (byte 48) and the stats kernel's block counter (52)
   ST_CUDA_CHECK(cudaMemsetAsync(counts + 12, 0, 4 * sizeof(uint32_t), s));
-  ST_CUDA_CHECK(cudaMemsetAsync(ws + L.pw_done, 0, sizeof(unsigned) * 2, s));
   st::k_stats_init<<<1, 32, 0, s>>>(stats_dev, n_cnt);
   ST_LAUNCH_CHECK("k_stats_init");
   double* eps_logs = (double*)(counts + 4);
@@ -813,7 +874,8 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
 
   const int iters = p->forced_iters > 0 ? p->forced_iters : p->max_iters;
   const int nblk = std::max(1, (int)blocks_for(n, EM_BLOCK));
-  const int sblk = std::max(1, std::min((int)blocks_for(n_cnt, STATS_BLOCK), STATS_GRID));
+  const int pw_d = st::stats_depth(n_cnt);
+  const int sblk = 1 << pw_d;  // numpy's pairwise tree, top levels (st_pw.cuh)
   // iterations >= 2 work on device-counted worklists (a fraction of the
   // pixels) and do nothing once converged: a fixed grid of grid-stride
   // blocks (16 per SM measured best: the worklists' items are latency-bound)
@@ -902,6 +964,9 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     tail.record_only = A.band ? 1 : 0;
     tail.record_n_act = n_cnt;
     tail.record_slots = n;
+    tail.pw_depth = pw_d;
+    tail.pw_scratch = (double*)(ws + L.pw_scratch);
+    tail.pw_val = (double*)(ws + L.pw_val);
     st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(
         n_cnt, it > 1, e_act + A.cnt_lo, pe_act + A.cnt_lo, chg + A.cnt_lo, work,
         (n > 0 ? (it == 1 ? mblk : it == 2 ? mwave2 : std::min(mblk, 148 * 4)) : 0) *
@@ -922,15 +987,6 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
       st::k_band_control<<<1, 32, 0, s>>>(it, recs, A.exchange ? A.world : 1, p->forced_iters,
                                           stats_dev, stop);
       ST_LAUNCH_CHECK("k_band_control");
-    }
-    // one device: the iteration's energy means exactly as numpy sums them
-    // (row bands keep the fixed-order record sums, summed over shards)
-    static const bool no_exact = getenv("ST_NO_EXACT_MEANS") != nullptr;  // (diagnostics)
-    if (!A.exchange && n_cnt > 0 && !no_exact) {
-      const int rc = st_pw_means(e_act + A.cnt_lo, pe_act + A.cnt_lo, n_cnt, reduced + it,
-                                 ws + L.pw_scratch, ws + L.pw_seq, (double*)(ws + L.pw_part),
-                                 (unsigned*)(ws + L.pw_done), it, stats_dev, s);
-      if (rc) return rc;
     }
   }
   if (A.active) {

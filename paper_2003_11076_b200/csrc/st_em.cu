@@ -12,6 +12,9 @@
 
 #include "st_common.cuh"
 #include "st_em.cuh"
+#include "st_pw.cuh"
+
+#include <cub/block/block_scan.cuh>
 
 namespace st {
 
@@ -493,89 +496,116 @@ __global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n, int6
 // Per-iteration statistics over every active slot, as fixed-order per-warp
 // partials (solver.py:463-475: mean of finite E, mean of finite previous
 // energies, changed count).
-__device__ void reduce_partials_block(const Partial* __restrict__ parts, int nparts,
-                                      Partial* __restrict__ out);
 __device__ void solve_control(int it, const Partial* __restrict__ reduced,
                               uint32_t* __restrict__ counts, int64_t n_act, int forced_iters,
                               st_stats* __restrict__ stats, int* __restrict__ stop);
 
-__global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ e,
-                           const double* __restrict__ pe, const uint8_t* __restrict__ chg,
-                           const Partial* __restrict__ work, int n_work_parts,
-                           Partial* __restrict__ parts, const int* stop, StatsTail tail) {
+// Per-iteration statistics (solver.py:463-475).  solver.py:466/471 take
+// `finite.mean()`: the grid is the top `pw_depth` levels of numpy's pairwise
+// tree over the slots (st_pw.cuh), each block sums its node of E (and of
+// the previous-disparity energies) exactly, and the last block adds the
+// nodes up the same tree.  Should a value be non-finite (never for
+// d_max >= 1), the last block compacts the finite values and sums them
+// itself (the slow path: numpy's tree over the compacted sequence).
+int stats_depth(int64_t n) {
+  int D = 0;  // nodes of ~4k values per block, <= 1024 blocks
+  while (D < 10 && (n >> D) > 4096) ++D;
+  return D;
+}
+
+int64_t pw_val_size(int64_t n) {  // the slow path's levels for n values
+  int depth = 0;
+  while (n > PW_LEAF) {
+    n -= n / 2 - (n / 2) % 8;
+    ++depth;
+  }
+  return ((int64_t)2 << depth) + 64;
+}
+
+__device__ double pw_sum_compacted(const double* __restrict__ x, int64_t n,
+                                   double* __restrict__ scratch, double* __restrict__ val,
+                                   int64_t* m_out) {
+  typedef cub::BlockScan<int, STATS_BLOCK> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int64_t base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t c = 0; c < n; c += STATS_BLOCK) {
+    const int64_t i = c + threadIdx.x;
+    const int f = (i < n && isfinite(x[i])) ? 1 : 0;
+    int off, tot;
+    Scan(tmp).ExclusiveSum(f, off, tot);
+    if (f) scratch[base + off] = x[i];
+    __syncthreads();
+    if (threadIdx.x == 0) base += tot;
+    __syncthreads();
+  }
+  const int64_t m = base;
+  *m_out = m;
+  const int levels = pw_depth_of(m, 62) + 1;
+  return m > 0 ? pw_block_sum(scratch, 0, m, val, levels) : 0.0;
+}
+
+__global__ void __launch_bounds__(STATS_BLOCK) k_em_stats(
+    int64_t n, int with_prev, const double* __restrict__ e, const double* __restrict__ pe,
+    const uint8_t* __restrict__ chg, const Partial* __restrict__ work, int n_work_parts,
+    Partial* __restrict__ parts, const int* stop, StatsTail tail) {
   if (stop && *stop) return;
-  // fixed grid (STATS_GRID), fixed per-thread order: deterministic sums
-  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  __shared__ double val[(1 << PW_MAX_LEVELS) - 1];
+  const int D = tail.pw_depth;
+  int64_t s0, nn;
+  const bool own = pw_block_node(n, D, blockIdx.x, s0, nn);
   double se = 0.0, spe = 0.0;
+  if (own && nn > 0) {
+    se = pw_block_sum(e, s0, nn, val, PW_MAX_LEVELS);
+    if (with_prev) spe = pw_block_sum(pe, s0, nn, val, PW_MAX_LEVELS);
+  }
   long long nf = 0, npf = 0, nch = 0;
-  for (int64_t i = t0; i < n; i += stride) {
-    const double x = e[i];
-    if (isfinite(x)) {
-      se += x;
-      nf += 1;
-    }
-    if (with_prev) {
-      const double y = pe[i];
-      if (isfinite(y)) {
-        spe += y;
-        npf += 1;
+  if (own) {
+    for (int64_t i = s0 + threadIdx.x; i < s0 + nn; i += blockDim.x) {
+      nf += isfinite(e[i]) ? 1 : 0;
+      if (with_prev) {
+        npf += isfinite(pe[i]) ? 1 : 0;
+        nch += chg[i];
       }
-      nch += chg[i];
     }
   }
   // the M-step's per-warp work counters (integers: any order is exact)
   long long wc = 0, we = 0, wh = 0, ws = 0;
-  for (int64_t w = t0; w < n_work_parts; w += stride) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n_work_parts;
+       w += (int64_t)gridDim.x * blockDim.x) {
     wc += work[w].n_cand;
     we += work[w].n_eval;
     wh += work[w].n_hopeless;
     ws += work[w].n_samples;
   }
-  wc = warp_sum(wc);
-  we = warp_sum(we);
-  wh = warp_sum(wh);
-  ws = warp_sum(ws);
-  se = warp_sum(se);
-  spe = warp_sum(spe);
-  nf = warp_sum(nf);
-  npf = warp_sum(npf);
-  nch = warp_sum(nch);
-  // one partial per block, warps combined in fixed order
-  __shared__ Partial sp[STATS_BLOCK / 32];
+  __shared__ long long si[7][STATS_BLOCK / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) {
-    Partial P = {};
-    P.sum_e = se;
-    P.sum_pe = spe;
-    P.n_fin = nf;
-    P.n_pfin = npf;
-    P.n_changed = nch;
-    P.n_cand = wc;
-    P.n_eval = we;
-    P.n_hopeless = wh;
-    P.n_samples = ws;
-    sp[wid] = P;
+  long long v7[7] = {nf, npf, nch, wc, we, wh, ws};
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const long long x = warp_sum(v7[k]);
+    if (lane == 0) si[k][wid] = x;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    Partial B = sp[0];
-    for (int j = 1; j < (int)(blockDim.x >> 5); ++j) {
-      B.sum_e += sp[j].sum_e;
-      B.sum_pe += sp[j].sum_pe;
-      B.n_fin += sp[j].n_fin;
-      B.n_pfin += sp[j].n_pfin;
-      B.n_changed += sp[j].n_changed;
-      B.n_cand += sp[j].n_cand;
-      B.n_eval += sp[j].n_eval;
-      B.n_hopeless += sp[j].n_hopeless;
-      B.n_samples += sp[j].n_samples;
-    }
+    Partial B = {};
+    B.sum_e = se;
+    B.sum_pe = spe;
+    long long t7[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j)
+      for (int k = 0; k < 7; ++k) t7[k] += si[k][j];
+    B.n_fin = t7[0];
+    B.n_pfin = t7[1];
+    B.n_changed = t7[2];
+    B.n_cand = t7[3];
+    B.n_eval = t7[4];
+    B.n_hopeless = t7[5];
+    B.n_samples = t7[6];
     parts[blockIdx.x] = B;
   }
   if (!tail.on) return;
-  // the last block to finish folds every block's partial (fixed order) and
-  // runs the iteration's control: no separate reduce / control launches
+  // the last block to finish folds the blocks' records and runs the control
   __shared__ bool last;
   if (threadIdx.x == 0) {
     __threadfence();
@@ -584,27 +614,76 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* __restrict__ 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  reduce_partials_block(parts, gridDim.x, tail.reduced + tail.it);
+  // integer counts: any order
+  const int nb = gridDim.x;
+  long long c7[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const Partial& P = parts[b];
+    c7[0] += P.n_fin;
+    c7[1] += P.n_pfin;
+    c7[2] += P.n_changed;
+    c7[3] += P.n_cand;
+    c7[4] += P.n_eval;
+    c7[5] += P.n_hopeless;
+    c7[6] += P.n_samples;
+  }
   __syncthreads();
-  if (threadIdx.x == 0 && tail.record_only) {
-    __threadfence();
-    *tail.done = 0u;
-    Partial* rec = tail.reduced + tail.it;
-    rec->n_act = tail.record_n_act;
-    rec->n_mwork = tail.it > 1 ? (long long)tail.counts[0] : tail.record_slots;
-    rec->n_ework = (long long)tail.counts[1];
-    tail.counts[0] = 0;  // next iteration's worklists
-    tail.counts[1] = 0;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const long long x = warp_sum(c7[k]);
+    if (lane == 0) si[k][wid] = x;
+  }
+  __syncthreads();
+  __shared__ long long tot7[7];
+  if (threadIdx.x < 7) {
+    long long x = 0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) x += si[threadIdx.x][j];
+    tot7[threadIdx.x] = x;
+  }
+  __syncthreads();
+  // the energy sums in numpy's order
+  double sum_e, sum_pe = 0.0;
+  int64_t m_e = tot7[0], m_pe = tot7[1];
+  if (m_e == n) {
+    sum_e = pw_top_sum(n, D, [&](unsigned p) { return parts[p].sum_e; }, val);
+  } else {
+    sum_e = pw_sum_compacted(e, n, tail.pw_scratch, tail.pw_val, &m_e);
+  }
+  if (with_prev) {
+    if (m_pe == n)
+      sum_pe = pw_top_sum(n, D, [&](unsigned p) { return parts[p].sum_pe; }, val);
+    else
+      sum_pe = pw_sum_compacted(pe, n, tail.pw_scratch, tail.pw_val, &m_pe);
+  }
+  if (threadIdx.x != 0) return;
+  Partial r = {};
+  r.sum_e = dadd(0.0, sum_e);  // np.add.reduce: the identity, then the pairwise sum
+  r.sum_pe = dadd(0.0, sum_pe);
+  r.n_fin = tot7[0];
+  r.n_pfin = tot7[1];
+  r.n_changed = tot7[2];
+  r.n_cand = tot7[3];
+  r.n_eval = tot7[4];
+  r.n_hopeless = tot7[5];
+  r.n_samples = tot7[6];
+  *tail.done = 0u;
+  if (tail.record_only) {
+    r.n_act = tail.record_n_act;
+    r.n_mwork = tail.it > 1 ? (long long)tail.counts[0] : tail.record_slots;
+    r.n_ework = (long long)tail.counts[1];
+    tail.reduced[tail.it] = r;
+    if (!tail.keep_counts) {
+      tail.counts[0] = 0;  // next iteration's worklists
+      tail.counts[1] = 0;
+    }
     if (tail.flist_count) *tail.flist_count = 0u;
     return;
   }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    *tail.done = 0u;
-    solve_control(tail.it, tail.reduced, tail.counts, tail.n_act, tail.forced_iters, tail.stats,
-                  tail.stop_rw);
-    if (tail.flist_count) *tail.flist_count = 0u;
-  }
+  tail.reduced[tail.it] = r;
+  __threadfence();
+  solve_control(tail.it, tail.reduced, tail.counts, tail.n_act, tail.forced_iters, tail.stats,
+                tail.stop_rw);
+  if (tail.flist_count) *tail.flist_count = 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -1770,67 +1849,6 @@ __global__ void k_fill_mu(const double* __restrict__ mu, int64_t npx, float* __r
   status[i] = ST_STATUS_VALID;
 }
 
-// Fixed-order sum of the per-block partials into slot `it` of the stats.
-// Fixed-order sum of the per-block partials by one 256-thread block.
-__device__ void reduce_partials_block(const Partial* __restrict__ parts, int nparts,
-                                      Partial* __restrict__ out) {
-  __shared__ double sd[2][256];
-  __shared__ long long si[7][256];
-  double a = 0.0, b = 0.0;
-  long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0;
-  // thread t sums parts t, t+256, ... in order
-  for (int j = threadIdx.x; j < nparts; j += blockDim.x) {
-    a += parts[j].sum_e;
-    b += parts[j].sum_pe;
-    c0 += parts[j].n_fin;
-    c1 += parts[j].n_pfin;
-    c2 += parts[j].n_changed;
-    c3 += parts[j].n_cand;
-    c4 += parts[j].n_eval;
-    c5 += parts[j].n_hopeless;
-    c6 += parts[j].n_samples;
-  }
-  sd[0][threadIdx.x] = a;
-  sd[1][threadIdx.x] = b;
-  si[0][threadIdx.x] = c0;
-  si[1][threadIdx.x] = c1;
-  si[2][threadIdx.x] = c2;
-  si[3][threadIdx.x] = c3;
-  si[4][threadIdx.x] = c4;
-  si[5][threadIdx.x] = c5;
-  si[6][threadIdx.x] = c6;
-  __syncthreads();
-  // fixed-order pairwise tree over the 256 thread sums (deterministic)
-  for (int h = 128; h > 0; h >>= 1) {
-    const int t = threadIdx.x;
-    if (t < h) {
-      sd[0][t] += sd[0][t + h];
-      sd[1][t] += sd[1][t + h];
-#pragma unroll
-      for (int k = 0; k < 7; ++k) si[k][t] += si[k][t + h];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    Partial r = {};
-    r.sum_e = sd[0][0];
-    r.sum_pe = sd[1][0];
-    r.n_fin = si[0][0];
-    r.n_pfin = si[1][0];
-    r.n_changed = si[2][0];
-    r.n_cand = si[3][0];
-    r.n_eval = si[4][0];
-    r.n_hopeless = si[5][0];
-    r.n_samples = si[6][0];
-    *out = r;
-  }
-}
-
-__global__ void k_reduce_partials(const Partial* __restrict__ parts, int nparts,
-                                  Partial* __restrict__ out, const int* stop) {
-  if (stop && *stop) return;
-  reduce_partials_block(parts, nparts, out);
-}
 
 // dynamic_only / explicit active-set compaction: count then scatter, in
 // pixel order (the reference's `active` is ascending).
@@ -1930,11 +1948,5 @@ __global__ void k_band_control(int it, const Partial* __restrict__ gathered, int
   control_step(it, r, r.n_act, r.n_mwork, r.n_ework, forced_iters, stats, stop);
 }
 
-__global__ void k_solve_control(int it, const Partial* __restrict__ reduced,
-                                uint32_t* __restrict__ counts, int64_t n_act, int forced_iters,
-                                st_stats* __restrict__ stats, int* __restrict__ stop) {
-  if (threadIdx.x != 0 || blockIdx.x != 0 || *stop) return;
-  solve_control(it, reduced, counts, n_act, forced_iters, stats, stop);
-}
 
 }  // namespace st

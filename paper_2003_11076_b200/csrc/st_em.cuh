@@ -16,9 +16,6 @@
 #endif
 #define MSTEP_BOUNDS __launch_bounds__(EM_BLOCK, MSTEP_MIN_BLOCKS)
 #define STATS_BLOCK 256
-#ifndef STATS_GRID
-#define STATS_GRID (148 * 2)  // fixed grid of k_em_stats: deterministic sums (measured best)
-#endif
 #define ESTEP_BLOCK 64
 #define ESTEP_TAPS_BLOCK 128
 #define ESTEP_CERT_BLOCK 128
@@ -114,8 +111,8 @@ __global__ void k_flag_mstep(const int64_t* active, int64_t n, int64_t pix0,
                              const uint32_t* static_all,
                              const uint32_t* mask_in, const double* e, double* pe, uint8_t* chg,
                              int32_t* list, uint32_t* count, const int* stop = nullptr);
-// st_solve_async: k_em_stats' last block also reduces the partials and runs
-// the iteration's control (k_reduce_partials + k_solve_control fused).
+// k_em_stats' last block folds the blocks' records and runs the iteration's
+// control (st_solve_async) or writes the record (row bands, st_solve).
 struct StatsTail {
   int on;
   int it;
@@ -133,10 +130,24 @@ struct StatsTail {
   int record_only;
   long long record_n_act;
   long long record_slots;  // iteration 1's M-step count (every slot)
+  int keep_counts;         // st_solve (host loop): leave the worklist counts to the host
+  // numpy's summation order (st_mean.cu): the grid is the top pw_depth levels
+  // of np.add.reduce's pairwise tree; non-finite values take the slow path
+  int pw_depth;
+  double* pw_scratch;      // n doubles: the finite values, compacted
+  double* pw_val;          // pw_val_size(n) doubles: the slow path's tree levels
 };
+// grid of k_em_stats for n counted slots (1 << pw_depth blocks) and its depth
+int stats_depth(int64_t n);
+int64_t pw_val_size(int64_t n);
+// Per-iteration statistics (solver.py:463-475): the mean of the finite M-step
+// energies and previous-disparity energies summed in numpy's own order
+// (st_mean.cu), the changed count and the M-step work counters; the last
+// block folds the blocks' records and runs the control (or writes the
+// shard's record, tail.record_only).
 __global__ void k_em_stats(int64_t n, int with_prev, const double* e, const double* pe,
                            const uint8_t* chg, const Partial* work, int n_work_parts,
-                           Partial* parts, const int* stop = nullptr, StatsTail tail = {});
+                           Partial* parts, const int* stop, StatsTail tail);
 template <int KT, bool RECT>
 __global__ void k_e_step_taps(EmCtx c, EStepArgs a);
 __global__ void k_e_step_at(EmCtx c, EStepArgs a);
@@ -158,13 +169,6 @@ __global__ void k_pack_outputs(const double* mu, int64_t npx, int64_t pix0, cons
                                int64_t n_active, const double* d_act, const uint8_t* st_act,
                                float* values, uint8_t* status, int dense);
 __global__ void k_fill_mu(const double* mu, int64_t npx, float* values, uint8_t* status);
-__global__ void k_reduce_partials(const Partial* parts, int nparts, Partial* out,
-                                  const int* stop = nullptr);
-// Device-side EM control for st_solve_async (solver.py:463-485): folds the
-// iteration's reduced partials and worklist counts into *stats, sets *stop
-// on convergence, and clears the worklist counts for the next iteration.
-__global__ void k_solve_control(int it, const Partial* reduced, uint32_t* counts, int64_t n_act,
-                                int forced_iters, st_stats* stats, int* stop);
 __global__ void k_stats_init(st_stats* stats, int64_t n_act);
 // Row bands: sum the shards' records (rank order, deterministic) and run the
 // iteration's control exactly as k_solve_control does for one device.
@@ -180,9 +184,4 @@ __global__ void k_scatter_active(const uint32_t* flags, const uint32_t* offs, in
 
 }  // namespace st
 
-// numpy-exact EM statistics means (st_mean.cu): the finite values of e / pe
-// (slot order) -> stats->mean_energy[it-1] / prev_energy[it-2].
-#define ST_PW_MAX_DEPTH 12
-int st_pw_means(const double* e, const double* pe, int64_t n, const void* rec, void* scratch,
-                void* seq, double* partial, unsigned* done, int it, st_stats* stats,
-                cudaStream_t s);
+

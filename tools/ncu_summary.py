@@ -62,6 +62,10 @@ WANT = {
     "launch__block_size": "block",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
+    "sm__sass_thread_inst_executed_op_dadd_pred_on.sum": "fp64_dadd",
+    "sm__sass_thread_inst_executed_op_dmul_pred_on.sum": "fp64_dmul",
+    "sm__sass_thread_inst_executed_op_dfma_pred_on.sum": "fp64_dfma",
+    "smsp__inst_executed_pipe_fp64.sum": "fp64_warp_instructions",
 }
 
 
@@ -90,6 +94,11 @@ def full(path, out):
         k["stall_samples"] = dict(sorted(stalls.items(), key=lambda x: -x[1])[:8])
         if "dram_read_bytes" in k:
             k["dram_bytes"] = k["dram_read_bytes"] + k.get("dram_write_bytes", 0.0)
+        if "fp64_dadd" in k:
+            k["fp64_flops"] = (k.get("fp64_dadd", 0.0) + k.get("fp64_dmul", 0.0)
+                               + 2.0 * k.get("fp64_dfma", 0.0))
+            if k.get("duration_ns"):
+                k["fp64_tflops"] = k["fp64_flops"] / k["duration_ns"] / 1e3
         kernels.append(k)
     json.dump({"source": path, "kernels": kernels}, open(out, "w"), indent=1)
     for k in kernels:
@@ -97,5 +106,40 @@ def full(path, out):
                                                   "fp64_pipe_pct", "occupancy_pct")}))
 
 
+def step(path, out, steps="1"):
+    """Whole-step DRAM traffic: a launch list captured with
+    --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+    over the last `steps` timed steps (cold-cache, serialised): per-kernel
+    and total bytes per step."""
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    per = collections.defaultdict(lambda: collections.defaultdict(float))
+    ids = collections.defaultdict(set)
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1.0,
+             "usecond": 1e3, "msecond": 1e6}
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if not hdr or len(r) != len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        k = d["Kernel Name"].split("(")[0]
+        per[k][d["Metric Name"]] += float(d["Metric Value"].replace(",", "")) * scale.get(
+            d["Metric Unit"], 1.0)
+        ids[k].add(d["ID"])
+    n = float(steps)
+    kern = sorted(({"kernel": k, "launches_per_step": len(ids[k]) / n,
+                    "dram_bytes_per_step": (v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"]) / n,
+                    "ns_per_step": v["gpu__time_duration.sum"] / n} for k, v in per.items()),
+                  key=lambda x: -x["dram_bytes_per_step"])
+    total = sum(x["dram_bytes_per_step"] for x in kern)
+    json.dump({"source": path, "steps": n, "dram_bytes_per_step": total, "kernels": kern},
+              open(out, "w"), indent=1)
+    print(f"DRAM bytes per step: {total / 1e6:.1f} MB")
+    for x in kern[:12]:
+        print(f"{x['dram_bytes_per_step'] / 1e6:8.2f} MB  {x['ns_per_step'] / 1e3:8.1f} us  {x['kernel']}")
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "step": step}[sys.argv[1]](*sys.argv[2:])
