@@ -205,6 +205,12 @@ int st_support_build(const double* support_uv, const double* support_d, int32_t 
                      void* workspace, int64_t workspace_bytes, int64_t* n_records,
                      void* stream);
 int64_t st_support_workspace(int32_t n, int32_t W, int32_t H, double radius);
+/* st_support_build for the tiles of rows [row0, row1) only (a row band's
+ * solved rows): the other tiles get no candidate groups. */
+int st_support_build_rows(const double* support_uv, const double* support_d, int32_t n,
+                          int32_t W, int32_t H, const st_params* p, st_frame* frame,
+                          void* workspace, int64_t workspace_bytes, int64_t* n_records,
+                          int32_t row0, int32_t row1, void* stream);
 
 /* ---- support harvest (prior.py:51-260) ----------------- */
 

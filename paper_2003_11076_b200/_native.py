@@ -110,6 +110,9 @@ _SIGS = {
     "st_support_build": (C.c_int, [_P, _P, _I32, _I32, _I32, C.POINTER(StParams),
                                    C.POINTER(StFrame), _P, _I64, C.POINTER(C.c_int64), _P]),
     "st_support_workspace": (C.c_int64, [_I32, _I32, _I32, _D]),
+    "st_support_build_rows": (C.c_int, [_P, _P, _I32, _I32, _I32, C.POINTER(StParams),
+                                        C.POINTER(StFrame), _P, _I64, C.POINTER(C.c_int64),
+                                        _I32, _I32, _P]),
     "st_solve_async": (C.c_int, [C.POINTER(StFrame), C.POINTER(StRig), C.POINTER(StParams),
                                  _P, _P, _P, _P, _P, _P, _I64, _P]),
     "st_frame_plan_init": (C.c_int, [C.POINTER(StFramePlan)]),

@@ -20,6 +20,7 @@ namespace st {
 struct SupGeom {
   int W, H, tiles_x, tiles_y, ir;
   double d_max;
+  int ty_lo, ty_hi;  // tile rows built (a row band's; all otherwise)
 };
 
 __device__ __forceinline__ bool sup_range(const SupGeom& g, double su, double sv, double sd,
@@ -35,9 +36,9 @@ __device__ __forceinline__ bool sup_range(const SupGeom& g, double su, double sv
   if (x0 > x1 || y0 > y1) return false;
   tx0 = x0 / ST_TW;
   tx1 = x1 / ST_TW;
-  ty0 = y0 / ST_TH;
-  ty1 = y1 / ST_TH;
-  return true;
+  ty0 = max(y0 / ST_TH, g.ty_lo);
+  ty1 = min(y1 / ST_TH, g.ty_hi);
+  return ty0 <= ty1;
 }
 
 // One point's 32x8 coverage rows in tile (tx, ty): the pixels inside its
@@ -284,10 +285,29 @@ extern "C" int64_t st_support_workspace(int32_t n, int32_t W, int32_t H, double 
   return (int64_t)sup_layout(n, W, H, radius).total;
 }
 
+extern "C" int st_support_build_rows(const double* support_uv, const double* support_d,
+                                     int32_t n, int32_t W, int32_t H, const st_params* p,
+                                     st_frame* frame, void* workspace, int64_t workspace_bytes,
+                                     int64_t* n_records, int32_t row0, int32_t row1,
+                                     void* stream);
+
 extern "C" int st_support_build(const double* support_uv, const double* support_d, int32_t n,
                                 int32_t W, int32_t H, const st_params* p, st_frame* frame,
                                 void* workspace, int64_t workspace_bytes, int64_t* n_records,
                                 void* stream) {
+  return st_support_build_rows(support_uv, support_d, n, W, H, p, frame, workspace,
+                               workspace_bytes, n_records, 0, H, stream);
+}
+
+extern "C" int st_support_build_rows(const double* support_uv, const double* support_d,
+                                     int32_t n, int32_t W, int32_t H, const st_params* p,
+                                     st_frame* frame, void* workspace, int64_t workspace_bytes,
+                                     int64_t* n_records, int32_t row0, int32_t row1,
+                                     void* stream) {
+  if (!(0 <= row0 && row0 < row1 && row1 <= H)) {
+    sthost::set_error("st_support_build_rows: bad rows [%d, %d) of %d", row0, row1, H);
+    return ST_EINVAL;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   const SupLayout L = sup_layout(n, W, H, p->neighborhood_radius);
   if ((int64_t)L.total > workspace_bytes) {
@@ -315,6 +335,8 @@ extern "C" int st_support_build(const double* support_uv, const double* support_
   g.tiles_y = L.tiles_y;
   g.ir = (int)floor(p->neighborhood_radius);
   g.d_max = p->d_max;
+  g.ty_lo = row0 / ST_TH;
+  g.ty_hi = (row1 - 1) / ST_TH;
   const double r = p->neighborhood_radius;
 
   // per-tile buckets: count, scan, fill -- no host round trip

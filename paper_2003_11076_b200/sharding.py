@@ -242,8 +242,9 @@ class BandPipeline:
         with t.cuda.stream(pipe.side2):
             pipe.side2.wait_event(ready)
             N.invoke("st_descriptors_rows", pipe.images, K, H, W, pipe.desc, d0, d1)
-            N.invoke("st_support_build", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W, H, p,
-                     pipe.frame, pipe.sup_ws, pipe.sup_ws.numel(), None)
+            e0, e1 = self.ext["solve"]
+            N.invoke("st_support_build_rows", tri_dev.sup_uv, tri_dev.sup_d, tri_dev.n_sup, W,
+                     H, p, pipe.frame, pipe.sup_ws, pipe.sup_ws.numel(), None, e0, e1)
             pre_done = t.cuda.Event()
             pre_done.record(pipe.side2)
         main.wait_event(pre_done)
