@@ -40,6 +40,7 @@ enum {
   ST_EINVAL = -1,  /* bad argument (ValueError in the reference) */
   ST_ECUDA = -2,   /* CUDA runtime / launch failure */
   ST_ENOMEM = -3,  /* workspace too small */
+  ST_EAGAIN = -4,  /* row bands: redo the frame with a whole-frame surface raster */
 };
 
 /* solver.py:48-50 */
@@ -177,6 +178,17 @@ int st_tri_tables(const st_tri* tri, double* planes_out, double* transform_out, 
 int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip_dmax, double* mu_out,
                  void* workspace, int64_t workspace_bytes, void* stream);
 int64_t st_mu_raster_workspace(int32_t W, int32_t H, int32_t n_tri);
+/* st_mu_raster for rows [row0, row1) only (a row band's solved rows): the
+ * Qhull walk replay runs over those rows plus 2 halo rows above, whose walks
+ * seed the band's (a pixel with a single claiming triangle ends every
+ * dependency chain).  *unsafe_out (device int, nullable) is set when the
+ * chain entering the band starts at the window's first pixel, or when a
+ * band pixel lies off the hull (the reference's nudged batch carries its
+ * start across the whole frame): the band's mu is then not exact and the
+ * caller rasters the whole frame instead. */
+int st_mu_raster_rows(const st_tri* tri, int32_t W, int32_t H, double clip_dmax,
+                      double* mu_out, void* workspace, int64_t workspace_bytes, int32_t row0,
+                      int32_t row1, int32_t* unsafe_out, void* stream);
 
 /* ---- solver pieces (DisparitySolver API, solver.py:162-432) ----------- */
 
@@ -192,6 +204,10 @@ typedef struct {
   const uint32_t* sup_tile_start;  /* (n_tiles+1) first group of each tile */
   const float* sup_value;          /* (n_groups) fp32-rounded support disparity */
   const uint32_t* sup_mask;        /* (n_groups, 8) row bit masks */
+  /* nullable: device flag from st_mu_raster_rows; nonzero = this shard's
+   * row-window raster could not be made exact (st_solve_rows then returns
+   * ST_EAGAIN on every shard and the caller rasters the whole frame) */
+  const int32_t* mu_unsafe;
 } st_frame;
 
 /* Build per-tile support candidate lists (solver.py:286-321 semantics).

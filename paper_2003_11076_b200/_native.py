@@ -48,7 +48,8 @@ class StStats(C.Structure):
 class StFrame(C.Structure):
     _fields_ = [("images", C.c_void_p), ("priors", C.c_void_p), ("desc", C.c_void_p),
                 ("mu", C.c_void_p), ("sup_tile_start", C.c_void_p),
-                ("sup_value", C.c_void_p), ("sup_mask", C.c_void_p)]
+                ("sup_value", C.c_void_p), ("sup_mask", C.c_void_p),
+                ("mu_unsafe", C.c_void_p)]
 
 
 class StTri(C.Structure):
@@ -107,6 +108,8 @@ _SIGS = {
     "st_warp": (C.c_int, [C.POINTER(StRig), _I32, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "st_mu_raster": (C.c_int, [C.POINTER(StTri), _I32, _I32, _D, _P, _P, _I64, _P]),
     "st_mu_raster_workspace": (C.c_int64, [_I32, _I32, _I32]),
+    "st_mu_raster_rows": (C.c_int, [C.POINTER(StTri), _I32, _I32, _D, _P, _P, _I64, _I32, _I32,
+                                    _P, _P]),
     "st_support_build": (C.c_int, [_P, _P, _I32, _I32, _I32, C.POINTER(StParams),
                                    C.POINTER(StFrame), _P, _I64, C.POINTER(C.c_int64), _P]),
     "st_support_workspace": (C.c_int64, [_I32, _I32, _I32, _D]),
@@ -165,6 +168,14 @@ class NativeError(RuntimeError):
     """CUDA / library failure inside the native path."""
 
 
+ST_EAGAIN = -4
+
+
+class BandRetry(RuntimeError):
+    """st_solve_rows: a shard's row-window surface raster was not exact;
+    every shard redoes the frame with the whole-frame raster."""
+
+
 def lib():
     """Load the CUDA library (no fallback: raise if it is missing)."""
     global _lib
@@ -194,6 +205,8 @@ def check(rc):
     msg = lib().st_last_error().decode(errors="replace")
     if rc == -1:
         raise ValueError(msg)
+    if rc == ST_EAGAIN:
+        raise BandRetry(msg)
     raise NativeError(msg)
 
 

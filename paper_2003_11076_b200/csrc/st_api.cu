@@ -897,6 +897,10 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
       int h_stop = 0;
       ST_CUDA_CHECK(cudaMemcpyAsync(&h_stop, stop, sizeof(int), cudaMemcpyDeviceToHost, s));
       ST_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (h_stop == 2) {
+        sthost::set_error("row band: whole-frame surface raster needed");
+        return ST_EAGAIN;
+      }
       if (h_stop) break;
     }
     // iteration 2 re-solves the pixels whose mask changed at iteration 1
@@ -967,6 +971,7 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     tail.pw_depth = pw_d;
     tail.pw_scratch = (double*)(ws + L.pw_scratch);
     tail.pw_val = (double*)(ws + L.pw_val);
+    tail.mu_unsafe = A.band ? f->mu_unsafe : nullptr;
     st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(
         n_cnt, it > 1, e_act + A.cnt_lo, pe_act + A.cnt_lo, chg + A.cnt_lo, work,
         (n > 0 ? (it == 1 ? mblk : it == 2 ? mwave2 : std::min(mblk, 148 * 4)) : 0) *
@@ -987,6 +992,15 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
       st::k_band_control<<<1, 32, 0, s>>>(it, recs, A.exchange ? A.world : 1, p->forced_iters,
                                           stats_dev, stop);
       ST_LAUNCH_CHECK("k_band_control");
+    }
+  }
+  if (A.band && A.exchange) {  // (max_iters == 1: the loop read no stop flag)
+    int h_stop = 0;
+    ST_CUDA_CHECK(cudaMemcpyAsync(&h_stop, stop, sizeof(int), cudaMemcpyDeviceToHost, s));
+    ST_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (h_stop == 2) {
+      sthost::set_error("row band: whole-frame surface raster needed");
+      return ST_EAGAIN;
     }
   }
   if (A.active) {

@@ -671,6 +671,7 @@ __global__ void __launch_bounds__(STATS_BLOCK) k_em_stats(
     r.n_act = tail.record_n_act;
     r.n_mwork = tail.it > 1 ? (long long)tail.counts[0] : tail.record_slots;
     r.n_ework = (long long)tail.counts[1];
+    r.n_unsafe = tail.mu_unsafe ? (long long)(*tail.mu_unsafe != 0) : 0;
     tail.reduced[tail.it] = r;
     if (!tail.keep_counts) {
       tail.counts[0] = 0;  // next iteration's worklists
@@ -1938,6 +1939,11 @@ __global__ void k_band_control(int it, const Partial* __restrict__ gathered, int
     r.n_act += g.n_act;
     r.n_mwork += g.n_mwork;
     r.n_ework += g.n_ework;
+    r.n_unsafe += g.n_unsafe;
+  }
+  if (r.n_unsafe > 0) {  // a shard's surface raster was not exact: redo the frame
+    *stop = 2;
+    return;
   }
   if (it == 1) stats->active_pixels = r.n_act;
   if (r.n_act == 0) {  // solver.py:486-488: no active pixel anywhere

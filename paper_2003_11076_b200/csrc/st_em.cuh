@@ -66,6 +66,7 @@ struct Partial {
   // row-band record (st_solve_rows): the shard's counted active pixels and its
   // M/E worklist sizes, summed over shards by k_band_control
   long long n_act, n_mwork, n_ework;
+  long long n_unsafe;  // shards whose row-window mu raster was not exact
 };
 
 // Slots are the rows of the active set (slot i -> pixel active[i], or i when
@@ -136,6 +137,7 @@ struct StatsTail {
   int pw_depth;
   double* pw_scratch;      // n doubles: the finite values, compacted
   double* pw_val;          // pw_val_size(n) doubles: the slow path's tree levels
+  const int32_t* mu_unsafe;  // nullable: st_mu_raster_rows' flag, into the shard record
 };
 // grid of k_em_stats for n counted slots (1 << pw_depth blocks) and its depth
 int stats_depth(int64_t n);

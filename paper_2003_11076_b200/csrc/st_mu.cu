@@ -30,6 +30,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "st_common.cuh"
@@ -58,6 +60,10 @@ struct MuWs {
   int chunk;  // chunk length for the speculative walks (MU_CHUNK, env ST_MU_CHUNK)
   unsigned* miss_bits;  // pixels the raster walk left outside the triangulation
   int32_t* miss_list;   // ... in pixel order (k_mu_nudge)
+  // row window (st_mu_raster_rows): pixels [p_lo, p_hi) are rastered (the
+  // band's rows plus a halo above), mu is written for [b_lo, p_hi); the whole
+  // frame otherwise (p_lo = b_lo = 0, p_hi = W*H)
+  int64_t p_lo, p_hi, b_lo;
 };
 
 // prior.py:296: pl[:, 0] * u + pl[:, 1] * v + pl[:, 2], left to right.
@@ -96,7 +102,7 @@ __device__ __forceinline__ bool bary_inside(const double* __restrict__ T, double
 // its pixel count, scanned afterwards so the claim tests can be spread
 // evenly over the grid (a few corner-anchor triangles span most of the
 // image; one thread per triangle would serialise them).
-__global__ void k_tri_bbox(TriDev d, int W, int H, int4* __restrict__ bbox,
+__global__ void k_tri_bbox(TriDev d, int W, int H, int y_lo, int y_hi, int4* __restrict__ bbox,
                            unsigned long long* __restrict__ area) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= d.n_tri) return;
@@ -108,8 +114,8 @@ __global__ void k_tri_bbox(TriDev d, int W, int H, int4* __restrict__ bbox,
   int4 bb;
   bb.x = max(0, (int)ceil(fmin(ax, fmin(bx, cx)) - 1e-6));
   bb.z = min(W - 1, (int)floor(fmax(ax, fmax(bx, cx)) + 1e-6));
-  bb.y = max(0, (int)ceil(fmin(ay, fmin(by, cy)) - 1e-6));
-  bb.w = min(H - 1, (int)floor(fmax(ay, fmax(by, cy)) + 1e-6));
+  bb.y = max(y_lo, (int)ceil(fmin(ay, fmin(by, cy)) - 1e-6));
+  bb.w = min(y_hi - 1, (int)floor(fmax(ay, fmax(by, cy)) + 1e-6));
   unsigned long long n = 0;
   if (T[0] == T[0] && bb.x <= bb.z && bb.y <= bb.w)  // nan transform: degenerate simplex
     n = (unsigned long long)(bb.z - bb.x + 1) * (unsigned long long)(bb.w - bb.y + 1);
@@ -355,7 +361,7 @@ __device__ __forceinline__ bool ambiguous(const MuWs& w, int64_t p) { return w.c
 // claimers (then the incoming start is one of those two).
 __device__ __forceinline__ bool chunk_start(const MuWs& w, int64_t p) {
   if (!ambiguous(w, p)) return false;
-  if (p == 0) return true;
+  if (p == w.p_lo) return true;  // (pixel 0, or a row window's first pixel)
   if (!ambiguous(w, p - 1)) return true;
   return (p % w.chunk) == 0 && w.cnt[p - 1] == 2u;
 }
@@ -377,21 +383,24 @@ __device__ __forceinline__ void append_lane(bool want, int32_t v, int32_t* list,
 // empty claimer/value ranges, every chunk undecided.
 __global__ void k_mu_init(int64_t npx, MuWs w) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npx; p += stride) {
+  (void)npx;
+  for (int64_t p = w.p_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < w.p_hi;
+       p += stride) {
     w.cnt[p] = 0u;
     w.tmin[p] = 0xffffffffu;
     w.tmax[p] = 0u;
     w.vmin[p] = ~0ull;
     w.vmax[p] = 0ull;
     w.chosen[p] = 0xff;
-    if ((p & 31) == 0) w.miss_bits[p >> 5] = 0u;
+    if ((p & 31) == 0 || p == w.p_lo) w.miss_bits[p >> 5] = 0u;
   }
   if (blockIdx.x == 0 && threadIdx.x < 8) w.counts[threadIdx.x] = 0u;
 }
 
 __global__ void k_mu_lists(int64_t npx, MuWs w) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool in = p < npx;
+  (void)npx;
+  const int64_t p = w.p_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = p < w.p_hi;
   const bool cs = in && chunk_start(w, p);
   append_lane(cs, (int32_t)p, w.chunks, w.counts);
 }
@@ -408,6 +417,12 @@ __global__ void __launch_bounds__(128, WALK_MIN_BLOCKS)
   int nopt;
   if (p == 0) {
     opts[0] = 0;  // find_simplex starts every batch at simplex 0
+    nopt = 1;
+  } else if (p == w.p_lo) {
+    // a row window's first pixel: its predecessor was not rastered.  Any
+    // start is a guess; k_mu_window_check flags the window when this run
+    // reaches the band's own rows (the caller then rasters the whole frame)
+    opts[0] = 0;
     nopt = 1;
   } else if (!ambiguous(w, p - 1)) {
     opts[0] = (int)w.tmin[p - 1];
@@ -430,9 +445,9 @@ __global__ void __launch_bounds__(128, WALK_MIN_BLOCKS)
       agnostic = agnostic && w.cnt[q] > 0 && w.vmin[q] == w.vmax[q];
       w.chunk_of[q] = (int32_t)p;
       ++q;
-    } while (q < npx && ambiguous(w, q) && !chunk_start(w, q));
+    } while (q < w.p_hi && ambiguous(w, q) && !chunk_start(w, q));
     end = q;
-    ends_run = q >= npx || !ambiguous(w, q);
+    ends_run = q >= w.p_hi || !ambiguous(w, q);
     if (agnostic && ends_run) {
       w.len[p] = (int32_t)(q - p);
       w.end0[p] = w.end1[p] = -1;  // never read: the run ends here
@@ -473,7 +488,7 @@ __global__ void k_resolve_chunks(TriDev d, int W, int64_t npx, MuWs w) {
   if (ch == 0xff) return;  // undecided: resolved by the thread of a decided predecessor
   for (;;) {
     const int64_t nxt = c + w.len[c];
-    if (nxt >= npx || !ambiguous(w, nxt) || w.chosen[nxt] != 0xff) break;
+    if (nxt >= w.p_hi || !ambiguous(w, nxt) || w.chosen[nxt] != 0xff) break;
     const int carry = ch == 1 ? w.end1[c] : w.end0[c];  // (a replayed chunk keeps its end in end0)
     uint8_t pick;
     if ((int)w.tmin[nxt - 1] == carry) {
@@ -499,8 +514,9 @@ __global__ void k_resolve_chunks(TriDev d, int W, int64_t npx, MuWs w) {
 
 __global__ void k_mu_eval(TriDev d, int W, int64_t npx, MuWs w, double clip_dmax,
                           double* __restrict__ mu) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npx) return;
+  (void)npx;
+  const int64_t p = w.b_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= w.p_hi) return;
   int s;
   bool agnostic = false;
   if (!ambiguous(w, p)) {
@@ -547,7 +563,15 @@ __global__ void __launch_bounds__(1024) k_mu_nudge(TriDev d, int W, int64_t npx,
                                                    double clip_dmax, double* __restrict__ mu) {
   __shared__ unsigned s_cnt[1024];
   if (w.counts[6] == 0u) return;  // the common case: every pixel found its simplex
-  const int64_t words = (npx + 31) / 32;
+  if (w.p_lo > 0) {
+    // the nudged batch carries its walk start from one off-hull pixel to the
+    // next in pixel order, from simplex 0: a window that starts at pixel 0
+    // replays its own misses exactly (later ones cannot affect them), any
+    // other window cannot -- flag it
+    if (threadIdx.x == 0) w.counts[5] = 1u;
+    return;
+  }
+  const int64_t words = (w.p_hi + 31) / 32;  // (a window from pixel 0: its own words)
   const int64_t per = (words + blockDim.x - 1) / blockDim.x;
   const int64_t w0 = (int64_t)threadIdx.x * per, w1 = min(w0 + per, words);
   unsigned c = 0;
@@ -832,14 +856,52 @@ extern "C" int st_tri_tables(const st_tri* tri, double* planes_out, double* tran
   return ST_OK;
 }
 
+namespace st {
+// A row window is exact when the run of ambiguous pixels that starts at its
+// first pixel (whose walk start was guessed) ends before the band's rows;
+// otherwise flag it (counts[5]).  One thread: at most the halo rows.
+__global__ void k_mu_window_check(MuWs w, int32_t* __restrict__ unsafe_out, int force) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned bad = w.counts[5] | (unsigned)force;
+  if (w.p_lo > 0 && w.p_lo < w.b_lo) {
+    int64_t q = w.p_lo;
+    while (q < w.b_lo && ambiguous(w, q)) ++q;
+    if (q >= w.b_lo) bad = 1u;
+  } else if (w.p_lo > 0) {
+    bad = 1u;  // no halo at all
+  }
+  w.counts[5] = bad;
+  if (unsafe_out) *unsafe_out = (int32_t)bad;
+}
+}  // namespace st
+
 extern "C" int64_t st_mu_raster_workspace(int32_t W, int32_t H, int32_t n_tri) {
   return (int64_t)mu_layout(W, H, n_tri).total;
 }
 
+extern "C" int st_mu_raster_rows(const st_tri* tri, int32_t W, int32_t H, double clip_dmax,
+                                 double* mu_out, void* workspace, int64_t workspace_bytes,
+                                 int32_t row0, int32_t row1, int32_t* unsafe_out,
+                                 void* stream);
+
 extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip_dmax,
                             double* mu_out, void* workspace, int64_t workspace_bytes,
                             void* stream) {
+  return st_mu_raster_rows(tri, W, H, clip_dmax, mu_out, workspace, workspace_bytes, 0, H,
+                           nullptr, stream);
+}
+
+#define MU_HALO_ROWS 2  // rows rastered above a band (their walks seed the band's)
+
+extern "C" int st_mu_raster_rows(const st_tri* tri, int32_t W, int32_t H, double clip_dmax,
+                                 double* mu_out, void* workspace, int64_t workspace_bytes,
+                                 int32_t row0, int32_t row1, int32_t* unsafe_out,
+                                 void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  if (!(0 <= row0 && row0 < row1 && row1 <= H)) {
+    sthost::set_error("st_mu_raster_rows: bad rows [%d, %d) of %d", row0, row1, H);
+    return ST_EINVAL;
+  }
   const MuLayout L = mu_layout(W, H, tri->n_tri);
   if ((int64_t)L.total > workspace_bytes) {
     sthost::set_error("mu raster workspace too small");
@@ -874,6 +936,10 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
   w.vmax = (unsigned long long*)(ws + L.off[15]);
   w.miss_bits = (unsigned*)(ws + L.miss_bits);
   w.miss_list = (int32_t*)(ws + L.miss_list);
+  const int y_lo = row0 > 0 ? std::max(0, row0 - MU_HALO_ROWS) : 0;
+  w.p_lo = (int64_t)y_lo * W;
+  w.b_lo = (int64_t)row0 * W;
+  w.p_hi = (int64_t)row1 * W;
   static const int chunk_env = [] {
     const char* e = getenv("ST_MU_CHUNK");
     const int v = e ? atoi(e) : 0;
@@ -921,7 +987,7 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
     auto* start = (unsigned long long*)(ws + L.start);
     prof();
     ST_CUDA_CHECK(cudaMemsetAsync(area + d.n_tri, 0, sizeof(unsigned long long), s));
-    st::k_tri_bbox<<<(d.n_tri + 127) / 128, 128, 0, s>>>(d, W, H, bbox, area);
+    st::k_tri_bbox<<<(d.n_tri + 127) / 128, 128, 0, s>>>(d, W, H, y_lo, row1, bbox, area);
     ST_LAUNCH_CHECK("k_tri_bbox");
     st::k_nb_equations<<<(d.n_tri + 127) / 128, 128, 0, s>>>(d, (double*)(ws + L.nb_eq));
     ST_LAUNCH_CHECK("k_nb_equations");
@@ -931,22 +997,30 @@ extern "C" int st_mu_raster(const st_tri* tri, int32_t W, int32_t H, double clip
     st::k_claim<<<sms * 8, 256, 0, s>>>(d, W, bbox, start, w);
     ST_LAUNCH_CHECK("k_claim");
   }
-  const unsigned blocks = (unsigned)((npx + 255) / 256);
+  const int64_t wpx = w.p_hi - w.p_lo;  // rastered pixels
+  const unsigned blocks = (unsigned)((wpx + 255) / 256);
   prof();
   st::k_mu_lists<<<blocks, 256, 0, s>>>(npx, w);
   ST_LAUNCH_CHECK("k_mu_lists");
   prof();
   // worklist grids are sized for the worst case; surplus threads exit at once
-  st::k_walk_chunks<<<(unsigned)((npx + 127) / 128), 128, 0, s>>>(d, W, npx, w);
+  st::k_walk_chunks<<<(unsigned)((wpx + 127) / 128), 128, 0, s>>>(d, W, npx, w);
   ST_LAUNCH_CHECK("k_walk_chunks");
   prof();
-  st::k_resolve_chunks<<<(unsigned)((npx + 127) / 128), 128, 0, s>>>(d, W, npx, w);
+  st::k_resolve_chunks<<<(unsigned)((wpx + 127) / 128), 128, 0, s>>>(d, W, npx, w);
   ST_LAUNCH_CHECK("k_resolve_chunks");
   prof();
-  st::k_mu_eval<<<blocks, 256, 0, s>>>(d, W, npx, w, clip_dmax, mu_out);
+  st::k_mu_eval<<<(unsigned)((w.p_hi - w.b_lo + 255) / 256), 256, 0, s>>>(d, W, npx, w,
+                                                                          clip_dmax, mu_out);
   ST_LAUNCH_CHECK("k_mu_eval");
   st::k_mu_nudge<<<1, 1024, 0, s>>>(d, W, npx, w, clip_dmax, mu_out);
   ST_LAUNCH_CHECK("k_mu_nudge");
+  if (row0 > 0 || row1 < H || unsafe_out) {
+    // (ST_MU_FORCE_UNSAFE: test hook for the whole-frame retry of row bands)
+    static const int force = getenv("ST_MU_FORCE_UNSAFE") != nullptr ? 1 : 0;
+    st::k_mu_window_check<<<1, 32, 0, s>>>(w, unsafe_out, (row0 > 0 || row1 < H) ? force : 0);
+    ST_LAUNCH_CHECK("k_mu_window_check");
+  }
   prof();
   if (prof_on && npev > 1) {
     cudaEventSynchronize(pev[npev - 1]);

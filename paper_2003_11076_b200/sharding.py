@@ -188,6 +188,8 @@ class BandPipeline:
         self.rec_recv = empty((self.world * nrec,), t.uint8)
         self.exchange = RecordExchange(self.rec_send, self.rec_recv, group) \
             if self.world > 1 else None
+        self.mu_unsafe = empty((1,), t.int32)
+        self.retries = 0  # frames redone with the whole-frame surface raster
 
     # -- inputs -------------------------------------------------------------------------
 
@@ -228,10 +230,20 @@ class BandPipeline:
         need = int(N.lib().st_mu_raster_workspace(W, H, tri_dev.n_tri))
         if pipe.mu_ws.numel() < need:
             pipe.mu_ws = empty((need,), t.uint8)
+        e0, e1 = self.ext["solve"]
+        banded_mu = self.world > 1 and (e0 > 0 or e1 < H)
         with t.cuda.stream(pipe.side):
             pipe.side.wait_event(ready)
-            N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max), pipe.mu,
-                     pipe.mu_ws, pipe.mu_ws.numel())
+            if banded_mu:
+                # the band's solved rows only (+ 2 halo rows of walks); the
+                # flag rides in the first statistics record (ST_EAGAIN below)
+                N.invoke("st_mu_raster_rows", tri_dev.st, W, H, float(self.prior_params.d_max),
+                         pipe.mu, pipe.mu_ws, pipe.mu_ws.numel(), e0, e1, self.mu_unsafe)
+                pipe.frame.mu_unsafe = self.mu_unsafe.data_ptr()
+            else:
+                N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max),
+                         pipe.mu, pipe.mu_ws, pipe.mu_ws.numel())
+                pipe.frame.mu_unsafe = None
             mu_done = t.cuda.Event()
             mu_done.record(pipe.side)
         need = int(N.lib().st_support_workspace(tri_dev.n_sup, W, H,
@@ -250,17 +262,29 @@ class BandPipeline:
         main.wait_event(pre_done)
         main.wait_event(mu_done)
         r0, r1 = self.ext["rows"]
-        e0, e1 = self.ext["solve"]
         ex = self.exchange
         fn = ex.fn if ex is not None else N.EXCHANGE_FN()
-        rc = N.lib().st_solve_rows(pipe.frame, pipe.rig, p, int(bool(dynamic_only)), r0, r1, e0,
-                                   e1, N.ptr(pipe.values), N.ptr(pipe.status), N.ptr(pipe.sbits),
-                                   N.ptr(pipe.vbits), N.ptr(pipe.stats_dev), N.ptr(pipe.solve_ws),
-                                   pipe.solve_ws.numel(), fn, None, self.world,
-                                   N.ptr(self.rec_send), N.ptr(self.rec_recv), N.stream_handle())
-        if rc and ex is not None and ex.error is not None:
-            raise ex.error
-        N.check(rc)
+
+        def solve():
+            rc = N.lib().st_solve_rows(
+                pipe.frame, pipe.rig, p, int(bool(dynamic_only)), r0, r1, e0, e1,
+                N.ptr(pipe.values), N.ptr(pipe.status), N.ptr(pipe.sbits), N.ptr(pipe.vbits),
+                N.ptr(pipe.stats_dev), N.ptr(pipe.solve_ws), pipe.solve_ws.numel(), fn, None,
+                self.world, N.ptr(self.rec_send), N.ptr(self.rec_recv), N.stream_handle())
+            if rc and ex is not None and ex.error is not None:
+                raise ex.error
+            N.check(rc)
+
+        try:
+            solve()
+        except N.BandRetry:
+            # some shard's row-window raster was not exact (every shard sees
+            # the same gathered records, so all of them retry together)
+            self.retries += 1
+            N.invoke("st_mu_raster", tri_dev.st, W, H, float(self.prior_params.d_max), pipe.mu,
+                     pipe.mu_ws, pipe.mu_ws.numel())
+            pipe.frame.mu_unsafe = None
+            solve()
         copy = None
         if dynamic_only:
             N.invoke("st_copy_mask", pipe.priors[pipe.rig.ref_index], H * W,

@@ -104,9 +104,11 @@ def test_gloo_ranks_exchange_and_gather(world):
         assert ok_x and ok_g, rank
 
 
-def _band_gpu_worker(rank, world, port, q, dynamic_only):
+def _band_gpu_worker(rank, world, port, q, dynamic_only, force_retry=False):
     import torch
     import torch.distributed as dist
+    if force_retry:
+        os.environ["ST_MU_FORCE_UNSAFE"] = "1"
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -120,6 +122,9 @@ def _band_gpu_worker(rank, world, port, q, dynamic_only):
         sp, pp = _params(st, g)
         frame, rig, tri = _frame(st, g), _Rig(g), _Tri(g)
         r = reconstruct_band(frame, rig, tri, sp, pp, dynamic_only=dynamic_only)
+        from paper_2003_11076_b200.sharding import _BANDS
+        retries = sum(b.retries for b in _BANDS.values())
+        assert (retries > 0) == force_retry, retries
         out = None
         if r is not None:
             out = dict(values=r.disparity.values, status=r.disparity.status,
@@ -136,14 +141,18 @@ def _band_gpu_worker(rank, world, port, q, dynamic_only):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,dynamic_only", [(2, False), (3, False), (2, True)])
-def test_row_bands_match_single_device(world, dynamic_only):
+@pytest.mark.parametrize("world,dynamic_only,force_retry",
+                         [(2, False, False), (3, False, False), (2, True, False),
+                          (3, False, True)])
+def test_row_bands_match_single_device(world, dynamic_only, force_retry):
     """`reconstruct_band` over 2-3 processes (gloo collectives, one GPU; no
     kernel waits on another process) reproduces the single-device
     `reconstruct` bit for bit: disparity, status, bits, refocused image
     (median halo rows included), provenance, n_rays; EMStats iterations,
     changed fractions exact, energies to 1e-12 (a different summation
-    order).  solve_band likewise."""
+    order).  solve_band likewise.  force_retry: every shard's row-window
+    surface raster is flagged inexact, so every shard redoes the frame with
+    the whole-frame raster (ST_EAGAIN) -- same results."""
     import torch.multiprocessing as mp
 
     import paper_2003_11076_b200 as st
@@ -155,7 +164,8 @@ def test_row_bands_match_single_device(world, dynamic_only):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_band_gpu_worker, args=(r, world, port, q, dynamic_only))
+    procs = [ctx.Process(target=_band_gpu_worker,
+                         args=(r, world, port, q, dynamic_only, force_retry))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -247,3 +257,44 @@ def test_banded_solve_matches_full_solve():
         assert stats.iterations_run == full_stats.iterations_run
         assert stats.converged_after == full_stats.converged_after
         assert np.allclose(stats.mean_energy, full_stats.mean_energy, rtol=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_row_window_mu_raster_equals_whole_frame(cfg):
+    """st_mu_raster_rows (a band's rows + 2 halo rows of Qhull-walk replay)
+    gives the whole-frame raster's mu bit for bit on the band's rows, for
+    the bands of 2, 3, 5 and 8 shards (a window it cannot make exact must
+    say so)."""
+    import torch
+
+    import bench
+    from paper_2003_11076_b200 import _native as N
+    from paper_2003_11076_b200.prior import TriDevice
+    from paper_2003_11076_b200.sharding import band_extents
+    frame, rig, tri, _ = bench.load_inputs(cfg)
+    sp, pp = bench.params_for(cfg)
+    h, w = frame.shape
+    td = TriDevice(tri)
+    ws = torch.empty(int(N.lib().st_mu_raster_workspace(w, h, td.n_tri)), dtype=torch.uint8,
+                     device="cuda")
+    full = torch.empty(h * w, dtype=torch.float64, device="cuda")
+    N.invoke("st_mu_raster", td.st, w, h, float(pp.d_max), full, ws, ws.numel())
+    want = full.cpu().numpy().reshape(h, w)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    unsafe = checked = 0
+    for world in (2, 3, 5, 8):
+        for rank in range(world):
+            e0, e1 = band_extents(h, world, rank, 1, True)["solve"]
+            mu = torch.full((h * w,), float("nan"), dtype=torch.float64, device="cuda")
+            N.invoke("st_mu_raster_rows", td.st, w, h, float(pp.d_max), mu, ws, ws.numel(), e0,
+                     e1, flag)
+            if int(flag.item()):
+                unsafe += 1
+                continue
+            got = mu.cpu().numpy().reshape(h, w)[e0:e1]
+            assert np.array_equal(got.view(np.uint64), want[e0:e1].view(np.uint64)), \
+                (world, rank, int((got != want[e0:e1]).sum()))
+            checked += 1
+    print(f"{cfg}: {checked} band windows exact, {unsafe} flagged for the whole-frame raster")
+    assert checked > 0
