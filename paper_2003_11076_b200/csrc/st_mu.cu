@@ -563,19 +563,26 @@ __global__ void __launch_bounds__(1024) k_mu_nudge(TriDev d, int W, int64_t npx,
                                                    double clip_dmax, double* __restrict__ mu) {
   __shared__ unsigned s_cnt[1024];
   if (w.counts[6] == 0u) return;  // the common case: every pixel found its simplex
-  if (w.p_lo > 0) {
-    // the nudged batch carries its walk start from one off-hull pixel to the
-    // next in pixel order, from simplex 0: a window that starts at pixel 0
-    // replays its own misses exactly (later ones cannot affect them), any
-    // other window cannot -- flag it
-    if (threadIdx.x == 0) w.counts[5] = 1u;
-    return;
-  }
-  const int64_t words = (w.p_hi + 31) / 32;  // (a window from pixel 0: its own words)
-  const int64_t per = (words + blockDim.x - 1) / blockDim.x;
-  const int64_t w0 = (int64_t)threadIdx.x * per, w1 = min(w0 + per, words);
+  // The nudged batch carries its walk start from one off-hull pixel to the
+  // next in pixel order, from simplex 0.  A window from pixel 0 replays its
+  // own misses exactly (later ones cannot affect them).  A window further
+  // down does not know the start its first miss inherits: its results are
+  // still exact when every nudged point has at most one claiming triangle
+  // (then any walk ends there, or outside for the nearest-vertex fallback),
+  // which the block checks below; otherwise the window is flagged.
+  const bool windowed = w.p_lo > 0;
+  const int64_t word_lo = w.p_lo >> 5;
+  const int64_t words = (w.p_hi + 31) / 32;
+  const int64_t nw = words - word_lo;
+  const int64_t per = (nw + blockDim.x - 1) / blockDim.x;
+  const int64_t w0 = word_lo + (int64_t)threadIdx.x * per, w1 = min(w0 + per, words);
+  const unsigned lo_mask = ~0u << (unsigned)(w.p_lo & 31);  // (bits below p_lo are stale)
+  auto miss_word = [&](int64_t i) {
+    const unsigned b = w.miss_bits[i];
+    return i == word_lo ? (b & lo_mask) : b;
+  };
   unsigned c = 0;
-  for (int64_t i = w0; i < w1; ++i) c += __popc(w.miss_bits[i]);
+  for (int64_t i = w0; i < w1; ++i) c += __popc(miss_word(i));
   s_cnt[threadIdx.x] = c;
   __syncthreads();
   if (threadIdx.x == 0) {  // exclusive scan (1024 entries)
@@ -593,7 +600,10 @@ __global__ void __launch_bounds__(1024) k_mu_nudge(TriDev d, int W, int64_t npx,
   if (total <= NUDGE_CAP) {
     unsigned o = s_cnt[threadIdx.x];
     for (int64_t i = w0; i < w1; ++i)
-      for (unsigned b = w.miss_bits[i]; b; b &= b - 1) w.miss_list[o++] = (int32_t)(i * 32 + __ffs(b) - 1);
+      for (unsigned b = miss_word(i); b; b &= b - 1) w.miss_list[o++] = (int32_t)(i * 32 + __ffs(b) - 1);
+  } else if (windowed) {
+    if (threadIdx.x == 0) w.counts[5] = 1u;  // (never seen) flag the window
+    return;
   }
   __syncthreads();
   // vertex centroid (NaN from the host: integer coordinates, exact sums in
@@ -618,6 +628,29 @@ __global__ void __launch_bounds__(1024) k_mu_nudge(TriDev d, int W, int64_t npx,
     }
     dd.cen0 = ddiv(s_sum[0][0], (double)d.n_pts);
     dd.cen1 = ddiv(s_sum[1][0], (double)d.n_pts);
+  }
+  if (windowed) {
+    // claimers of every nudged point (Qhull's inclusion test, as k_claim)
+    __shared__ unsigned s_multi;
+    if (threadIdx.x == 0) s_multi = 0u;
+    __syncthreads();
+    for (unsigned j = 0; j < total; ++j) {
+      const int64_t p = w.miss_list[j];
+      const double u = (double)(p % W), v = (double)(p / W);
+      const double x0 = dadd(u, dmul(1e-9, dsub(dd.cen0, u)));
+      const double x1 = dadd(v, dmul(1e-9, dsub(dd.cen1, v)));
+      unsigned k = 0;
+      for (int t = threadIdx.x; t < d.n_tri; t += blockDim.x)
+        k += bary_inside(d.transform + 6 * t, x0, x1) ? 1u : 0u;
+      k = __reduce_add_sync(0xffffffffu, k);
+      if ((threadIdx.x & 31) == 0 && k) atomicAdd(&s_multi, k);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (s_multi >= 2u) w.counts[5] = 1u;
+        s_multi = 0u;
+      }
+      __syncthreads();
+    }
   }
   if (threadIdx.x != 0) return;
   int start = 0;

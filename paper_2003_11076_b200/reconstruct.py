@@ -49,9 +49,13 @@ class Reconstruction:
 class FramePipeline:
     """Persistent device buffers for frames of shape (K, H, W)."""
 
-    def __init__(self, rig, width, height, params=None, prior_params=None):
+    def __init__(self, rig, width, height, params=None, prior_params=None, guard_bytes=0):
         t = require_cuda()
         self.t = t
+        # guard_bytes > 0 (tests): every device buffer sits between two guard
+        # zones of a known pattern; check_guards() finds out-of-bounds writes
+        self.guard_bytes = int(guard_bytes)
+        self._guards = []
         self.K = len(rig)
         _check_views(self.K)
         self.W, self.H = int(width), int(height)
@@ -60,23 +64,23 @@ class FramePipeline:
         self.rig_obj = rig
         self.rig = N.make_rig(rig, self.W, self.H)
         K, H, W = self.K, self.H, self.W
-        self.images = empty((K, H, W, 3), t.uint8)
-        self.priors = empty((K, H, W), t.float32)
-        self.desc = empty((K, H, W, 16), t.uint8)
-        self.mu = empty((H * W,), t.float64)
-        self.mu_ws = empty((1,), t.uint8)
-        self.sup_ws = empty((1,), t.uint8)
-        self.solve_ws = empty((int(N.lib().st_solve_workspace(W, H, K)),), t.uint8)
-        self.values = empty((H, W), t.float32)
-        self.status = empty((H, W), t.uint8)
-        self.sbits = empty((H, W), t.int32)
-        self.vbits = empty((H, W), t.int32)
-        self.image = empty((H, W, 3), t.uint8)
-        self.prov = empty((H, W), t.uint8)
-        self.n_rays = empty((H, W), t.uint8)
-        self.scratch = empty((H, W, 3), t.uint8)
-        self.copy = empty((H, W), t.uint8)
-        self.stats_dev = empty((N.C.sizeof(N.StStats),), t.uint8)
+        self.images = self._empty((K, H, W, 3), t.uint8)
+        self.priors = self._empty((K, H, W), t.float32)
+        self.desc = self._empty((K, H, W, 16), t.uint8)
+        self.mu = self._empty((H * W,), t.float64)
+        self.mu_ws = self._empty((1,), t.uint8)
+        self.sup_ws = self._empty((1,), t.uint8)
+        self.solve_ws = self._empty((int(N.lib().st_solve_workspace(W, H, K)),), t.uint8)
+        self.values = self._empty((H, W), t.float32)
+        self.status = self._empty((H, W), t.uint8)
+        self.sbits = self._empty((H, W), t.int32)
+        self.vbits = self._empty((H, W), t.int32)
+        self.image = self._empty((H, W, 3), t.uint8)
+        self.prov = self._empty((H, W), t.uint8)
+        self.n_rays = self._empty((H, W), t.uint8)
+        self.scratch = self._empty((H, W, 3), t.uint8)
+        self.copy = self._empty((H, W), t.uint8)
+        self.stats_dev = self._empty((N.C.sizeof(N.StStats),), t.uint8)
         self.frame = N.StFrame()
         self.frame.images = self.images.data_ptr()
         self.frame.priors = self.priors.data_ptr()
@@ -88,6 +92,24 @@ class FramePipeline:
         prio = int(os.environ.get("ST_SIDE_PRIORITY", "-1"))
         self.side = t.cuda.Stream(priority=prio)
         self.side2 = t.cuda.Stream()
+
+    def _empty(self, shape, dtype):
+        if not self.guard_bytes:
+            return empty(shape, dtype)
+        t = self.t
+        n = int(np.prod(shape)) * t.empty((), dtype=dtype).element_size()
+        g = (self.guard_bytes + 255) & ~255
+        raw = empty((n + 2 * g,), t.uint8)
+        raw.fill_(0xA5)
+        self._guards.append((raw, g, n))
+        return raw[g:g + n].view(dtype).view(shape)
+
+    def check_guards(self):
+        """Number of guard-zone bytes overwritten since allocation (0 = none)."""
+        bad = 0
+        for raw, g, n in self._guards:
+            bad += int((raw[:g] != 0xA5).sum()) + int((raw[g + n:] != 0xA5).sum())
+        return bad
 
     # -- inputs ---------------------------------------------------------------------
 
@@ -121,13 +143,13 @@ class FramePipeline:
         if getattr(self, "_hv_key", None) != stride:
             lib = N.lib()
             cap = max(int(lib.st_harvest_capacity(K, W, H, stride)), 1)
-            self.hv_ws = empty((max(int(lib.st_harvest_workspace(K, W, H, stride)), 1),),
+            self.hv_ws = self._empty((max(int(lib.st_harvest_workspace(K, W, H, stride)), 1),),
                                t.uint8)
-            self.hv_u = empty((cap,), t.int32)
-            self.hv_v = empty((cap,), t.int32)
-            self.hv_d = empty((cap,), t.float64)
-            self.hv_src = empty((cap,), t.int32)
-            self.hv_n = empty((1,), t.int64)
+            self.hv_u = self._empty((cap,), t.int32)
+            self.hv_v = self._empty((cap,), t.int32)
+            self.hv_d = self._empty((cap,), t.float64)
+            self.hv_src = self._empty((cap,), t.int32)
+            self.hv_n = self._empty((1,), t.int64)
             self.cams = N.make_cams(self.rig_obj, W, H)
             self._hv_key = stride
         N.invoke("st_descriptors", self.images, K, H, W, 3, self.desc, None, None)
@@ -168,7 +190,7 @@ class FramePipeline:
         mark()
         need = int(N.lib().st_mu_raster_workspace(W, H, tri_dev.n_tri))
         if self.mu_ws.numel() < need:
-            self.mu_ws = empty((need,), t.uint8)
+            self.mu_ws = self._empty((need,), t.uint8)
         if ready is None:
             ready = t.cuda.Event()
             ready.record(main)
@@ -181,7 +203,7 @@ class FramePipeline:
         need = int(N.lib().st_support_workspace(tri_dev.n_sup, W, H,
                                                 float(self.prior_params.neighborhood_radius)))
         if self.sup_ws.numel() < need:
-            self.sup_ws = empty((need,), t.uint8)
+            self.sup_ws = self._empty((need,), t.uint8)
         # no host round trip unless a diagnostic path wants the record count
         # (dynamic_only: st_solve_rows reads the active-list size back once)
         run_async = not dynamic_only and reduce is None and not timing
@@ -266,11 +288,11 @@ class FramePipeline:
         P.median_radius = int(median_radius)
         need = int(lib.st_mu_raster_workspace(W, H, tri_dev.n_tri))
         if self.mu_ws.numel() < need:
-            self.mu_ws = empty((need,), t.uint8)
+            self.mu_ws = self._empty((need,), t.uint8)
         need = int(lib.st_support_workspace(tri_dev.n_sup, W, H,
                                             float(self.prior_params.neighborhood_radius)))
         if self.sup_ws.numel() < need:
-            self.sup_ws = empty((need,), t.uint8)
+            self.sup_ws = self._empty((need,), t.uint8)
         P.mu_ws, P.mu_ws_bytes = self.mu_ws.data_ptr(), self.mu_ws.numel()
         P.sup_ws, P.sup_ws_bytes = self.sup_ws.data_ptr(), self.sup_ws.numel()
         P.main_stream = t.cuda.current_stream().cuda_stream

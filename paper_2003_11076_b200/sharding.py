@@ -166,7 +166,7 @@ class BandPipeline:
     frame only moves and computes its band's rows (+ halos)."""
 
     def __init__(self, rig, width, height, params=None, prior_params=None, group=None,
-                 median_radius=1):
+                 median_radius=1, guard_bytes=0):
         from .prior import PriorParams
         from .reconstruct import FramePipeline
         from .solver import SolverParams
@@ -178,7 +178,8 @@ class BandPipeline:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.params = params or SolverParams()
         self.prior_params = prior_params or PriorParams()
-        self.pipe = FramePipeline(rig, width, height, self.params, self.prior_params)
+        self.pipe = FramePipeline(rig, width, height, self.params, self.prior_params,
+                                  guard_bytes=guard_bytes)
         self.K, self.H, self.W = self.pipe.K, self.pipe.H, self.pipe.W
         self.rectified = is_rectified(rig)
         self.median_radius = int(median_radius)
@@ -229,7 +230,7 @@ class BandPipeline:
         ready.record(main)
         need = int(N.lib().st_mu_raster_workspace(W, H, tri_dev.n_tri))
         if pipe.mu_ws.numel() < need:
-            pipe.mu_ws = empty((need,), t.uint8)
+            pipe.mu_ws = pipe._empty((need,), t.uint8)
         e0, e1 = self.ext["solve"]
         banded_mu = self.world > 1 and (e0 > 0 or e1 < H)
         with t.cuda.stream(pipe.side):
@@ -249,7 +250,7 @@ class BandPipeline:
         need = int(N.lib().st_support_workspace(tri_dev.n_sup, W, H,
                                                 float(self.prior_params.neighborhood_radius)))
         if pipe.sup_ws.numel() < need:
-            pipe.sup_ws = empty((need,), t.uint8)
+            pipe.sup_ws = pipe._empty((need,), t.uint8)
         d0, d1 = self.ext["desc"]
         with t.cuda.stream(pipe.side2):
             pipe.side2.wait_event(ready)
