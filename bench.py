@@ -479,6 +479,87 @@ def config_block(cfg, args, exact):
             "forced_iters": args.forced_iters or None}
 
 
+# -- C5: a 1000-frame sequence of 16 distinct frames, frame-parallel -------------------------
+
+C5_FRAMES, C5_DISTINCT, C5_SEED0 = 1000, 16, 11
+
+
+def _render_c5(seed):
+    """One distinct C5 frame (occluder_scene seeds 11..26)."""
+    from paper_2003_11076_b200 import synth
+    w, h, k, dmax, iters = CONFIGS["C2"]
+    sc = dict(SCENE, seed=seed)
+    frame, _ = synth.render(synth.occluder_scene(width=w, height=h, cameras=k, **sc))
+    return np.stack(frame.images), np.stack(frame.priors)
+
+
+def measure_sequence(dist, rank, world, flush=None):
+    """BASELINE configs[4]: 1000 frames cycling 16 distinct rendered C2 frames,
+    split frame-parallel over the ranks (frame i on rank i % N), through the
+    pipelined public API from pinned host memory with the artefacts copied
+    back (host I/O inside the timed region).  The 16 frames' support points
+    and triangulations are computed once (device harvest + host Qhull), not
+    timed, as SURVEY.md §8d prescribes.  Total work is fixed: strong
+    scaling; time = max over ranks."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    import torch
+    import paper_2003_11076_b200 as st
+    w, h, k, dmax, iters = CONFIGS["C2"]
+    sp, pp = params_for("C2")
+    mine = [i for i in range(C5_FRAMES) if i % world == rank]
+    need = sorted({i % C5_DISTINCT for i in mine})
+    t0 = time.perf_counter()
+    workers = max(1, min(len(need), cpu_cores()))
+    with cf.ProcessPoolExecutor(workers, mp_context=mp.get_context("spawn")) as ex:
+        rendered = dict(zip(need, ex.map(_render_c5, [C5_SEED0 + j for j in need])))
+    t_render = time.perf_counter() - t0
+    from paper_2003_11076_b200 import synth
+    rig = synth.occluder_scene(width=w, height=h, cameras=k, **SCENE).rig()
+    pairs = {}
+    t0 = time.perf_counter()
+    for j, (imgs, pris) in rendered.items():
+        pin_i = st.device.pinned_empty(imgs.shape, np.uint8)
+        pin_p = st.device.pinned_empty(pris.shape, np.float32)
+        pin_i[...] = imgs
+        pin_p[...] = pris
+        frame = st.LightFieldFrame(images=list(pin_i), priors=list(pin_p))
+        sup = st.collect_support(frame, rig, pp, threshold=sp.threshold)
+        pairs[j] = (frame, st.triangulate(sup, w, h))
+    t_prep = time.perf_counter() - t0
+    seq = [pairs[i % C5_DISTINCT] for i in mine]
+
+    def run(items):
+        n = 0
+        for _ in st.reconstruct_stream(items, rig, sp, pp):
+            n += 1
+        return n
+
+    run(seq[:8])  # warm-up
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    n = run(seq)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    if dist is not None:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    assert n == len(mine)
+    f0 = pairs[need[0]][0]
+    h2d = sum(a.nbytes for a in f0.images) + sum(a.nbytes for a in f0.priors)
+    return {"config": "C5", "frames": C5_FRAMES, "distinct_frames": C5_DISTINCT,
+            "value": C5_FRAMES / (ms / 1e3), "unit": "frames/s", "n_gpus": world,
+            "ms_total": ms, "scaling": "strong",
+            "frames_per_rank": len(mine), "distinct_per_rank": len(need),
+            "h2d_frame_bytes": int(h2d), "d2h_bytes_per_frame": int(w * h * 18),
+            "api": "reconstruct_stream from pinned host frames, artefacts to host, "
+                   "host wall clock, max over ranks",
+            "untimed_setup_s": {"render": t_render, "support_and_triangulation": t_prep}}
+
+
 # -- row bands (BASELINE C3/C4: one frame split across the ranks) -------------------------
 
 def measure_row_bands(cfg, steps, warmup, dist, rank, world, flush):
@@ -862,6 +943,14 @@ def run_ours(args):
         except Exception as exc:  # noqa: BLE001 -- reported, the frame-parallel line stands
             row_bands = {"error": f"{type(exc).__name__}: {exc}"}
 
+    # -- BASELINE configs[4]: the C5 sequence (1000 frames, 16 distinct) over the ranks
+    sequence = None
+    if args.sequence and not args.forced_iters:
+        try:
+            sequence = measure_sequence(dist, rank, world)
+        except Exception as exc:  # noqa: BLE001 -- reported, the main line stands
+            sequence = {"error": f"{type(exc).__name__}: {exc}"}
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -987,6 +1076,7 @@ def run_ours(args):
         "gpix_plane_per_s": w * h * dmax * fps / 1e9,
         "forced_iters_mode": forced,
         "row_bands_C3": row_bands,
+        "sequence_C5": sequence,
         "next_rows": nxt,
         "pipelined_resident": {"value": pipelined_fps, "unit": "frames/s",
                                "ms_per_frame": pipe_ms / n_pipe, "frames": n_pipe,
@@ -1021,6 +1111,8 @@ def main():
     ap.add_argument("--row-band-steps", type=int, default=10,
                     help="frame-parallel runs also time C3 row bands over the same ranks "
                          "(0 = skip)")
+    ap.add_argument("--no-sequence", dest="sequence", action="store_false",
+                    help="skip the C5 sequence (1000 frames, 16 distinct) measurement")
     ap.add_argument("--budget", type=float, default=150.0,
                     help="reference arm: seconds for the whole run")
     args = ap.parse_args()
