@@ -455,7 +455,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(cfg, args, exact),
+        "config": dict(config_block(cfg, args, exact), l2="CPU arm: not applicable"),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cpu_cores(),
                          "kind": "port", "sample": sample, "cpu_model": cpu_model(),
                          "step_s": times},
@@ -474,7 +474,8 @@ def config_block(cfg, args, exact):
             "width": w, "height": h, "views": k, "d_max": dmax, "max_iters": iters,
             "scene": "occluder_scene(coverage=0.25, seed=11, p_flip=0.1, blur_radius=2)",
             "inputs_match_reference_digest": bool(exact),
-            "l2": "flushed between steps (256 MiB write)",
+            "l2": "two resident frame slots alternate (pre-solve of frame i+1 overlaps the "
+                  "EM of frame i); their ~300 MB working set exceeds the 126 MB L2, no flush",
             "parallelism": f"frame-parallel x{args.gpus}" if args.gpus > 1 else "1 GPU",
             "forced_iters": args.forced_iters or None}
 
@@ -683,7 +684,8 @@ def run_rows(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference renderer, reference support harvest)",
             "config": dict(config_block(cfg, args, r["inputs_match_reference_digest"]),
-                           parallelism=f"row bands x{world}"),
+                           parallelism=f"row bands x{world}",
+                           l2="flushed between steps (256 MiB write)"),
             "e2e": {"value": r["e2e"]["value"], "unit": "frames/s",
                     "h2d_bytes_per_step": r["e2e"]["h2d_bytes_per_step_max_rank"],
                     "d2h_bytes_per_step": r["e2e"]["d2h_bytes_per_step"]},
@@ -732,32 +734,43 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        pipe.run(tdev, forced_iters=args.forced_iters)
-    torch.cuda.synchronize()
+    # -- value: K frames on resident inputs, the production way: two frame slots
+    # alternate, each frame's pre-solve stages (side streams: surface raster,
+    # descriptors, support groups) overlapping the previous frame's EM.  The
+    # two slots' working set (~300 MB: views, priors, descriptor maps, EM
+    # state) exceeds the 126 MB L2, so no flush is needed between steps.
+    pipe2 = FramePipeline(rig, w, h, sp, pp)
+    pipe2.load(frame.images, frame.priors)
+    tdev2 = TriDevice(tri)
+    slots = [(pipe, tdev), (pipe2, tdev2)]
+    done_ev = [None, None]
 
-    # -- value: K steps on resident inputs, L2 flushed between steps ------------------
-    # (the production path: no host round trip inside a frame)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    def pipelined(n, events=None):
+        for j in range(n):
+            pp_, td_ = slots[j % 2]
+            ready = torch.cuda.Event()
+            if done_ev[j % 2] is not None:
+                ready = done_ev[j % 2]      # slot free once its previous frame finished
+            else:
+                ready.record(stream)
+            pp_.run(td_, forced_iters=args.forced_iters, ready=ready)
+            ev = torch.cuda.Event(enable_timing=events is not None)
+            ev.record(stream)
+            done_ev[j % 2] = ev
+            if events is not None:
+                events.append(ev)
+
+    pipelined(max(args.warmup, 4))
     barrier()
+    p0 = torch.cuda.Event(enable_timing=True)
+    marks = []
     launches0 = lib.st_launch_count()
-    with ClockSampler(local) as clocks:
-        for i in range(args.steps):
-            flush.fill_(i & 0xff)
-            starts[i].record(stream)
-            pipe.run(tdev, forced_iters=args.forced_iters)
-            ends[i].record(stream)
+    with ClockSampler(local) as clocks:  # (NVML starts before the first event)
+        p0.record(stream)
+        pipelined(args.steps, marks)
         barrier()
     launches = lib.st_launch_count() - launches0
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    # per-stage / per-kernel CUDA-event breakdown of the same workload (the
-    # synchronous solve variant records events around every kernel group)
-    stats = []
-    for i in range(args.steps):
-        flush.fill_(i & 0xff)
-        stats.append(pipe.run(tdev, forced_iters=args.forced_iters, timing=True))
-    barrier()
+    step_ms = [p0.elapsed_time(marks[0])] + [a.elapsed_time(b) for a, b in zip(marks, marks[1:])]
     total_ms = float(np.sum(step_ms))
     if dist is not None:
         tt = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
@@ -765,9 +778,32 @@ def run_ours(args):
         total_ms = float(tt.item())
     fps = world * args.steps / (total_ms / 1e3)
 
+    # -- one frame at a time, L2 flushed before each (the single-frame latency)
+    for _ in range(3):
+        pipe.run(tdev, forced_iters=args.forced_iters)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        starts[i].record(stream)
+        pipe.run(tdev, forced_iters=args.forced_iters)
+        ends[i].record(stream)
+    barrier()
+    latency_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(starts, ends)]))
+    # per-stage / per-kernel CUDA-event breakdown of the same workload (the
+    # synchronous solve variant records events around every kernel group)
+    stats = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        stats.append(pipe.run(tdev, forced_iters=args.forced_iters, timing=True))
+    barrier()
+
     if args.quick:
         if rank == 0:
             print(json.dumps({"value": fps, "ms_per_step": total_ms / args.steps,
+                              "single_frame_ms": latency_ms,
                               "stage_ms": {n: float(np.mean([s.stage_ms[n] for s in stats]))
                                            for n in stats[0].stage_ms},
                               "kernel_ms": [float(np.mean([s.kernel_ms[j] for s in stats]))
@@ -882,40 +918,6 @@ def run_ours(args):
     tdv = TriDevice(tri)
     h2d = sum(a.nbytes for a in pin_imgs) + sum(a.nbytes for a in pin_pris) + tdv.nbytes
     d2h = pipe.output_bytes()
-
-    # -- pipelined device-resident throughput: two resident frame slots alternate,
-    # each frame's pre-solve stages (side streams) overlapping the previous
-    # frame's EM; the two slots' working set (~300 MB) exceeds the 126 MB L2 -----
-    pipe2 = FramePipeline(rig, w, h, sp, pp)
-    pipe2.load(frame.images, frame.priors)
-    tdev2 = TriDevice(tri)
-    slots = [(pipe, tdev), (pipe2, tdev2)]
-    done_ev = [None, None]
-
-    def pipelined(n):
-        for j in range(n):
-            pp_, td_ = slots[j % 2]
-            ready = torch.cuda.Event()
-            if done_ev[j % 2] is not None:
-                ready = done_ev[j % 2]      # slot free once its previous frame finished
-            else:
-                ready.record(stream)
-            pp_.run(td_, forced_iters=args.forced_iters, ready=ready)
-            ev = torch.cuda.Event()
-            ev.record(stream)
-            done_ev[j % 2] = ev
-
-    pipelined(4)
-    barrier()
-    p0 = torch.cuda.Event(enable_timing=True)
-    p1 = torch.cuda.Event(enable_timing=True)
-    n_pipe = max(args.steps, 20)
-    p0.record(stream)
-    pipelined(n_pipe)
-    p1.record(stream)
-    barrier()
-    pipe_ms = max_ranks(p0.elapsed_time(p1))
-    pipelined_fps = world * n_pipe / (pipe_ms / 1e3)
 
     # -- forced-5 (non-reference bench mode): exactly max_iters EM iterations -----------
     forced = None
@@ -1078,11 +1080,10 @@ def run_ours(args):
         "row_bands_C3": row_bands,
         "sequence_C5": sequence,
         "next_rows": nxt,
-        "pipelined_resident": {"value": pipelined_fps, "unit": "frames/s",
-                               "ms_per_frame": pipe_ms / n_pipe, "frames": n_pipe,
-                               "note": "two resident frame slots, frame i+1's descriptors / "
-                                       "support groups / mu raster overlap frame i's EM; "
-                                       "no L2 flush (working set > L2)"},
+        "single_frame": {"value": 1e3 / latency_ms, "unit": "frames/s",
+                         "ms_per_frame": latency_ms,
+                         "note": "one frame at a time on one slot, L2 flushed (256 MiB "
+                                 "write) before each: the per-frame latency"},
     }
     print(json.dumps(out), flush=True)
     if dist is not None:
