@@ -106,15 +106,24 @@ class TriDevice:
         points = np.asarray(tri.points, dtype=np.float64).reshape(-1, 2)
         self.device_tables = _integral_coords(points)
         n_tri = int(np.asarray(tri.triangles).shape[0])
+        disps = np.asarray(tri.disparities, dtype=np.float64).reshape(-1)
+        sd = np.asarray(sd, dtype=np.float64).reshape(-1)
+        # the support list is the leading rows of the vertex list (prior.py:312-315):
+        # alias it on the device instead of sending it twice
+        self.sup_alias = (sp.shape[0] <= points.shape[0] and sd.shape[0] == sp.shape[0]
+                          and sp.ctypes.data == points.ctypes.data
+                          and sp.strides == points.strides
+                          and sd.ctypes.data == disps.ctypes.data
+                          and sd.strides == disps.strides)
         parts = [
             ("points", points),
-            ("disparities", np.asarray(tri.disparities, dtype=np.float64).reshape(-1)),
+            ("disparities", disps),
             ("triangles", np.asarray(tri.triangles, dtype=np.int32).reshape(-1, 3)),
             ("neighbors", np.asarray(dl.neighbors, dtype=np.int32).reshape(-1, 3)),
             ("equations", np.asarray(dl.equations, dtype=np.float64).reshape(-1, 4)),
-            ("sup_uv", sp),
-            ("sup_d", np.asarray(sd, dtype=np.float64).reshape(-1)),
         ]
+        if not self.sup_alias:
+            parts += [("sup_uv", sp), ("sup_d", sd)]
         if not self.device_tables:
             parts += [("planes", np.asarray(tri.planes, dtype=np.float64).reshape(-1, 3)),
                       ("transform", np.asarray(dl.transform, dtype=np.float64).reshape(-1, 3, 2))]
@@ -163,6 +172,9 @@ class TriDevice:
         self.n_pts = points.shape[0]
         self.n_tri = n_tri
         self.n_sup = int(sp.shape[0])
+        if self.sup_alias:
+            self.sup_uv = self.points[:self.n_sup] if self.n_sup else None
+            self.sup_d = self.disparities[:self.n_sup] if self.n_sup else None
         if self.device_tables:
             self.planes = self.buffer[t_planes:t_planes + n_tri * 24].view(torch.float64)
             self.transform = self.buffer[t_transform:t_transform + n_tri * 48].view(torch.float64)
@@ -200,7 +212,8 @@ class TriDevice:
 
     @property
     def nbytes(self):
-        return self.n_pts * 24 + self.n_tri * (12 + 12 + 32) + self.n_sup * 24 + (
+        return self.n_pts * 24 + self.n_tri * (12 + 12 + 32) + (
+            0 if self.sup_alias else self.n_sup * 24) + (
             0 if self.device_tables else self.n_tri * 72)
 
     def tensors(self):
