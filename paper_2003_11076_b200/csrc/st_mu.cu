@@ -656,62 +656,6 @@ __global__ void __launch_bounds__(1024) k_mu_nudge(TriDev d, int W, int64_t npx,
       __syncthreads();
     }
   }
-  // The walks below carry their start from miss to miss (one thread), but
-  // the two full scans they may need do not depend on it: the block does them
-  // first for every miss -- scipy's brute force (the lowest-index valid
-  // simplex whose barycentric test passes, at the nudged point) into
-  // final_s[p] and cKDTree's nearest vertex of the pixel (first minimum)
-  // into res1[p] (both per-pixel arrays are free once k_mu_eval has run).
-  if (total <= NUDGE_CAP) {
-    __shared__ int s_bf;
-    for (unsigned j = 0; j < total; ++j) {
-      const int64_t p = w.miss_list[j];
-      const double u = (double)(p % W), v = (double)(p / W);
-      const double x0 = dadd(u, dmul(1e-9, dsub(dd.cen0, u)));
-      const double x1 = dadd(v, dmul(1e-9, dsub(dd.cen1, v)));
-      if (threadIdx.x == 0) s_bf = INT_MAX;
-      __syncthreads();
-      int bf = INT_MAX;
-      for (int t = threadIdx.x; t < d.n_tri; t += blockDim.x) {
-        const double* T = d.transform + 6 * t;
-        if (T[0] == T[0] && bary_inside(T, x0, x1)) {
-          bf = t;
-          break;  // (t increases: this thread's first is its minimum)
-        }
-      }
-      if (bf != INT_MAX) atomicMin(&s_bf, bf);
-      // nearest vertex: the (d2, index) lexicographic minimum (cKDTree's first
-      // minimum), per thread over increasing indices, then a block tree
-      double bd = INFINITY;
-      int bi = INT_MAX;
-      for (int i = threadIdx.x; i < d.n_pts; i += blockDim.x) {
-        const double dx = d.pts[2 * i] - u, dy = d.pts[2 * i + 1] - v;
-        const double d2 = dx * dx + dy * dy;
-        if (d2 < bd) {
-          bd = d2;
-          bi = i;
-        }
-      }
-      s_sum[0][threadIdx.x] = bd;
-      s_cnt[threadIdx.x] = (unsigned)bi;
-      __syncthreads();
-      for (int h = blockDim.x / 2; h > 0; h >>= 1) {
-        if ((int)threadIdx.x < h) {
-          const double od = s_sum[0][threadIdx.x + h];
-          const unsigned oi = s_cnt[threadIdx.x + h];
-          if (od < s_sum[0][threadIdx.x] ||
-              (od == s_sum[0][threadIdx.x] && oi < s_cnt[threadIdx.x])) {
-            s_sum[0][threadIdx.x] = od;
-            s_cnt[threadIdx.x] = oi;
-          }
-        }
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) w.res1[p] = (int32_t)s_cnt[0];
-      if (threadIdx.x == 0) w.final_s[p] = s_bf == INT_MAX ? -1 : s_bf;
-      __syncthreads();
-    }
-  }
   if (threadIdx.x != 0) return;
   int start = 0;
   TriCache tc;
@@ -730,14 +674,10 @@ __global__ void __launch_bounds__(1024) k_mu_nudge(TriDev d, int W, int64_t npx,
     // q + 1e-9 * (centroid - q), numpy's elementwise order
     const double x0 = dadd(u, dmul(1e-9, dsub(dd.cen0, u)));
     const double x1 = dadd(v, dmul(1e-9, dsub(dd.cen1, v)));
-    const bool hinted = total <= NUDGE_CAP;
-    const int s = find_simplex(d, w, -1, x0, x1, start, tc,
-                               hinted ? (int)w.final_s[p] : INT_MIN);
+    const int s = find_simplex(d, w, -1, x0, x1, start, tc);
     double m;
     if (s >= 0) {
       m = plane_at(d, s, u, v);
-    } else if (hinted) {
-      m = d.disp[w.res1[p]];  // cKDTree nearest vertex (first minimum), found above
     } else {
       // cKDTree nearest vertex of the original point (first minimum)
       double best = INFINITY;
