@@ -416,6 +416,15 @@ int st_median(const uint8_t* image, int32_t H, int32_t W, int32_t C, int32_t rad
 
 /* ---- one frame, one call (the host runtime of reconstruct_stream) ------- */
 
+/* Host gathers of the streaming runtime (one C call per frame; ctypes drops
+ * the GIL for it): dst + dst_off[i] <- srcs[i], sizes[i] bytes -- host to
+ * host (st_host_gather), host to device asynchronously on `stream`
+ * (st_h2d_gather). */
+int st_host_gather(void* dst, const void* const* srcs, const int64_t* dst_off,
+                   const int64_t* sizes, int32_t n);
+int st_h2d_gather(void* dst_dev, const void* const* srcs, const int64_t* dst_off,
+                  const int64_t* sizes, int32_t n, void* stream);
+
 /* Everything a frame pipeline keeps across frames: the persistent device
  * buffers, workspaces, streams and (after st_frame_plan_init) its events. */
 typedef struct st_frame_plan {

@@ -123,6 +123,10 @@ _SIGS = {
     "st_frame_run": (C.c_int, [C.POINTER(StFramePlan), C.POINTER(StTri), _P, _P, _I32, _P, _P,
                                _P]),
     "st_frame_host_bytes": (C.c_int64, [_I32, _I32]),
+    "st_host_gather": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_int64), _I32]),
+    "st_h2d_gather": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                                C.POINTER(C.c_int64), _I32, _P]),
     "st_tri_tables": (C.c_int, [C.POINTER(StTri), _P, _P, _P, _P]),
     "st_harvest": (C.c_int, [_P, _P, C.POINTER(StCams), _D, _I32, C.c_float, _I32, _D,
                              _P, _P, _P, _P, _P, _P, _P, _I64, _P]),
@@ -327,3 +331,12 @@ def make_params(sp, pp, forced_iters=0, timing=False):
     p.forced_iters = int(forced_iters or 0)
     p.timing = 1 if timing else 0
     return p
+
+
+def gather_args(arrays, offsets):
+    """ctypes (srcs, dst_off, sizes, n) for st_host_gather / st_h2d_gather."""
+    n = len(arrays)
+    srcs = (C.c_void_p * n)(*[a.ctypes.data for a in arrays])
+    offs = (C.c_int64 * n)(*offsets)
+    sizes = (C.c_int64 * n)(*[a.nbytes for a in arrays])
+    return srcs, offs, sizes, n

@@ -149,9 +149,12 @@ class TriDevice:
                 slot.tri_stage = torch.empty(max(total, 1 << 20) * 5 // 4, dtype=torch.uint8,
                                              pin_memory=True)
             stage = slot.tri_stage
-        host = stage.numpy()
-        for (_, a), o in zip(parts, offs):
-            np.copyto(host[o:o + a.nbytes].view(a.dtype).reshape(a.shape), a)
+        # one native gather into the pinned staging block (the GIL is released
+        # for it: a stream's other host thread keeps enqueueing meanwhile)
+        arrs = [np.ascontiguousarray(a) for _, a in parts]
+        srcs, goffs, sizes, n_parts = N.gather_args(arrs, offs)
+        N.check(N.lib().st_host_gather(N.C.c_void_p(stage.data_ptr()), srcs, goffs, sizes,
+                                       n_parts))
         if slot is None:
             self.buffer = torch.empty(max(dev_total, 1), dtype=torch.uint8, device=dev())
         else:

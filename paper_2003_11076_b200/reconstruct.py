@@ -123,9 +123,15 @@ class FramePipeline:
             elif isinstance(src, np.ndarray):
                 dst.copy_(t.from_numpy(np.ascontiguousarray(src, dtype=dt)), non_blocking=True)
             else:
-                for k, a in enumerate(src):
-                    dst[k].copy_(t.from_numpy(np.ascontiguousarray(a, dtype=dt)),
-                                 non_blocking=True)
+                # per-view host arrays: one native call for every view's copy
+                views = [np.ascontiguousarray(a, dtype=dt) for a in src]
+                per = dst[0].numel() * dst.element_size()
+                if len(views) != dst.shape[0] or any(v.nbytes != per for v in views):
+                    raise ValueError("frame views do not match the pipeline's shape")
+                srcs, offs, sizes, n = N.gather_args(views, [k * per for k in range(len(views))])
+                N.check(N.lib().st_h2d_gather(N.ptr(dst), srcs, offs, sizes, n,
+                                              N.stream_handle()))
+                self._hold = views  # (pageable sources: copied before the call returns)
 
     # -- the frame --------------------------------------------------------------------
 
