@@ -425,6 +425,13 @@ int st_host_gather(void* dst, const void* const* srcs, const int64_t* dst_off,
 int st_h2d_gather(void* dst_dev, const void* const* srcs, const int64_t* dst_off,
                   const int64_t* sizes, int32_t n, void* stream);
 
+/* L2 residency (experiments and the stream runtime): set aside `bytes` of L2
+ * for persisting lines (clamped to the device maximum; 0 releases it), and
+ * mark [base, base + bytes) persisting for the kernels of `stream`
+ * (hit_ratio of its lines; bytes = 0 clears the window). */
+int st_l2_set_aside(int64_t bytes);
+int st_stream_l2_window(void* stream, void* base, int64_t bytes, float hit_ratio);
+
 /* Everything a frame pipeline keeps across frames: the persistent device
  * buffers, workspaces, streams and (after st_frame_plan_init) its events. */
 typedef struct st_frame_plan {

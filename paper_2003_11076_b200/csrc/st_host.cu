@@ -41,3 +41,34 @@ int st_h2d_gather(void* dst_dev, const void* const* srcs, const int64_t* dst_off
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// L2 residency control (B200: 126 MB L2): reserve `bytes` of L2 for
+// persisting accesses (0 = release) -- device-wide, cudaLimitPersistingL2CacheSize.
+int st_l2_set_aside(int64_t bytes) {
+  int dev = 0;
+  ST_CUDA_CHECK(cudaGetDevice(&dev));
+  int max_persist = 0;
+  ST_CUDA_CHECK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  size_t b = (size_t)(bytes < 0 ? 0 : bytes);
+  if (b > (size_t)max_persist) b = (size_t)max_persist;
+  ST_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, b));
+  return ST_OK;
+}
+
+// Kernels launched on `stream` treat [base, base + bytes) as persisting in L2
+// (hit_ratio of its lines; the rest streaming); bytes = 0 clears the window.
+int st_stream_l2_window(void* stream, void* base, int64_t bytes, float hit_ratio) {
+  cudaStreamAttrValue attr = {};
+  attr.accessPolicyWindow.base_ptr = base;
+  attr.accessPolicyWindow.num_bytes = (size_t)(bytes < 0 ? 0 : bytes);
+  attr.accessPolicyWindow.hitRatio = hit_ratio;
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  ST_CUDA_CHECK(cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow,
+                                       &attr));
+  return ST_OK;
+}
+
+}  // extern "C"

@@ -649,7 +649,10 @@ class _PipePair(list):
     busy = False
 
 
-STREAM_SLOTS = 3  # frames in flight: H2D of i+1 never waits for the D2H of i-1
+# Frames in flight.  A frame's H2D may start once its slot's previous frame
+# has left (its D2H done); with too few slots that gate, not the link or the
+# kernels, sets the stream's period (3 slots: H2D + pre-solve chain per frame)
+STREAM_SLOTS = int(os.environ.get("ST_STREAM_SLOTS", "5"))
 
 
 def _rig_key(rig, w, h, params, prior_params):
