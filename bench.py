@@ -121,6 +121,16 @@ class ClockSampler:
                 return
 
     def __enter__(self):
+        # preferred: the library's native NVML thread (never takes the GIL
+        # from the thread that enqueues the frames)
+        try:
+            from paper_2003_11076_b200 import _native as N
+            if N.lib().st_clocks_start(2000) == 0:
+                self.native = N
+                return self
+        except Exception:  # noqa: BLE001
+            pass
+        self.native = None
         try:
             import pynvml as nv
             nv.nvmlInit()
@@ -155,6 +165,16 @@ class ClockSampler:
                 continue
 
     def __exit__(self, *exc):
+        if getattr(self, "native", None) is not None:
+            cap = 65536
+            sm = np.zeros(cap, np.uint32)
+            mx = np.zeros(cap, np.uint32)
+            rs = np.zeros(cap, np.uint64)
+            n = int(self.native.lib().st_clocks_stop(sm.ctypes.data, mx.ctypes.data,
+                                                     rs.ctypes.data, cap))
+            for i in range(max(0, min(n, cap))):
+                self.samples.append((float(sm[i]), float(mx[i]), int(rs[i])))
+            return False
         if self.nvml is not None:
             self.stop.set()
             self.thread.join(timeout=2)
@@ -179,7 +199,9 @@ class ClockSampler:
             bits |= x[2]
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.samples[-1][1],
                 "reasons": sorted(n for n, b in self.REASONS if bits & b),
-                "samples": len(sm), "source": "nvml" if self.nvml else "nvidia-smi"}
+                "samples": len(sm),
+                "source": ("nvml (native sampler thread)" if getattr(self, "native", None)
+                           else "nvml" if self.nvml else "nvidia-smi")}
 
 
 # -- CPU oracle sample ------------------------------------------------------------------

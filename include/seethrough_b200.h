@@ -430,6 +430,12 @@ int st_h2d_gather(void* dst_dev, const void* const* srcs, const int64_t* dst_off
  * mark [base, base + bytes) persisting for the kernels of `stream`
  * (hit_ratio of its lines; bytes = 0 clears the window). */
 int st_l2_set_aside(int64_t bytes);
+/* Benchmark clock sampler: a native thread polls NVML every interval_us for
+ * the SM clock and the clock-event (throttle) reason bits of the current
+ * device; st_clocks_stop joins it and copies up to cap samples, returning
+ * their number (< 0: not running). */
+int st_clocks_start(int32_t interval_us);
+int64_t st_clocks_stop(uint32_t* sm_mhz, uint32_t* max_mhz, uint64_t* reason_bits, int64_t cap);
 int st_stream_l2_window(void* stream, void* base, int64_t bytes, float hit_ratio);
 
 /* Everything a frame pipeline keeps across frames: the persistent device

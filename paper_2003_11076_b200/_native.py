@@ -124,6 +124,8 @@ _SIGS = {
                                _P]),
     "st_frame_host_bytes": (C.c_int64, [_I32, _I32]),
     "st_l2_set_aside": (C.c_int, [_I64]),
+    "st_clocks_start": (C.c_int, [_I32]),
+    "st_clocks_stop": (C.c_int64, [_P, _P, _P, _I64]),
     "st_stream_l2_window": (C.c_int, [_P, _P, _I64, C.c_float]),
     "st_host_gather": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
                                  C.POINTER(C.c_int64), _I32]),

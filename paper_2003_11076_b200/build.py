@@ -63,7 +63,8 @@ def build(force=False, verbose=False, jobs=None, defines=(), out=None):
         if pr.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{logs[-1]}")
     tmp = lib + ".tmp"
-    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static"]
+    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static", "-ldl",
+                                                          "-Xcompiler", "-pthread"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout.decode(errors="replace"))

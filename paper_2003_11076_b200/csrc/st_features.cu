@@ -3,9 +3,11 @@
 // One CTA owns a 32x8 output tile of one view: it stages the edge-replicated
 // gray tile (+3 px halo) and the biased Sobel tile (+2 px halo) in shared
 // memory, then every thread writes its descriptor as a single 16-byte store.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "st_common.cuh"
 
@@ -119,15 +121,23 @@ __global__ void __launch_bounds__(DT_W* DT_H) k_descriptors(const uint8_t* __res
 // descriptors, a warp 32 consecutive ones per store.
 #define DW_W 128
 #define DW_H 16
-#define DW_ROWB 416  // >= 3 * (DW_W + 6) + 6 bytes of one staged row
+#define DW_ROWB 432  // >= 3 * (DW_W + 6) + 15 bytes of one staged row (TMA: 16-byte start)
+
+// TMA helpers (cp.async.bulk.tensor + an mbarrier carrying the byte count).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 
 __global__ void __launch_bounds__(256) k_descriptors_wide(const uint8_t* __restrict__ images,
                                                           int H, int W, size_t total_bytes,
                                                           uint4* __restrict__ desc,
                                                           uint8_t* __restrict__ gray_out,
                                                           uint8_t* __restrict__ sobel_out,
-                                                          int row0, int row1) {
-  __shared__ __align__(16) uint8_t raw[DW_H + 6][DW_ROWB];
+                                                          int row0, int row1,
+                                                          const __grid_constant__ CUtensorMap tmap,
+                                                          int use_tma) {
+  __shared__ __align__(128) uint8_t raw[DW_H + 6][DW_ROWB];
+  __shared__ __align__(8) uint64_t bar;
   __shared__ int16_t g[DW_H + 6][DW_W + 6];
   __shared__ uint16_t sxy[DW_H + 4][DW_W + 4];  // gx | gy << 8; 0x8080 off-image
   __shared__ int roff[DW_H + 6];  // byte of pixel 0 of the row, relative to the staged start
@@ -138,9 +148,43 @@ __global__ void __launch_bounds__(256) k_descriptors_wide(const uint8_t* __restr
   const int tid = threadIdx.x;
   const int cl0 = max(x0 - 3, 0), cl1 = min(x0 + DW_W + 3, W);  // clamped column range
   const uintptr_t buf0 = (uintptr_t)images, buf1 = buf0 + total_bytes;
+  // Interior tiles (no edge replication needed): the whole (DW_H + 6) x
+  // DW_ROWB staging box in one TMA load -- the view as a 3-D tensor of 32-bit
+  // words (W*3/4, H, K), box (DW_ROWB/4, DW_H + 6, 1) from the 16-byte
+  // boundary at or below pixel x0 - 3 (roff carries the offset, as for the
+  // word loop below).  Edge tiles replicate the border and take the loop.
+  const bool tma_tile = use_tma && x0 >= 3 && x0 + DW_W + 3 <= W && y0 >= 3 &&
+                        y0 + DW_H + 3 <= H;
+  if (tma_tile) {
+    const int xb = 3 * (x0 - 3);  // first byte of the staged run
+    const int xw = (xb >> 4) << 2;  // the box starts on a 16-byte boundary (a TMA rule)
+    if (tid < DW_H + 6) roff[tid] = (xb - 4 * xw) - 3 * cl0;
+    const uint32_t b = smem_u32(&bar);
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(1) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+                   "r"((DW_H + 6) * DW_ROWB)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+          "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(&raw[0][0])),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(xw), "r"(y0 - 3), "r"(k), "r"(b)
+          : "memory");
+    }
+    __syncthreads();  // (the barrier is initialised before anyone waits on it)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(b)
+        : "memory");
+  }
   // stage rows: 32-bit words covering bytes [3 cl0, 3 cl1) of each clamped row
   const int words_per_row = (3 * (cl1 - cl0) + 6) / 4 + 1;
-  for (int i = tid; i < (DW_H + 6) * words_per_row; i += blockDim.x) {
+  for (int i = tid; !tma_tile && i < (DW_H + 6) * words_per_row; i += blockDim.x) {
     const int r = i / words_per_row, j = i % words_per_row;
     const int yy = min(max(y0 - 3 + r, 0), H - 1);
     const uintptr_t a0 = buf0 + view + ((size_t)yy * W + cl0) * 3;
@@ -201,6 +245,51 @@ __global__ void __launch_bounds__(256) k_descriptors_wide(const uint8_t* __restr
 
 }  // namespace st
 
+namespace {
+
+// The views (K, H, W, 3) u8 as a 3-D tensor of 32-bit words for the TMA
+// staging of k_descriptors_wide: (W*3/4, H, K), box (DW_ROWB/4, DW_H + 6, 1).
+// 0 (no TMA; the kernel's word loop stages everything) when the layout does
+// not allow it: row pitch W*3 not a multiple of 16 bytes, a misaligned base,
+// frames smaller than the box, or ST_DESC_NO_TMA set.
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+  static EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+int desc_tensor_map(const uint8_t* images, int K, int H, int W, CUtensorMap* map) {
+  static const bool off = getenv("ST_DESC_NO_TMA") != nullptr;
+  memset(map, 0, sizeof(*map));
+  if (off || (W % 16) != 0 || ((uintptr_t)images & 15) != 0 || W * 3 / 4 < DW_ROWB / 4 ||
+      H < DW_H + 6)
+    return 0;
+  EncodeTiled enc = encode_fn();
+  if (!enc) return 0;
+  const cuuint64_t dims[3] = {(cuuint64_t)W * 3 / 4, (cuuint64_t)H, (cuuint64_t)K};
+  const cuuint64_t strides[2] = {(cuuint64_t)W * 3, (cuuint64_t)W * 3 * H};
+  const cuuint32_t box[3] = {DW_ROWB / 4, DW_H + 6, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, (void*)images, dims, strides,
+                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
+
+}  // namespace
+
 extern "C" int st_descriptors(const uint8_t* images, int32_t K, int32_t H, int32_t W,
                               int32_t channels, uint8_t* desc_out, uint8_t* gray_out,
                               uint8_t* sobel_out, void* stream) {
@@ -214,9 +303,11 @@ extern "C" int st_descriptors(const uint8_t* images, int32_t K, int32_t H, int32
   }
   if (channels == 3 && ((uintptr_t)images & 3) == 0 && getenv("ST_DESC_NARROW") == nullptr) {
     dim3 grid((W + DW_W - 1) / DW_W, (H + DW_H - 1) / DW_H, K);
+    CUtensorMap tmap;
+    const int tma = desc_tensor_map(images, K, H, W, &tmap);
     st::k_descriptors_wide<<<grid, 256, 0, (cudaStream_t)stream>>>(
         images, H, W, (size_t)K * H * W * 3, reinterpret_cast<uint4*>(desc_out), gray_out,
-        sobel_out, 0, H);
+        sobel_out, 0, H, tmap, tma);
     ST_LAUNCH_CHECK("k_descriptors_wide");
     return ST_OK;
   }
@@ -243,9 +334,11 @@ extern "C" int st_descriptors_rows(const uint8_t* images, int32_t K, int32_t H, 
   }
   if (row0 == row1) return ST_OK;
   dim3 grid((W + DW_W - 1) / DW_W, (row1 - row0 + DW_H - 1) / DW_H, K);
+  CUtensorMap tmap;
+  const int tma = desc_tensor_map(images, K, H, W, &tmap);
   st::k_descriptors_wide<<<grid, 256, 0, (cudaStream_t)stream>>>(
       images, H, W, (size_t)K * H * W * 3, reinterpret_cast<uint4*>(desc_out), nullptr, nullptr,
-      row0, row1);
+      row0, row1, tmap, tma);
   ST_LAUNCH_CHECK("k_descriptors_wide");
   return ST_OK;
 }
