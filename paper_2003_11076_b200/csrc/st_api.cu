@@ -229,7 +229,11 @@ void launch_e_step(int K, int64_t n, cudaStream_t s, const st::EmCtx& c,
     case 4: launch_taps<4>(bt, s, c, a); break;
     case 5: launch_taps<5>(bt, s, c, a); break;
     default:
-      st::k_e_step_at<<<blocks_for(n, ESTEP_BLOCK), ESTEP_BLOCK, estep_smem(K), s>>>(c, a);
+      // (ST_ESTEP_SMEM: the shared-memory ray staging, for cross-checks)
+      if (c.rectified && !a.exhaustive && getenv("ST_ESTEP_SMEM") == nullptr)
+        st::k_e_step_at_taps<<<blocks_for(n, ESTEP_BLOCK), ESTEP_BLOCK, 0, s>>>(c, a);
+      else
+        st::k_e_step_at<<<blocks_for(n, ESTEP_BLOCK), ESTEP_BLOCK, estep_smem(K), s>>>(c, a);
       break;
   }
 }

@@ -1042,8 +1042,9 @@ __device__ double score_generic(uint32_t m, int K, const double* __restrict__ f,
   return dsub(dadd(a, b), dmul(p.beta, vr));
 }
 
-__device__ uint32_t estep_bnb(int K, const double* __restrict__ f, int stride, const double* l1,
-                              const double* l0, uint32_t vbits, const st_params& p) {
+template <typename Score>
+__device__ uint32_t estep_bnb_core(int K, const double* l1, const double* l0, uint32_t vbits,
+                                   const st_params& p, Score score) {
   constexpr double QS = 1048576.0;  // 2^20
   long long dq[ST_MAX_VIEWS];
   long long base = 0;
@@ -1077,11 +1078,11 @@ __device__ uint32_t estep_bnb(int K, const double* __restrict__ f, int stride, c
       mtop = m;
     }
   }
-  double best = score_generic(mtop, K, f, stride, l1, l0, p);
+  double best = score(mtop);
   int bpop = __popc(mtop);
   uint32_t bm = mtop;
   auto consider = [&](uint32_t mm) {
-    const double sc = score_generic(mm, K, f, stride, l1, l0, p);
+    const double sc = score(mm);
     const int pop = __popc(mm);
     if (prefer(sc, pop, mm, best, bpop, bm)) {
       best = sc;
@@ -1133,6 +1134,13 @@ __device__ uint32_t estep_bnb(int K, const double* __restrict__ f, int stride, c
     m = (m - vbits) & vbits;
   } while (m != 0);
   return bm;
+}
+
+__device__ uint32_t estep_bnb(int K, const double* __restrict__ f, int stride, const double* l1,
+                              const double* l0, uint32_t vbits, const st_params& p) {
+  return estep_bnb_core(K, l1, l0, vbits, p, [&](uint32_t m) {
+    return score_generic(m, K, f, stride, l1, l0, p);
+  });
 }
 
 // Loader over rays staged in shared memory: element (k, ch) of thread t at
@@ -1674,6 +1682,99 @@ __global__ void __launch_bounds__(ESTEP_BLOCK) k_e_step_at(EmCtx c, EStepArgs a)
   }
   const uint32_t m = a.exhaustive ? estep_generic(K, f, stride, l1, l0, vb, c.p)
                                   : estep_bnb(K, f, stride, l1, l0, vb, c.p);
+  const int64_t o = a.scatter ? pix : i;
+  a.static_out[o] = m;
+  a.valid_out[o] = vb;
+  }
+}
+
+// The K >= 6 fallback on rectified rigs without the shared-memory ray
+// staging: each ray keeps only its tap (descriptor index, horizontal
+// weight) in shared memory (12 B instead of 128 B of fp64 samples), and a
+// mask's exact score re-samples its rays' descriptors (L1/L2 hits) with the
+// arithmetic of gather_rays + score_generic: channels 0-7 then 8-15 (two
+// passes of 8 accumulators), each channel's sums over the mask's views in
+// view order, the 16 channel terms added in channel order.  Same outputs as
+// k_e_step_at with ~10x less shared memory per pixel (occupancy).
+#ifndef ESTEP_AT_TAPS_MIN_BLOCKS
+#define ESTEP_AT_TAPS_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(ESTEP_BLOCK, ESTEP_AT_TAPS_MIN_BLOCKS)
+    k_e_step_at_taps(EmCtx c, EStepArgs a) {
+  __shared__ uint32_t s_off[ST_MAX_VIEWS * ESTEP_BLOCK];
+  __shared__ double s_fu[ST_MAX_VIEWS * ESTEP_BLOCK];
+  if (a.stop && *a.stop) return;  // converged (st_solve_async)
+  const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
+  const int K = c.rig.num_views;
+  uint32_t* toff = s_off + threadIdx.x;
+  double* tfu = s_fu + threadIdx.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_work;
+       t += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t i = a.list ? (int64_t)a.list[t] : t;
+  if (a.status && a.status[i] == ST_STATUS_LOW_TEXTURE) continue;  // solver.py:476-478
+  const int64_t pix = a.pix ? a.pix[i] : c.pix0 + i;
+  const int x = (int)(pix % c.W), y = (int)(pix / c.W);
+  const double u = (double)x, v = (double)y;
+  const double d = a.d[i];
+  const uint32_t row = (uint32_t)y * (uint32_t)c.W;
+  double l1[ST_MAX_VIEWS], l0[ST_MAX_VIEWS];
+  uint32_t vb = 0;
+  // gather_rays (solver.py:206-227): taps of the valid rays, priors at them
+  for (int k = 0; k < K; ++k) {
+    const WarpOut w = warp_ctx(c, k, u, v, d);
+    double q = 0.5;
+    if (in_margin(c.rig, k, w)) {
+      const Taps tp = taps_ctx(c, w);
+      toff[k * ESTEP_BLOCK] = (uint32_t)k * (uint32_t)c.HW + row + (uint32_t)tp.iu;
+      tfu[k * ESTEP_BLOCK] = tp.fu;
+      q = sample_prior(c.priors + (size_t)k * c.HW, c.W, tp);
+      vb |= 1u << k;
+    }
+    clamp_logs(q, c.p.epsilon_prior, a.eps_logs, l1[k], l0[k]);
+  }
+  auto score = [&](uint32_t m) -> double {
+    const int pop = __popc(m);
+    double vr;
+    if (pop < c.p.min_static_rays) {
+      vr = variance_ceiling();
+    } else {
+      double acc = 0.0;
+#pragma unroll 1
+      for (int ps = 0; ps < 2; ++ps) {
+        double a1[8], a2[8];
+        int n = 0;
+        for (uint32_t r = m; r; r &= r - 1) {
+          const int k = __ffs(r) - 1;
+          const uint4* pl = c.desc + toff[k * ESTEP_BLOCK];
+          const uint4 ta = __ldg(pl), tb = __ldg(pl + 1);
+          const double fu = tfu[k * ESTEP_BLOCK];
+          double xv[8];
+          lerp_word(ps ? ta.z : ta.x, ps ? tb.z : tb.x, fu, *reinterpret_cast<double(*)[4]>(xv));
+          lerp_word(ps ? ta.w : ta.y, ps ? tb.w : tb.y, fu,
+                    *reinterpret_cast<double(*)[4]>(xv + 4));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const double x2 = dmul(xv[j], xv[j]);
+            a1[j] = n ? dadd(a1[j], xv[j]) : xv[j];
+            a2[j] = n ? dadd(a2[j], x2) : x2;
+          }
+          ++n;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = dadd(acc, dsub(a2[j], div_n(dmul(a1[j], a1[j]), n)));
+      }
+      vr = fmax(div_n(acc, pop), 0.0);
+    }
+    double sa = 0.0, sb = 0.0;
+    for (int k = 0; k < K; ++k) {
+      if ((m >> k) & 1)
+        sa = dadd(sa, l1[k]);
+      else
+        sb = dadd(sb, l0[k]);
+    }
+    return dsub(dadd(sa, sb), dmul(c.p.beta, vr));
+  };
+  const uint32_t m = estep_bnb_core(K, l1, l0, vb, c.p, score);
   const int64_t o = a.scatter ? pix : i;
   a.static_out[o] = m;
   a.valid_out[o] = vb;

@@ -153,6 +153,8 @@ __global__ void k_em_stats(int64_t n, int with_prev, const double* e, const doub
 template <int KT, bool RECT>
 __global__ void k_e_step_taps(EmCtx c, EStepArgs a);
 __global__ void k_e_step_at(EmCtx c, EStepArgs a);
+// K >= 6 on rectified rigs: taps in shared memory, samples re-read per scored mask
+__global__ void k_e_step_at_taps(EmCtx c, EStepArgs a);
 template <int KT, bool RECT>
 __global__ void k_e_step_cert(EmCtx c, EStepArgs a);
 template <bool RECT>

@@ -376,6 +376,21 @@ def test_k9_certificate_and_bnb_equal_exhaustive(st, monkeypatch, name):
         assert list(a.stats.mean_energy) == list(b.stats.mean_energy)
 
 
+def test_k9_tap_fallback_equals_staged_fallback(st, monkeypatch):
+    """K >= 6 on a rectified rig: the E-step fallback that keeps only taps in
+    shared memory (k_e_step_at_taps) decides exactly what the fp64-staged
+    one (k_e_step_at) decides, over 5 forced iterations."""
+    g = load("occ128_k9")
+    sp, pp = _params(st, g)
+    a = st.reconstruct(_frame(st, g), _Rig(g), _Tri(g), sp, pp, forced_iters=5)
+    monkeypatch.setenv("ST_ESTEP_SMEM", "1")
+    b = st.reconstruct(_frame(st, g), _Rig(g), _Tri(g), sp, pp, forced_iters=5)
+    assert np.array_equal(a.segmentation.static_bits, b.segmentation.static_bits)
+    assert np.array_equal(a.segmentation.valid_bits, b.segmentation.valid_bits)
+    assert np.array_equal(a.disparity.values, b.disparity.values)
+    assert list(a.stats.mean_energy) == list(b.stats.mean_energy)
+
+
 @pytest.mark.parametrize("n", [0, 1, 7, 8, 127, 128, 129, 1000, 4097, 19200, 307200, 921600])
 def test_device_mean_is_numpys_mean(st, n):
     """st_numpy_mean (the EM statistics' reduction, st_mean.cu) equals
