@@ -110,6 +110,12 @@ int64_t st_struct_size(int32_t which);
  * threads; CUB's internal launches inside st_support_build / st_solve count
  * as one per CUB call). */
 int64_t st_launch_count(void);
+/* The EM tail loop (iterations >= 3 of a one-device solve run as a CUDA
+ * graph WHILE loop, cached per argument set; the environment variable
+ * ST_NO_GRAPH selects the plain launch loop): which = 0 graphs built,
+ * 1 graph launches, cumulative.  A graph launch counts its body's kernels
+ * once in st_launch_count. */
+int64_t st_tail_graph_count(int32_t which);
 /* Diagnostics: which = 1 checks the kernels' exact small-integer division
  * (div_small) against __ddiv_rn on n random doubles x 12 divisors and
  * returns the number of bit mismatches (expected 0). */

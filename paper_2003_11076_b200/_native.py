@@ -100,6 +100,7 @@ _SIGS = {
     "st_version": (C.c_int, []),
     "st_device_count": (C.c_int, []),
     "st_launch_count": (C.c_int64, []),
+    "st_tail_graph_count": (C.c_int64, [C.c_int32]),
     "st_struct_size": (C.c_int64, [_I32]),
     "st_fp64_peak": (C.c_int, [C.POINTER(C.c_double), _P]),
     "st_selftest": (C.c_int, [_I32, _I64, C.c_uint64, C.POINTER(C.c_int64), _P]),

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <functional>
 #include <mutex>
 #include <cub/cub.cuh>
 #include <vector>
@@ -818,6 +819,131 @@ int st_solve(const st_frame* f, const st_rig* rig, const st_params* p, int32_t d
   return ST_OK;
 }
 
+namespace {
+
+// Iterations >= 3 as a CUDA graph: a WHILE conditional node whose body is
+// one iteration's launches, captured once per argument set (TailGraphKey)
+// and cached.  The statistics kernel keeps the iteration count on the device
+// (counts[14]) and sets the loop condition.
+struct TailGraphFields {
+  cudaGraphConditionalHandle cond;
+};
+
+struct TailGraphKey {
+  st::EmCtx c;
+  const int64_t* active;
+  int64_t n, cnt_lo, cnt_hi;
+  const uint32_t* static_bits;
+  const uint32_t* valid_bits;
+  const st_stats* stats;
+  const char* ws;
+  const int32_t* mu_unsafe;
+  int band, forced_iters, iters, wave_env, device;
+};
+
+struct TailGraph {
+  TailGraphKey key;
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  long long launches;  // kernels per body run
+  unsigned long long used;
+};
+
+constexpr size_t TAIL_GRAPH_CAP = 32;
+std::mutex g_tail_mu;
+std::vector<TailGraph>* g_tail = new std::vector<TailGraph>();  // (never freed: exit order)
+unsigned long long g_tail_tick = 0;
+std::atomic<long long> g_tail_builds{0};
+std::atomic<long long> g_tail_launches{0};
+
+// ST_NO_GRAPH: the plain launch loop.  The E-step's diagnostic / cross-check
+// switches (launch_e_step) are read per launch, so they disable the graph.
+bool tail_graphs_enabled() {
+  return !getenv("ST_NO_GRAPH") && !getenv("ST_ESTEP_STATS") && !getenv("ST_ESTEP_EXHAUSTIVE") &&
+         !getenv("ST_ESTEP_SMEM");
+}
+
+void destroy_tail_graph(TailGraph& t) {
+  if (t.exec) cudaGraphExecDestroy(t.exec);  // (freed once in-flight launches finish)
+  if (t.graph) cudaGraphDestroy(t.graph);
+  t.exec = nullptr;
+  t.graph = nullptr;
+}
+
+int build_tail_graph(TailGraph& t, const std::function<int(const TailGraphFields*, cudaStream_t)>& body_fn) {
+  TailGraphFields fields;
+  ST_CUDA_CHECK(cudaGraphCreate(&t.graph, 0));
+  ST_CUDA_CHECK(cudaGraphConditionalHandleCreate(&fields.cond, t.graph, 1u,
+                                                 cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = fields.cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  ST_CUDA_CHECK(cudaGraphAddNode(&node, t.graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaStream_t cs;
+  ST_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaError_t e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                                cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return sthost::cuda_fail(e, "cudaStreamBeginCaptureToGraph");
+  }
+  const long long l0 = sthost::g_launches.load();
+  const int rc = body_fn(&fields, cs);
+  t.launches = sthost::g_launches.load() - l0;
+  sthost::g_launches.fetch_sub(t.launches);  // (counted per graph launch instead)
+  cudaGraph_t captured = nullptr;
+  e = cudaStreamEndCapture(cs, &captured);
+  cudaStreamDestroy(cs);
+  if (rc) return rc;
+  if (e != cudaSuccess) return sthost::cuda_fail(e, "cudaStreamEndCapture");
+  ST_CUDA_CHECK(cudaGraphInstantiate(&t.exec, t.graph, 0));
+  g_tail_builds.fetch_add(1);
+  return ST_OK;
+}
+
+int run_tail_graph(cudaStream_t s, TailGraphKey key,
+                   const std::function<int(const TailGraphFields*, cudaStream_t)>& body_fn) {
+  ST_CUDA_CHECK(cudaGetDevice(&key.device));
+  std::lock_guard<std::mutex> lock(g_tail_mu);
+  std::vector<TailGraph>& cache = *g_tail;
+  TailGraph* hit = nullptr;
+  for (TailGraph& t : cache)
+    if (memcmp(&t.key, &key, sizeof(key)) == 0) hit = &t;
+  if (!hit) {
+    if (cache.size() >= TAIL_GRAPH_CAP) {  // least recently used out
+      auto lru = std::min_element(cache.begin(), cache.end(),
+                                  [](const TailGraph& a, const TailGraph& b) { return a.used < b.used; });
+      destroy_tail_graph(*lru);
+      cache.erase(lru);
+    }
+    TailGraph t;
+    memset(&t, 0, sizeof(t));
+    t.key = key;
+    const int rc = build_tail_graph(t, body_fn);
+    if (rc) {
+      destroy_tail_graph(t);
+      return rc;
+    }
+    cache.push_back(t);
+    hit = &cache.back();
+  }
+  hit->used = ++g_tail_tick;
+  ST_CUDA_CHECK(cudaGraphLaunch(hit->exec, s));
+  sthost::g_launches.fetch_add(hit->launches);
+  g_tail_launches.fetch_add(1);
+  return ST_OK;
+}
+
+}  // namespace
+
+int64_t st_tail_graph_count(int32_t which) {
+  return which == 0 ? g_tail_builds.load() : which == 1 ? g_tail_launches.load() : -1;
+}
+
 // The asynchronous EM driver behind st_solve_async and st_solve_rows.
 // Slots: i -> pixel pix0 + i (dense) or active[i] (a sorted list); slots
 // [cnt_lo, cnt_hi) are this shard's own pixels (the statistics count only
@@ -890,23 +1016,29 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
   const int wave2 = std::min(nblk, 148 * wave_env);
   const int mblk = (int)mstep_blocks(c, n);
   const int mwave2 = std::min(mblk, 148 * wave_env);
-  // a row band with no active pixel still takes part in every exchange
-  for (int it = 1; it <= iters && (n > 0 || A.band); ++it) {
-    // long caps (max_iters > ST_ASYNC_CHUNK) and row bands: read the device
-    // stop flag back before enqueueing more iterations, so a converged solve
-    // does not enqueue max_iters rounds of (immediately exiting) launches and
-    // exchanges (row bands check every iteration)
-    const int chunk = A.band && A.exchange ? 1 : ST_ASYNC_CHUNK;
-    if (it > chunk && (it - 1) % chunk == 0) {
-      int h_stop = 0;
-      ST_CUDA_CHECK(cudaMemcpyAsync(&h_stop, stop, sizeof(int), cudaMemcpyDeviceToHost, s));
-      ST_CUDA_CHECK(cudaStreamSynchronize(s));
-      if (h_stop == 2) {
-        sthost::set_error("row band: whole-frame surface raster needed");
-        return ST_EAGAIN;
-      }
-      if (h_stop) break;
-    }
+  uint32_t* it_off = counts + 14;  // (zeroed above with counts + 12 .. + 15)
+  // everything the captured launches depend on: the cache key of the graph
+  TailGraphKey graph_key;
+  memset(&graph_key, 0, sizeof(graph_key));
+  graph_key.c = c;
+  graph_key.active = A.active;
+  graph_key.n = n;
+  graph_key.cnt_lo = A.cnt_lo;
+  graph_key.cnt_hi = A.cnt_hi;
+  graph_key.static_bits = static_bits;
+  graph_key.valid_bits = valid_bits;
+  graph_key.stats = stats_dev;
+  graph_key.ws = ws;
+  graph_key.mu_unsafe = f->mu_unsafe;
+  graph_key.band = A.band ? 1 : 0;
+  graph_key.forced_iters = p->forced_iters;
+  graph_key.iters = iters;
+  graph_key.wave_env = wave_env;
+  // One EM iteration's launches (M-step worklist, M-step, E-step, statistics
+  // + control).  Every iteration >= 3 enqueues the same launches with the
+  // same arguments; `g` (nullable) turns on the graph loop's fields of the
+  // statistics kernel (the iteration counter and the WHILE condition).
+  auto iteration = [&](int it, const TailGraphFields* g, cudaStream_t s) -> int {
     // iteration 2 re-solves the pixels whose mask changed at iteration 1
     // (~20 %); later iterations have far smaller worklists, or none once
     // converged (the launches then exit at once): a smaller grid
@@ -917,7 +1049,8 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
                                                  e_act, pe_act, chg, mlist, counts, stop);
       ST_LAUNCH_CHECK("k_flag_mstep");
     }
-    st::MStepArgs a = {};
+    st::MStepArgs a;
+    memset(&a, 0, sizeof(a));
     a.active = A.active;
     a.n = n;
     a.list = it > 1 ? mlist : nullptr;
@@ -937,7 +1070,8 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     const int mgrid = it == 1 ? mblk : it == 2 ? mwave2 : std::min(mblk, 148 * 4);
     launch_m_step(c, a, mgrid, s);
     ST_LAUNCH_CHECK("k_m_step");
-    st::EStepArgs e = {};
+    st::EStepArgs e;
+    memset(&e, 0, sizeof(e));
     e.pix = A.active;
     e.n = n;
     e.list = elist;
@@ -958,7 +1092,8 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     }  // n > 0
     // statistics, their fixed-order reduction and the control in one launch
     // (the last block folds the partials; it also clears the fallback count)
-    st::StatsTail tail = {};
+    st::StatsTail tail;
+    memset(&tail, 0, sizeof(tail));
     tail.on = 1;
     tail.it = it;
     tail.done = counts + 13;
@@ -976,6 +1111,12 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     tail.pw_scratch = (double*)(ws + L.pw_scratch);
     tail.pw_val = (double*)(ws + L.pw_val);
     tail.mu_unsafe = A.band ? f->mu_unsafe : nullptr;
+    if (g) {
+      tail.it_off = it_off;
+      tail.use_cond = 1;
+      tail.iters = iters;
+      tail.cond = g->cond;
+    }
     st::k_em_stats<<<sblk, STATS_BLOCK, 0, s>>>(
         n_cnt, it > 1, e_act + A.cnt_lo, pe_act + A.cnt_lo, chg + A.cnt_lo, work,
         (n > 0 ? (it == 1 ? mblk : it == 2 ? mwave2 : std::min(mblk, 148 * 4)) : 0) *
@@ -993,10 +1134,52 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
         }
         recs = (const st::Partial*)A.rec_recv;
       }
+      st::BandLoop loop;
+      memset(&loop, 0, sizeof(loop));
+      if (g) {
+        loop.it_off = it_off;
+        loop.use_cond = 1;
+        loop.iters = iters;
+        loop.cond = g->cond;
+      }
       st::k_band_control<<<1, 32, 0, s>>>(it, recs, A.exchange ? A.world : 1, p->forced_iters,
-                                          stats_dev, stop);
+                                          stats_dev, stop, loop);
       ST_LAUNCH_CHECK("k_band_control");
     }
+    return ST_OK;
+  };
+  // Iterations >= 3 of a one-device solve run as a CUDA-graph WHILE loop
+  // (the statistics kernel sets its condition): the frame's converged
+  // iterations cost no launches and no host round trip, whatever the cap.
+  // (row bands exchanging records through the host callback keep the loop)
+  bool use_graph = !A.exchange && n > 0 && iters >= 3 && tail_graphs_enabled();
+  // a row band with no active pixel still takes part in every exchange
+  for (int it = 1; it <= iters && (n > 0 || A.band); ++it) {
+    if (use_graph && it == 3) {
+      const int rc = run_tail_graph(
+          s, graph_key,
+          [&](const TailGraphFields* g, cudaStream_t cs) { return iteration(3, g, cs); });
+      if (rc == ST_OK) break;
+      use_graph = false;  // (could not build the graph: the launch loop below)
+      sthost::set_error("");
+    }
+    // long caps (max_iters > ST_ASYNC_CHUNK) and row bands: read the device
+    // stop flag back before enqueueing more iterations, so a converged solve
+    // does not enqueue max_iters rounds of (immediately exiting) launches and
+    // exchanges (row bands check every iteration)
+    const int chunk = A.band && A.exchange ? 1 : ST_ASYNC_CHUNK;
+    if (it > chunk && (it - 1) % chunk == 0) {
+      int h_stop = 0;
+      ST_CUDA_CHECK(cudaMemcpyAsync(&h_stop, stop, sizeof(int), cudaMemcpyDeviceToHost, s));
+      ST_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (h_stop == 2) {
+        sthost::set_error("row band: whole-frame surface raster needed");
+        return ST_EAGAIN;
+      }
+      if (h_stop) break;
+    }
+    const int rc = iteration(it, nullptr, s);
+    if (rc) return rc;
   }
   if (A.band && A.exchange) {  // (max_iters == 1: the loop read no stop flag)
     int h_stop = 0;

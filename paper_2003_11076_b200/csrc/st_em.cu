@@ -550,7 +550,12 @@ __global__ void __launch_bounds__(STATS_BLOCK) k_em_stats(
     int64_t n, int with_prev, const double* __restrict__ e, const double* __restrict__ pe,
     const uint8_t* __restrict__ chg, const Partial* __restrict__ work, int n_work_parts,
     Partial* __restrict__ parts, const int* stop, StatsTail tail) {
-  if (stop && *stop) return;
+  if (stop && *stop) {
+    // (in the graph loop every body run must set the condition, else the
+    // WHILE node would keep its last value)
+    if (tail.use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(tail.cond, 0u);
+    return;
+  }
   __shared__ double val[(1 << PW_MAX_LEVELS) - 1];
   const int D = tail.pw_depth;
   int64_t s0, nn;
@@ -667,12 +672,13 @@ __global__ void __launch_bounds__(STATS_BLOCK) k_em_stats(
   r.n_hopeless = tot7[5];
   r.n_samples = tot7[6];
   *tail.done = 0u;
+  const int it = tail.it + (tail.it_off ? (int)*tail.it_off : 0);
   if (tail.record_only) {
     r.n_act = tail.record_n_act;
-    r.n_mwork = tail.it > 1 ? (long long)tail.counts[0] : tail.record_slots;
+    r.n_mwork = it > 1 ? (long long)tail.counts[0] : tail.record_slots;
     r.n_ework = (long long)tail.counts[1];
     r.n_unsafe = tail.mu_unsafe ? (long long)(*tail.mu_unsafe != 0) : 0;
-    tail.reduced[tail.it] = r;
+    tail.reduced[it] = r;
     if (!tail.keep_counts) {
       tail.counts[0] = 0;  // next iteration's worklists
       tail.counts[1] = 0;
@@ -680,11 +686,14 @@ __global__ void __launch_bounds__(STATS_BLOCK) k_em_stats(
     if (tail.flist_count) *tail.flist_count = 0u;
     return;
   }
-  tail.reduced[tail.it] = r;
+  tail.reduced[it] = r;
   __threadfence();
-  solve_control(tail.it, tail.reduced, tail.counts, tail.n_act, tail.forced_iters, tail.stats,
+  solve_control(it, tail.reduced, tail.counts, tail.n_act, tail.forced_iters, tail.stats,
                 tail.stop_rw);
   if (tail.flist_count) *tail.flist_count = 0u;
+  if (tail.it_off) *tail.it_off += 1u;
+  if (tail.use_cond)
+    cudaGraphSetConditional(tail.cond, (*tail.stop_rw == 0 && it + 1 <= tail.iters) ? 1u : 0u);
 }
 
 // ---------------------------------------------------------------------------
@@ -2021,10 +2030,9 @@ __device__ void solve_control(int it, const Partial* __restrict__ reduced,
   counts[1] = 0;
 }
 
-__global__ void k_band_control(int it, const Partial* __restrict__ gathered, int world,
-                               int forced_iters, st_stats* __restrict__ stats,
-                               int* __restrict__ stop) {
-  if (threadIdx.x != 0 || blockIdx.x != 0 || *stop) return;
+__device__ void band_control(int it, const Partial* __restrict__ gathered, int world,
+                             int forced_iters, st_stats* __restrict__ stats,
+                             int* __restrict__ stop) {
   Partial r = gathered[0];
   for (int w = 1; w < world; ++w) {  // rank order: identical on every shard
     const Partial& g = gathered[w];
@@ -2053,6 +2061,23 @@ __global__ void k_band_control(int it, const Partial* __restrict__ gathered, int
     return;
   }
   control_step(it, r, r.n_act, r.n_mwork, r.n_ework, forced_iters, stats, stop);
+}
+
+__global__ void k_band_control(int it, const Partial* __restrict__ gathered, int world,
+                               int forced_iters, st_stats* __restrict__ stats,
+                               int* __restrict__ stop, BandLoop loop) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (*stop) {
+    if (loop.use_cond) cudaGraphSetConditional(loop.cond, 0u);
+    return;
+  }
+  if (loop.it_off) {  // the graph loop: the iteration and its record on the device
+    it += (int)*loop.it_off;
+    gathered += *loop.it_off;
+  }
+  band_control(it, gathered, world, forced_iters, stats, stop);
+  if (loop.it_off) *loop.it_off += 1u;
+  if (loop.use_cond) cudaGraphSetConditional(loop.cond, (*stop == 0 && it + 1 <= loop.iters) ? 1u : 0u);
 }
 
 

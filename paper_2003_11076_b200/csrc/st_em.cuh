@@ -138,6 +138,14 @@ struct StatsTail {
   double* pw_scratch;      // n doubles: the finite values, compacted
   double* pw_val;          // pw_val_size(n) doubles: the slow path's tree levels
   const int32_t* mu_unsafe;  // nullable: st_mu_raster_rows' flag, into the shard record
+  // CUDA-graph loop (st_api.cu, iterations >= 3 in a conditional WHILE node):
+  // the iteration is it + *it_off (it_off nullable; the last block advances
+  // it), and the kernel sets the loop's condition: another iteration unless
+  // stopped or past `iters`
+  uint32_t* it_off;
+  int use_cond;
+  int iters;
+  cudaGraphConditionalHandle cond;
 };
 // grid of k_em_stats for n counted slots (1 << pw_depth blocks) and its depth
 int stats_depth(int64_t n);
@@ -175,9 +183,17 @@ __global__ void k_pack_outputs(const double* mu, int64_t npx, int64_t pix0, cons
 __global__ void k_fill_mu(const double* mu, int64_t npx, float* values, uint8_t* status);
 __global__ void k_stats_init(st_stats* stats, int64_t n_act);
 // Row bands: sum the shards' records (rank order, deterministic) and run the
-// iteration's control exactly as k_solve_control does for one device.
+// iteration's control exactly as the statistics kernel does for one device.
+// `loop` (zero: off) is the graph loop's state, as in StatsTail: iteration
+// it + *it_off, record gathered[*it_off], and the WHILE condition.
+struct BandLoop {
+  uint32_t* it_off;
+  int use_cond;
+  int iters;
+  cudaGraphConditionalHandle cond;
+};
 __global__ void k_band_control(int it, const Partial* gathered, int world, int forced_iters,
-                               st_stats* stats, int* stop);
+                               st_stats* stats, int* stop, BandLoop loop);
 // log(eps), log(1 - eps), log(1 - (1 - eps)) with the device log: the E-step
 // reuses them for rays whose prior is clamped (identical values).
 __global__ void k_eps_logs(double eps, double* out);

@@ -156,3 +156,39 @@ def test_c4_mu_raster_bit_exact_incl_off_hull_pixels(st):
                                 tri.num_anchors).disparity_map(w, h)
     want = oracle.mu_raster(tri.points, tri.disparities, tri.triangles, tri.planes, w, h)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), int((got != want).sum())
+
+
+@pytest.mark.parametrize("cfg,forced,max_iters,dyn", [
+    ("C2", 0, None, False), ("C2", 9, None, False), ("C3", 0, None, False),
+    ("C2", 0, 200, False), ("C2", 0, None, True), ("C2", 6, None, True)])
+def test_graph_tail_equals_launch_loop(st, monkeypatch, cfg, forced, max_iters, dyn):
+    """Iterations >= 3 as a CUDA-graph WHILE loop (st_api.cu run_tail_graph,
+    the statistics kernel sets the condition) == the plain launch loop
+    (ST_NO_GRAPH), outputs and EMStats bit for bit, with the reference's
+    convergence test, forced iterations, a long cap and dynamic_only (the
+    row-band driver, world 1: k_band_control sets the condition)."""
+    import dataclasses
+    from paper_2003_11076_b200 import _native as N
+    frame, rig, tri, sp, pp = _inputs(cfg)
+    if max_iters:
+        sp = dataclasses.replace(sp, max_iters=max_iters)
+    lib = N.lib()
+    l0 = lib.st_tail_graph_count(1)
+    a = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=forced, dynamic_only=dyn)
+    b0 = lib.st_tail_graph_count(0)
+    a2 = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=forced, dynamic_only=dyn)
+    assert lib.st_tail_graph_count(0) == b0, "the second solve did not reuse the cached graph"
+    l1 = lib.st_tail_graph_count(1)
+    assert l1 == l0 + 2, "the graph loop did not run"
+    monkeypatch.setenv("ST_NO_GRAPH", "1")
+    b = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=forced, dynamic_only=dyn)
+    assert lib.st_tail_graph_count(1) == l1
+    for r in (a, a2):
+        for x, y in ((r.disparity.values, b.disparity.values),
+                     (r.disparity.status, b.disparity.status),
+                     (r.segmentation.static_bits, b.segmentation.static_bits),
+                     (r.segmentation.valid_bits, b.segmentation.valid_bits), (r.image, b.image)):
+            assert np.array_equal(x, y)
+        assert repr(r.stats) == repr(b.stats)
+    if forced:
+        assert a.stats.iterations_run == forced
