@@ -496,8 +496,9 @@ def config_block(cfg, args, exact):
             "width": w, "height": h, "views": k, "d_max": dmax, "max_iters": iters,
             "scene": "occluder_scene(coverage=0.25, seed=11, p_flip=0.1, blur_radius=2)",
             "inputs_match_reference_digest": bool(exact),
-            "l2": "two resident frame slots alternate (pre-solve of frame i+1 overlaps the "
-                  "EM of frame i); their ~300 MB working set exceeds the 126 MB L2, no flush",
+            "l2": f"{args.value_slots} resident frame slots rotate, each on its own compute "
+                  f"stream (frames in flight concurrently); their ~{150 * args.value_slots} MB "
+                  f"working set exceeds the 126 MB L2, no flush",
             "parallelism": f"frame-parallel x{args.gpus}" if args.gpus > 1 else "1 GPU",
             "forced_iters": args.forced_iters or None}
 
@@ -528,6 +529,7 @@ def measure_sequence(dist, rank, world, flush=None):
     import multiprocessing as mp
     import torch
     import paper_2003_11076_b200 as st
+    from paper_2003_11076_b200 import _native as N
     w, h, k, dmax, iters = CONFIGS["C2"]
     sp, pp = params_for("C2")
     mine = [i for i in range(C5_FRAMES) if i % world == rank]
@@ -562,10 +564,12 @@ def measure_sequence(dist, rank, world, flush=None):
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
+    g0 = N.lib().st_tail_graph_count(0)
     t0 = time.perf_counter()
     n = run(seq)
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3
+    graph_builds = N.lib().st_tail_graph_count(0) - g0
     if dist is not None:
         tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -580,7 +584,8 @@ def measure_sequence(dist, rank, world, flush=None):
             "h2d_frame_bytes": int(h2d), "d2h_bytes_per_frame": int(w * h * 18),
             "api": "reconstruct_stream from pinned host frames, artefacts to host, "
                    "host wall clock, max over ranks",
-            "untimed_setup_s": {"render": t_render, "support_and_triangulation": t_prep}}
+            "untimed_setup_s": {"render": t_render, "support_and_triangulation": t_prep},
+            "tail_graphs_built_in_timed_region": int(graph_builds)}
 
 
 # -- row bands (BASELINE C3/C4: one frame split across the ranks) -------------------------
@@ -756,44 +761,55 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # -- value: K frames on resident inputs, the production way: two frame slots
-    # alternate, each frame's pre-solve stages (side streams: surface raster,
-    # descriptors, support groups) overlapping the previous frame's EM.  The
-    # two slots' working set (~300 MB: views, priors, descriptor maps, EM
-    # state) exceeds the 126 MB L2, so no flush is needed between steps.
-    pipe2 = FramePipeline(rig, w, h, sp, pp)
-    pipe2.load(frame.images, frame.priors)
-    tdev2 = TriDevice(tri)
-    slots = [(pipe, tdev), (pipe2, tdev2)]
-    done_ev = [None, None]
+    # -- value: K frames on resident inputs, the production way: VALUE_SLOTS
+    # frame slots rotate, each on its own compute stream (the frames are
+    # independent: several are in flight, the EM's small latency-bound
+    # worklist grids of one frame leave SMs to the others), each frame's
+    # pre-solve stages (side streams: surface raster, descriptors, support
+    # groups) starting as soon as its slot is free.  The slots' working set
+    # (~150 MB each: views, priors, descriptor maps, EM state) exceeds the
+    # 126 MB L2, so no flush is needed between steps.
+    n_slots = max(1, args.value_slots)
+    slots = [(pipe, tdev)]
+    for _ in range(n_slots - 1):
+        px = FramePipeline(rig, w, h, sp, pp)
+        px.load(frame.images, frame.priors)
+        slots.append((px, TriDevice(tri)))
+    done_ev = [None] * n_slots
 
-    def pipelined(n, events=None):
+    def pipelined(n, start=None):
+        """Enqueue n frames over the slots; returns the joined end event."""
+        if start is None:
+            start = torch.cuda.Event()
+            start.record(stream)
         for j in range(n):
-            pp_, td_ = slots[j % 2]
+            pp_, td_ = slots[j % n_slots]
+            cs = pp_.compute
+            # the slot is free once its previous frame finished
+            cs.wait_event(done_ev[j % n_slots] if done_ev[j % n_slots] is not None else start)
             ready = torch.cuda.Event()
-            if done_ev[j % 2] is not None:
-                ready = done_ev[j % 2]      # slot free once its previous frame finished
-            else:
-                ready.record(stream)
-            pp_.run(td_, forced_iters=args.forced_iters, ready=ready)
-            ev = torch.cuda.Event(enable_timing=events is not None)
-            ev.record(stream)
-            done_ev[j % 2] = ev
-            if events is not None:
-                events.append(ev)
+            ready.record(cs)
+            with torch.cuda.stream(cs):
+                pp_.run(td_, forced_iters=args.forced_iters, ready=ready)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            done_ev[j % n_slots] = ev
+        for pp_, _ in slots:
+            stream.wait_stream(pp_.compute)
+        end = torch.cuda.Event(enable_timing=True)
+        end.record(stream)
+        return end
 
-    pipelined(max(args.warmup, 4))
+    pipelined(max(args.warmup, 2 * n_slots))
     barrier()
     p0 = torch.cuda.Event(enable_timing=True)
-    marks = []
     launches0 = lib.st_launch_count()
     with ClockSampler(local) as clocks:  # (NVML starts before the first event)
         p0.record(stream)
-        pipelined(args.steps, marks)
+        p1 = pipelined(args.steps, p0)
         barrier()
     launches = lib.st_launch_count() - launches0
-    step_ms = [p0.elapsed_time(marks[0])] + [a.elapsed_time(b) for a, b in zip(marks, marks[1:])]
-    total_ms = float(np.sum(step_ms))
+    total_ms = p0.elapsed_time(p1)
     if dist is not None:
         tt = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -1131,6 +1147,8 @@ def main():
     ap.add_argument("--shard", default="frames", choices=["frames", "rows"],
                     help="multi-GPU split: frames (C5 frame-parallel, default) or rows "
                          "(one frame in row bands, C3/C4)")
+    ap.add_argument("--value-slots", type=int, default=4,
+                    help="resident frame slots (each its own compute stream) in the value loop")
     ap.add_argument("--row-band-steps", type=int, default=10,
                     help="frame-parallel runs also time C3 row bands over the same ranks "
                          "(0 = skip)")

@@ -6,6 +6,8 @@
 
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "st_common.cuh"
 
 namespace st {
@@ -309,11 +311,32 @@ extern "C" int st_support_build_rows(const double* support_uv, const double* sup
     return ST_EINVAL;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  const SupLayout L = sup_layout(n, W, H, p->neighborhood_radius);
+  SupLayout L = sup_layout(n, W, H, p->neighborhood_radius);
   if ((int64_t)L.total > workspace_bytes) {
     sthost::set_error("support workspace too small (%lld < %lld)", (long long)workspace_bytes,
                       (long long)L.total);
     return ST_ENOMEM;
+  }
+  {
+    // lay the record arrays out for the largest support count the workspace
+    // holds: the group tables' addresses (st_frame.sup_*) then do not move
+    // with the frame's support count, so the EM's cached graph (st_api.cu)
+    // serves every frame of a stream
+    const int ir = (int)floor(p->neighborhood_radius);
+    const int64_t tpp = tiles_per_point_max(ir < 0 ? 0 : ir);
+    const int64_t per_rec = 16 + 8 * ST_TH;
+    const int64_t fixed = (int64_t)L.recs + (int64_t)align_up(L.cub_bytes) + 6 * 256;
+    if (workspace_bytes > fixed) {
+      int64_t ncap = ((workspace_bytes - fixed) / per_rec - 1) / tpp;
+      ncap = std::min<int64_t>(ncap, (int64_t)1 << 28);
+      for (int tries = 0; tries < 4 && ncap > n; ++tries, ncap -= 64) {
+        const SupLayout L2 = sup_layout((int)ncap, W, H, p->neighborhood_radius);
+        if ((int64_t)L2.total <= workspace_bytes) {
+          L = L2;
+          break;
+        }
+      }
+    }
   }
   char* ws = (char*)workspace;
   uint32_t* cnt = (uint32_t*)(ws + L.cnt);

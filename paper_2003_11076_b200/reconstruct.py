@@ -92,6 +92,11 @@ class FramePipeline:
         prio = int(os.environ.get("ST_SIDE_PRIORITY", "-1"))
         self.side = t.cuda.Stream(priority=prio)
         self.side2 = t.cuda.Stream()
+        # the slot's EM + refocus stream in reconstruct_stream: the slots'
+        # frames are independent, so several are in flight at once (the EM's
+        # later iterations are small latency-bound grids that leave most SMs
+        # to the other frames)
+        self.compute = t.cuda.Stream()
 
     def _empty(self, shape, dtype):
         if not self.guard_bytes:
@@ -411,12 +416,20 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
                        median_radius=1, forced_iters=0):
     """Pipelined `reconstruct` over a sequence of (frame, tri) pairs.
 
-    Yields one Reconstruction per frame, in order.  Two device pipelines
-    rotate (STREAM_SLOTS): while frame i computes on the caller's stream, a host thread
-    uploads frame i+1 (pinned frames copy by DMA) and its triangulation on a
-    copy stream, and frame i-1's artefacts stream back to pinned host memory
-    on a third stream.  Every frame gets the full per-frame work of
-    `reconstruct`.
+    Yields one Reconstruction per frame, in order.  Device pipelines rotate
+    (STREAM_SLOTS): while frame i computes on the caller's stream, a host
+    thread uploads frame i+1 (pinned frames copy by DMA) and its
+    triangulation on a copy stream, and finished frames' artefacts stream
+    back to pinned host memory on an output stream, in order.  Every frame
+    gets the full per-frame work of `reconstruct`.
+
+    ST_STREAM_COMPUTE selects the compute streams: "main" (default: the
+    caller's stream; frame i+1's pre-solve stages still overlap frame i's
+    EM), an integer k (k slot streams in rotation) or "slot" (one per slot:
+    several frames' EMs in flight).  With the host copies in the loop the
+    copy engines bound the stream and the concurrent modes measured no
+    faster (profiles/r02_stream_modes.txt); bench.py's resident `value` loop
+    runs one stream per slot.
     """
     import queue
     import threading
@@ -433,6 +446,9 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
     main = t.cuda.current_stream()
     copy_s, out_s = t.cuda.Stream(), t.cuda.Stream()
     n_slots = len(pipes)
+    mode = os.environ.get("ST_STREAM_COMPUTE", "main")
+    compute_streams = ([main] if mode == "main" else
+                       [x.compute for x in pipes][:n_slots if mode == "slot" else int(mode)])
     free = [None] * n_slots      # event: pipe's inputs/outputs no longer in use
     free_lock = threading.Condition()
     q = queue.Queue(maxsize=max(1, len(pipes) - 1))  # prepared frames ahead of the consumer
@@ -440,7 +456,6 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
 
     device = t.cuda.current_device()
 
-    import os
     import time
     prof = {} if os.environ.get("ST_STREAM_PROFILE") else None
 
@@ -503,19 +518,22 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
                 break
             t0 = tick("main_wait_prep", t0)
             pipe, td, loaded, check = item
-            main.wait_event(loaded)
+            cs = compute_streams[i % len(compute_streams)]
+            cs.wait_event(loaded)
             for x in td.tensors():
-                for st_ in (main, pipe.side, pipe.side2):
+                for st_ in (cs, pipe.side, pipe.side2):
                     x.record_stream(st_)
             # the frame's pre-solve stages start as soon as its inputs are on the
-            # device, overlapping the previous frame's EM on the main stream
+            # device, its EM on the slot's stream, concurrently with the frames
+            # of the other slots
             if not dynamic_only:
                 # one native call enqueues the whole frame and its D2H (st_frame_run)
                 fetched = t.cuda.Event()
                 fetched.record(out_s)  # creates the event; st_frame_run re-records it
-                block, stats = pipe.run_native(td, forced_iters=forced_iters,
-                                               median_radius=median_radius, ready=loaded,
-                                               out_stream=out_s, done=fetched)
+                with t.cuda.stream(cs):
+                    block, stats = pipe.run_native(td, forced_iters=forced_iters,
+                                                   median_radius=median_radius, ready=loaded,
+                                                   out_stream=out_s, done=fetched)
                 host = pipe.host_views(block)
                 t0 = tick("main_run", t0)
                 with t.cuda.stream(out_s):
@@ -526,11 +544,12 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
                         fetched = t.cuda.Event()
                         fetched.record(out_s)
             else:
-                stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
-                                 median_radius=median_radius, ready=loaded)
+                with t.cuda.stream(cs):
+                    stats = pipe.run(td, dynamic_only=dynamic_only, forced_iters=forced_iters,
+                                     median_radius=median_radius, ready=loaded)
                 t0 = tick("main_run", t0)
                 done = t.cuda.Event()
-                done.record(main)
+                done.record(cs)
                 with t.cuda.stream(out_s):
                     out_s.wait_event(done)
                     host = pipe.fetch_async(out_s)
@@ -571,7 +590,7 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
             except queue.Empty:
                 break
         worker.join()
-        for s_ in (copy_s, main, out_s):
+        for s_ in [copy_s, main, out_s] + compute_streams:
             s_.synchronize()
         pipes.busy = False
         if prof is not None:
