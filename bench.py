@@ -46,15 +46,25 @@ def log(*a):
 
 # -- inputs -----------------------------------------------------------------------
 
-def load_inputs(cfg):
-    """Render the config's frame (bit-identical to the reference renderer) and
-    triangulate the support the reference harvested for it."""
+def load_inputs(cfg, host=None):
+    """Render the config's frame (bit-identical to the reference renderer:
+    checked against the digests the reference recorded) and triangulate the
+    support the reference harvested for it.  The device renderer
+    (paper_2003_11076_b200.renderer) when CUDA is up; `host` (the reference
+    arm, CPU-only tests) takes the numpy restatement in oracle/synth.py."""
     import hashlib
+    import torch
     from paper_2003_11076_b200 import synth
     from paper_2003_11076_b200.prior import SupportPoint, triangulate
+    if host is None:
+        host = not torch.cuda.is_available()
     w, h, k, dmax, iters = CONFIGS[cfg]
     spec = synth.occluder_scene(width=w, height=h, cameras=k, **SCENE)
-    frame, _ = synth.render(spec)
+    if host:
+        from oracle.synth import render
+    else:
+        render = synth.render
+    frame, _ = render(spec)
     rig = spec.rig()
     path = os.path.join(ROOT, "tests", "golden", f"bench_{cfg}.npz")
     z = np.load(path)
@@ -462,7 +472,7 @@ def run_reference(args):
         return
     cfg = args.config
     w, h, k, dmax, iters = CONFIGS[cfg]
-    frame, rig, tri, exact = load_inputs(cfg)
+    frame, rig, tri, exact = load_inputs(cfg, host=True)  # (none of this repo's kernels)
     with blas_threads(None):
         for _ in range(args.warmup):
             oracle_sample(frame, rig, tri, cfg, rows=max(8, h // 16))
@@ -509,7 +519,8 @@ C5_FRAMES, C5_DISTINCT, C5_SEED0 = 1000, 16, 11
 
 
 def _render_c5(seed):
-    """One distinct C5 frame (occluder_scene seeds 11..26)."""
+    """One distinct C5 frame (occluder_scene seeds 11..26),
+    rendered on the device."""
     from paper_2003_11076_b200 import synth
     w, h, k, dmax, iters = CONFIGS["C2"]
     sc = dict(SCENE, seed=seed)
@@ -525,8 +536,6 @@ def measure_sequence(dist, rank, world, flush=None):
     and triangulations are computed once (device harvest + host Qhull), not
     timed, as SURVEY.md §8d prescribes.  Total work is fixed: strong
     scaling; time = max over ranks."""
-    import concurrent.futures as cf
-    import multiprocessing as mp
     import torch
     import paper_2003_11076_b200 as st
     from paper_2003_11076_b200 import _native as N
@@ -535,9 +544,7 @@ def measure_sequence(dist, rank, world, flush=None):
     mine = [i for i in range(C5_FRAMES) if i % world == rank]
     need = sorted({i % C5_DISTINCT for i in mine})
     t0 = time.perf_counter()
-    workers = max(1, min(len(need), cpu_cores()))
-    with cf.ProcessPoolExecutor(workers, mp_context=mp.get_context("spawn")) as ex:
-        rendered = dict(zip(need, ex.map(_render_c5, [C5_SEED0 + j for j in need])))
+    rendered = {j: _render_c5(C5_SEED0 + j) for j in need}
     t_render = time.perf_counter() - t0
     from paper_2003_11076_b200 import synth
     rig = synth.occluder_scene(width=w, height=h, cameras=k, **SCENE).rig()

@@ -104,7 +104,7 @@ int st_version(void);
 int st_device_count(void);
 /* sizeof the ABI structs as this library was compiled (binding checks, no GPU
  * needed): which = 0 st_rig, 1 st_params, 2 st_stats, 3 st_frame, 4 st_tri,
- * 5 st_cams, 6 st_frame_plan; -1 for an unknown id. */
+ * 5 st_cams, 6 st_frame_plan, 7 st_scene; -1 for an unknown id. */
 int64_t st_struct_size(int32_t which);
 /* Cumulative number of __global__ launches issued by this library (all
  * threads; CUB's internal launches inside st_support_build / st_solve count
@@ -490,6 +490,58 @@ int st_frame_run(st_frame_plan* plan, const st_tri* tri, const double* support_u
                  const double* support_d, int32_t n_support, void* ready, void* host_block,
                  void* done);
 int64_t st_frame_host_bytes(int32_t W, int32_t H);
+
+/* ---- synthetic light fields on the device -------------
+ * Replaces the reference renderer `render` (synth.py:244-309: _trace
+ * :174-230, surface_color :59-82, value noise :25-56, billboard edges
+ * :264-283, ground truth :287-290) and `corrupt_prior` (synth.py:334-346).
+ * The host side (render.py) draws each surface's texture constants with
+ * numpy exactly as surface_color does and passes them in st_surface. */
+#define ST_MAX_SURFACES 8
+
+typedef struct st_surface {
+  int32_t is_occluder;      /* OccluderSpec (1) or PlaneSpec (0) */
+  int32_t seed;             /* lattice-noise seed (low 32 bits used, synth.py:33) */
+  int32_t has_x_min, has_x_max;
+  double depth, base, amplitude, frequency;
+  double x_min, x_max;      /* planes: px >= x_min, px < x_max */
+  double half_w, half_h;    /* occluders: width / 2.0, height / 2.0 */
+  double center_x, center_y;
+  double c0[3];             /* 2.0 * np.pi * rate[i] */
+  double ca[3], sa[3];      /* np.cos(ang[i]), np.sin(ang[i]) */
+  double ph[3][3];          /* ph[i][c] */
+  double nw[3];
+} st_surface;
+
+typedef struct st_scene {
+  int32_t width, height;
+  int32_t n_surfaces;       /* in trace order: occluders by depth, then planes by depth */
+  int32_t pad_;
+  double fx, fy, cx, cy;    /* SceneSpec.intrinsics() */
+  st_surface surf[ST_MAX_SURFACES];
+} st_scene;
+
+/* One view: image (H, W, 3) u8 and occluder mask (H, W) u8 (cover >= 0.5),
+ * with the 4-sample supersampling on the billboard edges of the n_rects
+ * occluder rectangles (device array of (u0, u1, v0, v1), synth.py:236-241).
+ * center = camera centre, rotation = the extrinsic rotation (row-major).
+ * *fail (device) is set to 1 when a ray hits no surface (the reference's
+ * ValueError). */
+int st_render_view(const st_scene* scene, const double* center, const double* rotation,
+                   const double* rects_dev, int32_t n_rects, uint8_t* image, uint8_t* mask,
+                   int32_t* fail, void* stream);
+/* The reference view's background (no occluders) and ground-truth
+ * disparity float32(focal_baseline / depth) (synth.py:287-290). */
+int st_render_background(const st_scene* scene, const double* center, const double* rotation,
+                         double focal_baseline, uint8_t* image, float* disparity, int32_t* fail,
+                         void* stream);
+/* corrupt_prior(1 - mask, p_flip, blur_radius, seed) -> float32 (H, W):
+ * pcg_state = numpy PCG64 {state_hi, state_lo, inc_hi, inc_lo} of
+ * default_rng(seed) (the flips are its first H*W random() draws). */
+int st_corrupt_prior(const uint8_t* mask, int32_t W, int32_t H, const uint64_t* pcg_state,
+                     double p_flip, int32_t blur_radius, float* prior, void* workspace,
+                     int64_t workspace_bytes, void* stream);
+int64_t st_corrupt_prior_workspace(int32_t W, int32_t H);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,27 @@ class StRig(C.Structure):
                 ("view_w", C.c_int32 * MAX_VIEWS), ("view_h", C.c_int32 * MAX_VIEWS)]
 
 
+MAX_SURFACES = 8
+
+
+class StSurface(C.Structure):
+    _fields_ = [("is_occluder", C.c_int32), ("seed", C.c_int32),
+                ("has_x_min", C.c_int32), ("has_x_max", C.c_int32),
+                ("depth", C.c_double), ("base", C.c_double), ("amplitude", C.c_double),
+                ("frequency", C.c_double), ("x_min", C.c_double), ("x_max", C.c_double),
+                ("half_w", C.c_double), ("half_h", C.c_double),
+                ("center_x", C.c_double), ("center_y", C.c_double),
+                ("c0", C.c_double * 3), ("ca", C.c_double * 3), ("sa", C.c_double * 3),
+                ("ph", (C.c_double * 3) * 3), ("nw", C.c_double * 3)]
+
+
+class StScene(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("n_surfaces", C.c_int32),
+                ("pad_", C.c_int32), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double),
+                ("surf", StSurface * MAX_SURFACES)]
+
+
 class StParams(C.Structure):
     _fields_ = [("beta", C.c_double), ("threshold", C.c_double),
                 ("max_iters", C.c_int32), ("min_static_rays", C.c_int32),
@@ -167,6 +188,10 @@ _SIGS = {
     "st_refocus_pixels": (C.c_int, [_P, C.POINTER(StRig), _P, _P, _P, _I64, _I32, _P, _P, _P,
                                     _P, _P]),
     "st_copy_mask": (C.c_int, [_P, _I64, _D, _P, _P]),
+    "st_render_view": (C.c_int, [C.POINTER(StScene), _P, _P, _P, _I32, _P, _P, _P, _P]),
+    "st_render_background": (C.c_int, [C.POINTER(StScene), _P, _P, _D, _P, _P, _P, _P]),
+    "st_corrupt_prior": (C.c_int, [_P, _I32, _I32, _P, _D, _I32, _P, _P, _I64, _P]),
+    "st_corrupt_prior_workspace": (C.c_int64, [_I32, _I32]),
     "st_median": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P]),
 }
 

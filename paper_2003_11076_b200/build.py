@@ -16,7 +16,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libseethrough_b200.so")
 SOURCES = ["st_api.cu", "st_em.cu", "st_features.cu", "st_frame.cu", "st_harvest.cu",
-           "st_host.cu", "st_mean.cu", "st_mu.cu", "st_prior.cu", "st_refocus.cu"]
+           "st_host.cu", "st_mean.cu", "st_mu.cu", "st_prior.cu", "st_refocus.cu",
+           "st_render.cu"]
 HEADERS = ["st_common.cuh", "st_em.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

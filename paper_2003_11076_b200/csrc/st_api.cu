@@ -407,6 +407,7 @@ int64_t st_struct_size(int32_t which) {
     case 4: return (int64_t)sizeof(st_tri);
     case 5: return (int64_t)sizeof(st_cams);
     case 6: return (int64_t)sizeof(st_frame_plan);
+    case 7: return (int64_t)sizeof(st_scene);
     default: return -1;
   }
 }

@@ -44,7 +44,8 @@ def test_binding_covers_header(lib):
 def test_struct_layouts_match_the_header(lib):
     """The ctypes mirrors have the size the compiled library gives each struct."""
     from paper_2003_11076_b200 import _native as N
-    mirrors = (N.StRig, N.StParams, N.StStats, N.StFrame, N.StTri, N.StCams, N.StFramePlan)
+    mirrors = (N.StRig, N.StParams, N.StStats, N.StFrame, N.StTri, N.StCams, N.StFramePlan,
+               N.StScene)
     for which, cls in enumerate(mirrors):
         assert ctypes.sizeof(cls) == N.lib().st_struct_size(which), cls.__name__
     assert N.lib().st_struct_size(99) == -1

@@ -21,7 +21,8 @@ import pytest
 
 from paper_2003_11076_b200 import pipeline as pl
 from paper_2003_11076_b200 import pnm
-from paper_2003_11076_b200.synth import occluder_scene, render
+from oracle.synth import render
+from paper_2003_11076_b200.synth import occluder_scene
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 _GOLD = json.load(open(os.path.join(HERE, "golden", "pipeline_cases.json")))
@@ -265,10 +266,12 @@ def test_run_reconstruct_sequence_equals_single_runs(tmp_path):
 
 # -- run_synth / run_evaluate (§8(f)4) ----------------------------------------------------
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("name", sorted(SYNTH))
 def test_run_synth_matches_reference_files(tmp_path, name):
     """Every file run_synth writes (scene.txt, calibration, views, priors,
-    ground-truth masks / disparity / background) equals the reference's."""
+    ground-truth masks / disparity / background; the device renderer)
+    equals the reference's."""
     case = SYNTH[name]
     out = str(tmp_path / "synth")
     pl.run_synth(out, preset=case["preset"], seed=case["seed"])
@@ -276,6 +279,20 @@ def test_run_synth_matches_reference_files(tmp_path, name):
     assert got == case["synth"]
 
 
+@pytest.mark.parametrize("name", sorted(SYNTH))
+def test_run_synth_writers_with_the_oracle_renderer(tmp_path, monkeypatch, name):
+    """run_synth's writers on CPU: with the numpy renderer (oracle/synth.py)
+    in place of the device one, every file equals the reference's."""
+    from paper_2003_11076_b200 import synth
+    monkeypatch.setattr(synth, "render", render)
+    case = SYNTH[name]
+    out = str(tmp_path / "synth")
+    pl.run_synth(out, preset=case["preset"], seed=case["seed"])
+    got = {f: _digest(os.path.join(out, f)) for f in sorted(os.listdir(out))}
+    assert got == case["synth"]
+
+
+@pytest.mark.gpu
 def test_run_synth_scene_file_and_errors(tmp_path):
     from paper_2003_11076_b200 import synth
     a = str(tmp_path / "a")

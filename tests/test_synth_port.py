@@ -1,8 +1,7 @@
-"""The in-package renderer reproduces the reference renderer bit for bit (CPU).
-
-The bench renders its inputs on the GPU box with paper_2003_11076_b200.synth;
-this pins that port to the reference (synth.py) here, and to the digests the
-reference recorded in tests/golden/bench_*.npz.
+"""The numpy restatement of the reference renderer (oracle/synth.py) is
+bit-identical to the reference (synth.py) here, and to the digests the
+reference recorded in tests/golden/bench_*.npz (CPU).  It is the checker of
+the device renderer (tests/test_gpu_render.py).
 """
 
 import hashlib
@@ -11,7 +10,8 @@ import os
 import numpy as np
 import pytest
 
-from paper_2003_11076_b200 import synth as port
+from oracle import synth as port
+from paper_2003_11076_b200 import synth as specs
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
@@ -24,7 +24,7 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 ])
 def test_render_matches_reference(reference, maker, kw):
     ref_spec = getattr(reference, maker)(**kw)
-    my_spec = getattr(port, maker)(**kw)
+    my_spec = getattr(specs, maker)(**kw)
     rf, rgt = reference.render(ref_spec)
     mf, mgt = port.render(my_spec)
     for a, b in zip(rf.images, mf.images):
@@ -60,7 +60,7 @@ def test_c1_bench_frame_matches_recorded_digest():
         pytest.skip("bench inputs not recorded")
     z = np.load(path)
     w, h, k = (int(x) for x in z["config"][:3])
-    frame, _ = port.render(port.occluder_scene(width=w, height=h, cameras=k, coverage=0.25,
+    frame, _ = port.render(specs.occluder_scene(width=w, height=h, cameras=k, coverage=0.25,
                                                seed=11, p_flip=0.1, blur_radius=2))
     assert _digest(frame.images) == str(z["image_digest"])
     assert _digest(frame.priors) == str(z["prior_digest"])
