@@ -293,7 +293,24 @@ def next_rows(frame, rig, cfg, pipe, host_frame, peak, cpu_leg=True):
         single_s = time.perf_counter() - t0
     finally:
         shutil.rmtree(io_dir, ignore_errors=True)
+    # (f)4 the device renderer (st_render.cu): one whole synthetic frame
+    # (K views + priors + ground truth) to host numpy arrays
+    from paper_2003_11076_b200 import synth
+    spec = synth.occluder_scene(width=w, height=h, cameras=k, **SCENE)
+    synth.render(spec)
+    torch.cuda.synchronize()
+    n_r = 5
+    t0 = time.perf_counter()
+    for _ in range(n_r):
+        synth.render(spec)
+    torch.cuda.synchronize()
+    render_ms = (time.perf_counter() - t0) * 1e3 / n_r
     out = {
+        "renderer": {"device_frame_ms": render_ms, "config": cfg,
+                     "api": "synth.render (device: st_render_view / st_render_background / "
+                            "st_corrupt_prior), host numpy frame + ground truth out",
+                     "parity": "bit-identical to the reference renderer "
+                               "(tests/test_gpu_render.py, bench digests C1-C4)"},
         "harvest": {"device_ms": hv_ms, "includes": "descriptors + st_harvest",
                     "candidates": n_cand, "reverse_scans": n_rev, "grid": nd,
                     "host_d2h_dedup_ms": t_host * 1e3, "points_kept": int(len(u)),
@@ -338,6 +355,14 @@ def next_rows(frame, rig, cfg, pipe, host_frame, peak, cpu_leg=True):
             "kind": "port",
             "sample": f"reference view's detection + SAD match + left-right check through the "
                       f"numpy oracle ({t_view:.2f} s), x{k} views; descriptors from the device"}
+        from oracle.synth import render as host_render
+        t0 = time.perf_counter()
+        host_render(spec)
+        t_r = time.perf_counter() - t0
+        out["renderer"]["cpu_baseline"] = {
+            "value": 1.0 / t_r, "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": f"one whole {cfg} frame through the numpy restatement of the reference "
+                      f"renderer (oracle/synth.py, {t_r:.2f} s)"}
     return out
 
 
