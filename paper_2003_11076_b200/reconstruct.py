@@ -417,19 +417,20 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
     """Pipelined `reconstruct` over a sequence of (frame, tri) pairs.
 
     Yields one Reconstruction per frame, in order.  Device pipelines rotate
-    (STREAM_SLOTS): while frame i computes on the caller's stream, a host
-    thread uploads frame i+1 (pinned frames copy by DMA) and its
-    triangulation on a copy stream, and finished frames' artefacts stream
-    back to pinned host memory on an output stream, in order.  Every frame
-    gets the full per-frame work of `reconstruct`.
+    (STREAM_SLOTS), each computing on its own stream, so several frames are
+    in flight: a host thread uploads the next frames (pinned frames copy by
+    DMA) and their triangulations on a copy stream, each frame's pre-solve
+    stages, EM and refocus run on its slot's streams, and finished frames'
+    artefacts stream back to pinned host memory on an output stream, in
+    order; a frame is handed out once `depth` (STREAM_SLOTS - 1) later
+    frames are enqueued.  Every frame gets the full per-frame work of
+    `reconstruct`.
 
-    ST_STREAM_COMPUTE selects the compute streams: "main" (default: the
-    caller's stream; frame i+1's pre-solve stages still overlap frame i's
-    EM), an integer k (k slot streams in rotation) or "slot" (one per slot:
-    several frames' EMs in flight).  With the host copies in the loop the
-    copy engines bound the stream and the concurrent modes measured no
-    faster (profiles/r02_stream_modes.txt); bench.py's resident `value` loop
-    runs one stream per slot.
+    ST_STREAM_COMPUTE selects the compute streams: "slot" (default, one per
+    slot), an integer k (k slot streams in rotation) or "main" (the caller's
+    stream: the frames' EMs serialised, frame i+1's pre-solve stages still
+    overlapping frame i's EM); ST_STREAM_DEPTH the frames in flight
+    (profiles/r02_stream_modes.txt).
     """
     import queue
     import threading
@@ -446,9 +447,14 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
     main = t.cuda.current_stream()
     copy_s, out_s = t.cuda.Stream(), t.cuda.Stream()
     n_slots = len(pipes)
-    mode = os.environ.get("ST_STREAM_COMPUTE", "main")
+    mode = os.environ.get("ST_STREAM_COMPUTE", "slot")
     compute_streams = ([main] if mode == "main" else
                        [x.compute for x in pipes][:n_slots if mode == "slot" else int(mode)])
+    # frames enqueued ahead of the one being handed out (its D2H awaited):
+    # concurrent compute streams need several in flight
+    depth = int(os.environ.get("ST_STREAM_DEPTH",
+                               "1" if len(compute_streams) == 1 else str(n_slots - 1)))
+    depth = max(1, min(depth, n_slots - 1))
     free = [None] * n_slots      # event: pipe's inputs/outputs no longer in use
     free_lock = threading.Condition()
     q = queue.Queue(maxsize=max(1, len(pipes) - 1))  # prepared frames ahead of the consumer
@@ -508,7 +514,8 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
 
     worker = threading.Thread(target=prep, daemon=True)
     worker.start()
-    pending = None
+    from collections import deque
+    pending = deque()
     i = 0
     try:
         while True:
@@ -563,19 +570,17 @@ def reconstruct_stream(items, rig, params=None, prior_params=None, dynamic_only=
                 free[i % n_slots] = fetched
                 free_lock.notify_all()
             t0 = tick("main_fetch_enqueue", t0)
-            if pending is not None:
-                prev, pending = pending, None
-                out = _finish(prev)
+            pending.append((pipe, stats, fetched, host, flags))
+            i += 1
+            if len(pending) > depth:
+                out = _finish(pending.popleft())
                 t0 = tick("main_finish_prev", t0)
                 yield out
                 t0 = time.perf_counter()
-            pending = (pipe, stats, fetched, host, flags)
-            i += 1
         if error:
             raise error[0]
-        if pending is not None:
-            prev, pending = pending, None
-            yield _finish(prev)
+        while pending:
+            yield _finish(pending.popleft())
     finally:
         # normal end, an error, or a consumer that stopped early (generator
         # close): stop the prep thread, let the device finish every enqueued

@@ -135,8 +135,10 @@ def render(spec):
     if int(download(fail)[0]):
         raise ValueError("scene constraint violated: some rays hit no surface "
                          "(deepest plane must be an unbounded backdrop)")
-    frame = LightFieldFrame(images=[download(x) for x in images],
-                            priors=[download(x) for x in priors])
-    gt = GroundTruth(disparity=download(gt_disp), background=download(gt_bg),
-                     masks=[download(m).astype(bool) for m in masks])
+    # plain (pageable) numpy arrays out, like the reference's
+    t.cuda.current_stream().synchronize()
+    frame = LightFieldFrame(images=[x.cpu().numpy() for x in images],
+                            priors=[x.cpu().numpy() for x in priors])
+    gt = GroundTruth(disparity=gt_disp.cpu().numpy(), background=gt_bg.cpu().numpy(),
+                     masks=[m.cpu().numpy().astype(bool) for m in masks])
     return frame, gt

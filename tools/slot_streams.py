@@ -21,7 +21,7 @@ w, h, k, dmax, iters = bench.CONFIGS[cfg]
 sp, pp = bench.params_for(cfg)
 frame, rig, tri, exact = bench.load_inputs(cfg)
 pipes = []
-for _ in range(4):
+for _ in range(int(os.environ.get('SLOTS_MAX', '4'))):
     p = FramePipeline(rig, w, h, sp, pp)
     p.load(frame.images, frame.priors)
     pipes.append((p, TriDevice(tri)))
@@ -57,7 +57,8 @@ def run(n_slots, n_streams, steps, prio=0):
 
 
 out = {}
-for slots, streams, prio in ((2, 1, 0), (2, 2, 0), (3, 3, 0), (4, 4, 0), (4, 2, 0), (2, 2, -1), (3, 3, -1)):
+CASES = [tuple(int(v) for v in c.split(',')) for c in os.environ['SLOT_CASES'].split(';')] if os.environ.get('SLOT_CASES') else ((2, 1, 0), (2, 2, 0), (3, 3, 0), (4, 4, 0), (4, 2, 0), (2, 2, -1), (3, 3, -1))
+for slots, streams, prio in CASES:
     run(slots, streams, 8, prio)
     fps = [run(slots, streams, steps, prio) for _ in range(5)]
     out[f"slots{slots}_streams{streams}_prio{prio}"] = [round(float(np.median(fps)), 1), round(min(fps), 1), round(max(fps), 1)]

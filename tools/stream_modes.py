@@ -34,9 +34,12 @@ def stream(n, dyn):
     return n / (time.perf_counter() - t0)
 
 
-for mode in ("main", "2", "3", "slot", "main"):
+CASES = os.environ.get("MODE_CASES", "main:1,main:2,main:4,slot:4,2:4,slot:2,main:1").split(",")
+for case in CASES:
+    mode, depth = case.split(":")
     os.environ["ST_STREAM_COMPUTE"] = mode
+    os.environ["ST_STREAM_DEPTH"] = depth
     for dyn in (False, True):
         r = [stream(60, dyn) for _ in range(3)]
-        print(f"mode {mode:5s} dyn {int(dyn)}: fps {np.median(r):.1f} ({min(r):.1f}-{max(r):.1f})",
-              flush=True)
+        print(f"mode {mode:5s} depth {depth} dyn {int(dyn)}: fps {np.median(r):.1f} "
+              f"({min(r):.1f}-{max(r):.1f})", flush=True)
