@@ -1104,7 +1104,10 @@ def run_ours(args):
                                   "evaluated real candidate, static in-margin view), "
                                   "counted on the device",
                      "launch_ms": ms_m / max(1, n_m), "launches_per_step": n_m,
-                     "share_of_step": ms_m / step_ms_mean,
+                     # the step as ncu sees it: one frame at a time (the launch list
+                     # is serialised), not the concurrent slots' 1/fps
+                     "share_of_step": ms_m / latency_ms,
+                     "share_of_concurrent_step": ms_m / step_ms_mean,
                      "model": {"algorithmic_bytes_per_launch": model_bytes_m / max(1, n_m),
                                "achieved": model_achieved, "frac": model_achieved / peak,
                                "note": "SURVEY 8d charges every candidate; exact pruning "
