@@ -962,7 +962,7 @@ def run_ours(args):
 
     dropin_n = 10
     dropin_ms = max_ranks(e2e_dropin(dropin_n))
-    dyn_n = max(10, e2e_steps // 2)
+    dyn_n = max(10, e2e_steps)
     dyn_ms = max_ranks(dyn_stream(dyn_n))
     # resident dynamic_only frames (CUDA events, L2 flushed between steps)
     pipe.run(tdev, dynamic_only=True)
