@@ -1152,8 +1152,10 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
   // Iterations >= 3 of a one-device solve run as a CUDA-graph WHILE loop
   // (the statistics kernel sets its condition): the frame's converged
   // iterations cost no launches and no host round trip, whatever the cap.
-  // (row bands exchanging records through the host callback keep the loop)
-  bool use_graph = !A.exchange && n > 0 && iters >= 3 && tail_graphs_enabled();
+  // (row bands exchanging records through the host callback keep the loop,
+  // and so do active-pixel lists (dynamic_only): their length, part of the
+  // captured arguments, changes from frame to frame)
+  bool use_graph = !A.exchange && !A.active && n > 0 && iters >= 3 && tail_graphs_enabled();
   // a row band with no active pixel still takes part in every exchange
   for (int it = 1; it <= iters && (n > 0 || A.band); ++it) {
     if (use_graph && it == 3) {

@@ -165,8 +165,8 @@ def test_graph_tail_equals_launch_loop(st, monkeypatch, cfg, forced, max_iters, 
     """Iterations >= 3 as a CUDA-graph WHILE loop (st_api.cu run_tail_graph,
     the statistics kernel sets the condition) == the plain launch loop
     (ST_NO_GRAPH), outputs and EMStats bit for bit, with the reference's
-    convergence test, forced iterations, a long cap and dynamic_only (the
-    row-band driver, world 1: k_band_control sets the condition)."""
+    convergence test, forced iterations and a long cap; dynamic_only (the
+    row-band driver with an active list) stays on the launch loop."""
     import dataclasses
     from paper_2003_11076_b200 import _native as N
     frame, rig, tri, sp, pp = _inputs(cfg)
@@ -179,7 +179,9 @@ def test_graph_tail_equals_launch_loop(st, monkeypatch, cfg, forced, max_iters, 
     a2 = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=forced, dynamic_only=dyn)
     assert lib.st_tail_graph_count(0) == b0, "the second solve did not reuse the cached graph"
     l1 = lib.st_tail_graph_count(1)
-    assert l1 == l0 + 2, "the graph loop did not run"
+    # (dynamic_only's active lists change length frame to frame: it keeps the
+    # launch loop, st_api.cu)
+    assert l1 == l0 + (0 if dyn else 2), "graph loop launches"
     monkeypatch.setenv("ST_NO_GRAPH", "1")
     b = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=forced, dynamic_only=dyn)
     assert lib.st_tail_graph_count(1) == l1
