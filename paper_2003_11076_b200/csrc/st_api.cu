@@ -839,6 +839,7 @@ struct TailGraphKey {
   const st_stats* stats;
   const char* ws;
   const int32_t* mu_unsafe;
+  const uint32_t* n_dev;
   int band, forced_iters, iters, wave_env, device;
 };
 
@@ -961,6 +962,9 @@ struct AsyncSolve {
   int world;
   void* rec_send;
   void* rec_recv;
+  // nullable: the slot count on the device (dynamic_only, one shard: no host
+  // read-back); n and cnt_hi are then its upper bound (the grids)
+  const uint32_t* n_dev;
 };
 
 static int solve_async_core(const st_frame* f, const st_rig* rig, const st_params* p,
@@ -988,7 +992,7 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
   ST_CUDA_CHECK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t) + sizeof(int), s));
   // E-step fallback count (byte 48) and the stats kernel's block counter (52)
   ST_CUDA_CHECK(cudaMemsetAsync(counts + 12, 0, 4 * sizeof(uint32_t), s));
-  st::k_stats_init<<<1, 32, 0, s>>>(stats_dev, n_cnt);
+  st::k_stats_init<<<1, 32, 0, s>>>(stats_dev, A.n_dev ? 0 : n_cnt);  // (band control sets it)
   ST_LAUNCH_CHECK("k_stats_init");
   double* eps_logs = (double*)(counts + 4);
   st::k_eps_logs<<<1, 32, 0, s>>>(p->epsilon_prior, eps_logs);
@@ -1031,6 +1035,7 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
   graph_key.stats = stats_dev;
   graph_key.ws = ws;
   graph_key.mu_unsafe = f->mu_unsafe;
+  graph_key.n_dev = A.n_dev;
   graph_key.band = A.band ? 1 : 0;
   graph_key.forced_iters = p->forced_iters;
   graph_key.iters = iters;
@@ -1047,7 +1052,8 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     if (n > 0) {
     if (it > 1) {
       st::k_flag_mstep<<<wave, EM_BLOCK, 0, s>>>(A.active, n, c.pix0, static_bits, mask_in,
-                                                 e_act, pe_act, chg, mlist, counts, stop);
+                                                 e_act, pe_act, chg, mlist, counts, stop,
+                                                 A.n_dev);
       ST_LAUNCH_CHECK("k_flag_mstep");
     }
     st::MStepArgs a;
@@ -1068,6 +1074,7 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     a.elist_count = counts + 1;
     a.partials = work;
     a.stop = stop;
+    a.n_dev = A.n_dev;
     const int mgrid = it == 1 ? mblk : it == 2 ? mwave2 : std::min(mblk, 148 * 4);
     launch_m_step(c, a, mgrid, s);
     ST_LAUNCH_CHECK("k_m_step");
@@ -1112,6 +1119,7 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     tail.pw_scratch = (double*)(ws + L.pw_scratch);
     tail.pw_val = (double*)(ws + L.pw_val);
     tail.mu_unsafe = A.band ? f->mu_unsafe : nullptr;
+    tail.n_dev = A.n_dev;
     if (g) {
       tail.it_off = it_off;
       tail.use_cond = 1;
@@ -1153,9 +1161,11 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
   // (the statistics kernel sets its condition): the frame's converged
   // iterations cost no launches and no host round trip, whatever the cap.
   // (row bands exchanging records through the host callback keep the loop,
-  // and so do active-pixel lists (dynamic_only): their length, part of the
-  // captured arguments, changes from frame to frame)
-  bool use_graph = !A.exchange && !A.active && n > 0 && iters >= 3 && tail_graphs_enabled();
+  // and so do active-pixel lists whose length the host passes: it is part of
+  // the captured arguments and changes from frame to frame; a device-side
+  // count (A.n_dev) keeps the captured arguments fixed)
+  bool use_graph = !A.exchange && (!A.active || A.n_dev) && n > 0 && iters >= 3 &&
+                   tail_graphs_enabled();
   // a row band with no active pixel still takes part in every exchange
   for (int it = 1; it <= iters && (n > 0 || A.band); ++it) {
     if (use_graph && it == 3) {
@@ -1200,7 +1210,7 @@ static int solve_async_core(const st_frame* f, const st_rig* rig, const st_param
     ST_LAUNCH_CHECK("k_fill_mu");
     if (n > 0) {
       st::k_pack_outputs<<<blocks_for(n, 256), 256, 0, s>>>(f->mu, npx, 0, A.active, n, d_act,
-                                                            st_act, values, status, 0);
+                                                            st_act, values, status, 0, A.n_dev);
       ST_LAUNCH_CHECK("k_pack_outputs");
     }
   } else {
@@ -1303,6 +1313,18 @@ int st_solve_rows(const st_frame* f, const st_rig* rig, const st_params* p,
     sthost::count_launch();
     st::k_scatter_active<<<blocks_for(npx, 256), 256, 0, s>>>(flags, offs, npx, active);
     ST_LAUNCH_CHECK("k_scatter_active");
+    A.active = active;
+    if (world == 1 && row0 == 0 && row1 == H && ext0 == 0 && ext1 == H &&
+        !getenv("ST_DYNAMIC_READBACK")) {
+      // one shard over the whole frame: the count stays on the device (the
+      // grids cover every pixel; the kernels read the count), no host sync
+      A.n_dev = offs + npx;
+      A.n = npx;
+      A.cnt_lo = 0;
+      A.cnt_hi = npx;
+      return solve_async_core(f, rig, p, c, A, values, status, static_bits, valid_bits,
+                              stats_dev, ws, L, s);
+    }
     uint32_t h[3] = {0, 0, 0};
     ST_CUDA_CHECK(cudaMemcpyAsync(&h[0], offs + npx, 4, cudaMemcpyDeviceToHost, s));
     ST_CUDA_CHECK(cudaMemcpyAsync(&h[1], offs + (int64_t)row0 * W, 4, cudaMemcpyDeviceToHost, s));

@@ -313,7 +313,7 @@ __device__ __forceinline__ void list_append(bool want, int32_t slot, int32_t* li
 
 __global__ void MSTEP_BOUNDS k_m_step(EmCtx c, MStepArgs a) {
   if (a.stop && *a.stop) return;  // converged (st_solve_async)
-  const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n;
+  const int64_t n_work = a.list ? (int64_t)*a.list_count : a.n_dev ? (int64_t)*a.n_dev : a.n;
   long long n_cand = 0, n_eval = 0, n_hopeless = 0, n_samples = 0;
   __shared__ uint32_t s_off[ST_MAX_VIEWS * EM_BLOCK];
   __shared__ double s_f64[ST_MAX_VIEWS * EM_BLOCK];
@@ -475,8 +475,9 @@ __global__ void k_flag_mstep(const int64_t* __restrict__ active, int64_t n, int6
                              const uint32_t* __restrict__ mask_in, const double* __restrict__ e,
                              double* __restrict__ pe, uint8_t* __restrict__ chg,
                              int32_t* __restrict__ list, uint32_t* __restrict__ count,
-                             const int* stop) {
+                             const int* stop, const uint32_t* n_dev) {
   if (stop && *stop) return;
+  if (n_dev) n = *n_dev;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
@@ -507,7 +508,7 @@ __device__ void solve_control(int it, const Partial* __restrict__ reduced,
 // nodes up the same tree.  Should a value be non-finite (never for
 // d_max >= 1), the last block compacts the finite values and sums them
 // itself (the slow path: numpy's tree over the compacted sequence).
-int stats_depth(int64_t n) {
+__host__ __device__ int stats_depth(int64_t n) {
   int D = 0;  // nodes of ~4k values per block, <= 1024 blocks
   while (D < 10 && (n >> D) > 4096) ++D;
   return D;
@@ -557,9 +558,10 @@ __global__ void __launch_bounds__(STATS_BLOCK) k_em_stats(
     return;
   }
   __shared__ double val[(1 << PW_MAX_LEVELS) - 1];
-  const int D = tail.pw_depth;
+  if (tail.n_dev) n = *tail.n_dev;  // (the grid covers the upper bound's tree)
+  const int D = tail.n_dev ? stats_depth(n) : tail.pw_depth;
   int64_t s0, nn;
-  const bool own = pw_block_node(n, D, blockIdx.x, s0, nn);
+  const bool own = blockIdx.x < (1u << D) && pw_block_node(n, D, blockIdx.x, s0, nn);
   double se = 0.0, spe = 0.0;
   if (own && nn > 0) {
     se = pw_block_sum(e, s0, nn, val, PW_MAX_LEVELS);
@@ -674,8 +676,8 @@ __global__ void __launch_bounds__(STATS_BLOCK) k_em_stats(
   *tail.done = 0u;
   const int it = tail.it + (tail.it_off ? (int)*tail.it_off : 0);
   if (tail.record_only) {
-    r.n_act = tail.record_n_act;
-    r.n_mwork = it > 1 ? (long long)tail.counts[0] : tail.record_slots;
+    r.n_act = tail.n_dev ? (long long)n : tail.record_n_act;
+    r.n_mwork = it > 1 ? (long long)tail.counts[0] : tail.n_dev ? (long long)n : tail.record_slots;
     r.n_ework = (long long)tail.counts[1];
     r.n_unsafe = tail.mu_unsafe ? (long long)(*tail.mu_unsafe != 0) : 0;
     tail.reduced[it] = r;
@@ -1929,8 +1931,9 @@ __global__ void k_pack_outputs(const double* __restrict__ mu, int64_t npx, int64
                                const int64_t* __restrict__ active, int64_t n_active,
                                const double* __restrict__ d_act,
                                const uint8_t* __restrict__ st_act, float* __restrict__ values,
-                               uint8_t* __restrict__ status, int dense) {
+                               uint8_t* __restrict__ status, int dense, const uint32_t* n_dev) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n_dev) n_active = *n_dev;
   if (dense) {
     if (i >= npx) return;
     const int64_t p = pix0 + i;

@@ -88,6 +88,7 @@ struct MStepArgs {
   uint32_t* elist_count;
   Partial* partials;           // nullable: per-warp work counters
   const int* stop;             // nullable: device flag, set -> the launch does nothing
+  const uint32_t* n_dev;       // nullable: the slot count on the device (n: its upper bound)
 };
 
 struct EStepArgs {
@@ -111,7 +112,8 @@ __global__ void k_m_step(EmCtx c, MStepArgs a);
 __global__ void k_flag_mstep(const int64_t* active, int64_t n, int64_t pix0,
                              const uint32_t* static_all,
                              const uint32_t* mask_in, const double* e, double* pe, uint8_t* chg,
-                             int32_t* list, uint32_t* count, const int* stop = nullptr);
+                             int32_t* list, uint32_t* count, const int* stop = nullptr,
+                             const uint32_t* n_dev = nullptr);
 // k_em_stats' last block folds the blocks' records and runs the iteration's
 // control (st_solve_async) or writes the record (row bands, st_solve).
 struct StatsTail {
@@ -146,9 +148,13 @@ struct StatsTail {
   int use_cond;
   int iters;
   cudaGraphConditionalHandle cond;
+  // nullable: the counted slots' number on the device (dynamic_only's active
+  // list, no host read-back); the kernel's n and pw_depth are then upper
+  // bounds (the grid), the tree depth is derived on the device
+  const uint32_t* n_dev;
 };
 // grid of k_em_stats for n counted slots (1 << pw_depth blocks) and its depth
-int stats_depth(int64_t n);
+__host__ __device__ int stats_depth(int64_t n);
 int64_t pw_val_size(int64_t n);
 // Per-iteration statistics (solver.py:463-475): the mean of the finite M-step
 // energies and previous-disparity energies summed in numpy's own order
@@ -179,7 +185,8 @@ __global__ void k_masked_variance(const double* desc, const uint8_t* mask, int64
                                   double* out);
 __global__ void k_pack_outputs(const double* mu, int64_t npx, int64_t pix0, const int64_t* active,
                                int64_t n_active, const double* d_act, const uint8_t* st_act,
-                               float* values, uint8_t* status, int dense);
+                               float* values, uint8_t* status, int dense,
+                               const uint32_t* n_dev = nullptr);
 __global__ void k_fill_mu(const double* mu, int64_t npx, float* values, uint8_t* status);
 __global__ void k_stats_init(st_stats* stats, int64_t n_act);
 // Row bands: sum the shards' records (rank order, deterministic) and run the
@@ -191,6 +198,10 @@ struct BandLoop {
   int use_cond;
   int iters;
   cudaGraphConditionalHandle cond;
+  // nullable: the counted slots' number on the device (dynamic_only's active
+  // list, no host read-back); the kernel's n and pw_depth are then upper
+  // bounds (the grid), the tree depth is derived on the device
+  const uint32_t* n_dev;
 };
 __global__ void k_band_control(int it, const Partial* gathered, int world, int forced_iters,
                                st_stats* stats, int* stop, BandLoop loop);

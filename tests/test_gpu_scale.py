@@ -165,8 +165,9 @@ def test_graph_tail_equals_launch_loop(st, monkeypatch, cfg, forced, max_iters, 
     """Iterations >= 3 as a CUDA-graph WHILE loop (st_api.cu run_tail_graph,
     the statistics kernel sets the condition) == the plain launch loop
     (ST_NO_GRAPH), outputs and EMStats bit for bit, with the reference's
-    convergence test, forced iterations and a long cap; dynamic_only (the
-    row-band driver with an active list) stays on the launch loop."""
+    convergence test, forced iterations, a long cap and dynamic_only (the
+    row-band driver, one shard: the active count stays on the device and
+    k_band_control sets the condition)."""
     import dataclasses
     from paper_2003_11076_b200 import _native as N
     frame, rig, tri, sp, pp = _inputs(cfg)
@@ -179,9 +180,7 @@ def test_graph_tail_equals_launch_loop(st, monkeypatch, cfg, forced, max_iters, 
     a2 = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=forced, dynamic_only=dyn)
     assert lib.st_tail_graph_count(0) == b0, "the second solve did not reuse the cached graph"
     l1 = lib.st_tail_graph_count(1)
-    # (dynamic_only's active lists change length frame to frame: it keeps the
-    # launch loop, st_api.cu)
-    assert l1 == l0 + (0 if dyn else 2), "graph loop launches"
+    assert l1 == l0 + 2, "the graph loop did not run"
     monkeypatch.setenv("ST_NO_GRAPH", "1")
     b = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=forced, dynamic_only=dyn)
     assert lib.st_tail_graph_count(1) == l1
@@ -194,3 +193,22 @@ def test_graph_tail_equals_launch_loop(st, monkeypatch, cfg, forced, max_iters, 
         assert repr(r.stats) == repr(b.stats)
     if forced:
         assert a.stats.iterations_run == forced
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_dynamic_only_device_count_equals_readback(st, monkeypatch, cfg):
+    """dynamic_only with the active count kept on the device (one shard, no
+    host read-back, st_solve_rows) == the read-back path
+    (ST_DYNAMIC_READBACK), outputs and EMStats bit for bit."""
+    frame, rig, tri, sp, pp = _inputs(cfg)
+    a = st.reconstruct(frame, rig, tri, sp, pp, dynamic_only=True)
+    monkeypatch.setenv("ST_DYNAMIC_READBACK", "1")
+    monkeypatch.setenv("ST_NO_GRAPH", "1")
+    b = st.reconstruct(frame, rig, tri, sp, pp, dynamic_only=True)
+    for x, y in ((a.disparity.values, b.disparity.values),
+                 (a.disparity.status, b.disparity.status),
+                 (a.segmentation.static_bits, b.segmentation.static_bits),
+                 (a.segmentation.valid_bits, b.segmentation.valid_bits), (a.image, b.image),
+                 (a.provenance, b.provenance)):
+        assert np.array_equal(x, y)
+    assert repr(a.stats) == repr(b.stats)
