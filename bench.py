@@ -1133,7 +1133,8 @@ def run_ours(args):
                          "resident_fps": world * args.steps / (dyn_res_ms / 1e3),
                          "resident_ms_per_step": dyn_res_ms / args.steps,
                          "note": "person-only mode (PAPER.md:242; solver.py:449-452): "
-                                 "st_solve_rows (one read-back of the active-list size)"},
+                                 "st_solve_rows (the active count stays on the device: no host "
+                                 "read-back; iterations >= 3 in the graph loop)"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "em": {"iterations_run": s0.iterations_run, "converged_after": s0.converged_after,
