@@ -872,7 +872,9 @@ void destroy_tail_graph(TailGraph& t) {
   t.graph = nullptr;
 }
 
-int build_tail_graph(TailGraph& t, const std::function<int(const TailGraphFields*, cudaStream_t)>& body_fn) {
+using TailBody = std::function<int(const TailGraphFields*, cudaStream_t)>;
+
+int build_tail_graph(TailGraph& t, const TailBody& body_fn) {
   TailGraphFields fields;
   ST_CUDA_CHECK(cudaGraphCreate(&t.graph, 0));
   ST_CUDA_CHECK(cudaGraphConditionalHandleCreate(&fields.cond, t.graph, 1u,
@@ -907,8 +909,7 @@ int build_tail_graph(TailGraph& t, const std::function<int(const TailGraphFields
   return ST_OK;
 }
 
-int run_tail_graph(cudaStream_t s, TailGraphKey key,
-                   const std::function<int(const TailGraphFields*, cudaStream_t)>& body_fn) {
+int run_tail_graph(cudaStream_t s, TailGraphKey key, const TailBody& body_fn) {
   ST_CUDA_CHECK(cudaGetDevice(&key.device));
   std::lock_guard<std::mutex> lock(g_tail_mu);
   std::vector<TailGraph>& cache = *g_tail;
@@ -917,8 +918,9 @@ int run_tail_graph(cudaStream_t s, TailGraphKey key,
     if (memcmp(&t.key, &key, sizeof(key)) == 0) hit = &t;
   if (!hit) {
     if (cache.size() >= TAIL_GRAPH_CAP) {  // least recently used out
-      auto lru = std::min_element(cache.begin(), cache.end(),
-                                  [](const TailGraph& a, const TailGraph& b) { return a.used < b.used; });
+      auto lru = std::min_element(
+          cache.begin(), cache.end(),
+          [](const TailGraph& a, const TailGraph& b) { return a.used < b.used; });
       destroy_tail_graph(*lru);
       cache.erase(lru);
     }
