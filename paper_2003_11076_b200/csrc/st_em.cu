@@ -508,9 +508,12 @@ __device__ void solve_control(int it, const Partial* __restrict__ reduced,
 // nodes up the same tree.  Should a value be non-finite (never for
 // d_max >= 1), the last block compacts the finite values and sums them
 // itself (the slow path: numpy's tree over the compacted sequence).
+#ifndef STATS_NODE
+#define STATS_NODE 4096
+#endif
 __host__ __device__ int stats_depth(int64_t n) {
-  int D = 0;  // nodes of ~4k values per block, <= 1024 blocks
-  while (D < 10 && (n >> D) > 4096) ++D;
+  int D = 0;  // nodes of ~STATS_NODE values per block, <= 1024 blocks
+  while (D < 10 && (n >> D) > STATS_NODE) ++D;
   return D;
 }
 
