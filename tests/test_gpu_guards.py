@@ -83,3 +83,32 @@ def test_results_do_not_depend_on_scheduling(name):
         assert list(r.stats.mean_energy) == list(ref.stats.mean_energy)
         assert list(r.stats.prev_energy) == list(ref.stats.prev_energy)
         assert r.stats.energy_evals == ref.stats.energy_evals
+
+
+@pytest.mark.parametrize("mode", ["slot", "main", "2"])
+@pytest.mark.parametrize("dyn", [False, True])
+def test_stream_modes_keep_frames_apart(monkeypatch, mode, dyn):
+    """reconstruct_stream's compute-stream modes (ST_STREAM_COMPUTE: one
+    stream per slot, the caller's stream, two slot streams) with several
+    frames in flight: every output equals reconstruct() of its own frame,
+    for two alternating frames (distinct active sets and results)."""
+    import paper_2003_11076_b200 as st
+    frame, rig, tri, sp, pp = _inputs("C1")
+    other = st.LightFieldFrame(images=[np.ascontiguousarray(np.roll(x, 7, axis=1))
+                                       for x in frame.images],
+                               priors=[np.ascontiguousarray(np.roll(x, 7, axis=1))
+                                       for x in frame.priors])
+    frames = [frame, other]
+    refs = [st.reconstruct(f, rig, tri, sp, pp, dynamic_only=dyn) for f in frames]
+    assert not np.array_equal(refs[0].image, refs[1].image)
+    monkeypatch.setenv("ST_STREAM_COMPUTE", mode)
+    outs = list(st.reconstruct_stream([(frames[i % 2], tri) for i in range(9)], rig, sp, pp,
+                                      dynamic_only=dyn))
+    assert len(outs) == 9
+    for i, r in enumerate(outs):
+        ref = refs[i % 2]
+        for a, b in ((r.disparity.values, ref.disparity.values),
+                     (r.segmentation.static_bits, ref.segmentation.static_bits),
+                     (r.image, ref.image), (r.provenance, ref.provenance)):
+            assert np.array_equal(a, b), (mode, dyn, i)
+        assert list(r.stats.mean_energy) == list(ref.stats.mean_energy)
