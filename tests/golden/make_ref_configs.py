@@ -22,7 +22,10 @@ The margins are computed with the oracle (oracle/em.py m_margins/e_margins,
 itself pinned bit-exact to the reference by tests/test_oracle.py); the
 outputs and statistics come from the reference.
 
-    OPENBLAS_NUM_THREADS=1 python tests/golden/make_ref_configs.py C1 C2 C3 forced C4rows
+  * `ref_<cfg>_dynamic.npz`: the same for dynamic_only (the person-only mode).
+
+    OPENBLAS_NUM_THREADS=1 python tests/golden/make_ref_configs.py C1 C2 C3 forced C4rows \
+        C1dynamic C2dynamic
 """
 
 import hashlib
@@ -128,6 +131,83 @@ def traced_solve(solver, forced=None):
     return dict(values=values.reshape(h, w), status=status.reshape(h, w),
                 static_bits=static.reshape(h, w), valid_bits=valid.reshape(h, w),
                 stats=stats, last_masks=before, last_d=d)
+
+
+def traced_dynamic(solver):
+    """solver.py:436-502 with dynamic_only=True (active = ref prior < threshold),
+    keeping the final iteration's masks and disparities (full-frame arrays,
+    NaN / LOW_TEXTURE outside the active set)."""
+    h, w = solver.height, solver.width
+    allp = np.arange(h * w, dtype=np.int64)
+    ref_prior = solver.frame.priors[solver.rig.ref_index].ravel()
+    active = allp[ref_prior < solver.params.threshold]
+    static, valid = solver.initial_masks(allp)
+    d_prev = None
+    last = None
+    for it in range(1, solver.params.max_iters + 1):
+        before = static
+        d, e, status = solver.m_step(active, static)
+        changed = None
+        if d_prev is not None:
+            with np.errstate(invalid="ignore"):
+                changed = float(np.mean(np.abs(d - d_prev) > 0.5))
+        ok = status != st.STATUS_LOW_TEXTURE
+        s_new, v_new = solver.e_step_at(active[ok], d[ok])
+        static = static.copy()
+        static[active[ok]] = s_new
+        last = (before, d, status)
+        if changed is not None and changed < 1e-3:
+            break
+        d_prev = d
+    before, d, status = last
+    d_full = np.full(h * w, np.nan)
+    d_full[active] = d
+    st_full = np.full(h * w, st.STATUS_LOW_TEXTURE, dtype=np.uint8)
+    st_full[active] = status
+    return before, d_full, st_full, active
+
+
+def make_dynamic(cfg):
+    """dynamic_only (PAPER.md:242 person-only mode; solver.py:449-452,
+    pipeline.py:250-260) at a bench config: the reference's solve + refocus
+    with the copy mask, and the final-iteration margins on the active set."""
+    frame, rig, tri, sp, pp = bench_inputs(cfg)
+    t1 = time.time()
+    dmap, seg, stats = st.em_solve(frame, rig, tri, params=sp, prior_params=pp,
+                                   dynamic_only=True)
+    copy_mask = frame.priors[rig.ref_index] >= sp.threshold
+    img, prov, nr = st.synthesize(frame, rig, dmap, seg, min_static_rays=sp.min_static_rays,
+                                  median_radius=1, copy_mask=copy_mask)
+    t2 = time.time()
+    solver = st.DisparitySolver(frame, rig, tri, params=sp, prior_params=pp)
+    masks, d, status, active = traced_dynamic(solver)
+    orc = oracle_of(frame, rig, tri, sp, pp, solver)
+    n = masks.size
+    m = np.full(n, np.inf)
+    e = np.full(n, np.inf)
+    for lo in range(0, active.size, CHUNK):
+        act = active[lo:lo + CHUNK]
+        db, eb, mm = orc.m_margins(act, masks)
+        m[act] = mm
+        ok = status[act] != st.STATUS_LOW_TEXTURE
+        if ok.any():
+            e[act[ok]] = orc.e_margins(act[ok], d[act[ok]])
+    summ = margin_summary(m, e)
+    print(f"{cfg} dynamic_only: solve+refocus {t2 - t1:.1f}s, active {active.size}, "
+          f"iterations {stats.iterations_run}, {summ}", flush=True)
+    np.savez_compressed(
+        os.path.join(HERE, f"ref_{cfg}_dynamic.npz"),
+        values=dmap.values, status=dmap.status, static_bits=seg.static_bits,
+        valid_bits=seg.valid_bits, image=img, provenance=prov, n_rays=nr,
+        stats=json.dumps(dict(iterations_run=stats.iterations_run,
+                              converged_after=stats.converged_after,
+                              mean_energy=stats.mean_energy, prev_energy=stats.prev_energy,
+                              changed_fraction=stats.changed_fraction)),
+        m_low=np.flatnonzero(~(m > MARGIN)).astype(np.int64),
+        e_low=np.flatnonzero(~(e > MARGIN)).astype(np.int64),
+        margins=json.dumps(summ),
+        inputs=json.dumps(dict(config=cfg, scene=SCENE, dynamic_only=True,
+                               image_digest=digest(frame.images))))
 
 
 def margins(orc, masks, d, status):
@@ -252,6 +332,8 @@ def main(args):
             make_forced("C1")
         elif a == "C4rows":
             make_c4rows()
+        elif a.endswith("dynamic") and a[:2] in CONFIGS:
+            make_dynamic(a[:2])
         else:
             raise SystemExit(f"unknown target {a}")
 

@@ -173,3 +173,16 @@ def test_c4_rows_m_and_e_step_match_reference(st):
     assert np.array_equal(v1, z["e_valid"])
     print(f"C4 rows: d agree {same.mean():.6f}, static agree {(s1 == z['e_static']).mean():.6f}, "
           f"margins {str(z['margins'])}")
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_dynamic_only_matches_reference(st, cfg):
+    """The person-only mode (solver.py:449-452 with the copy
+    mask of pipeline.py:250-260) at C1 and C2, whole frames, against the
+    reference's em_solve(dynamic_only=True) + synthesize(copy_mask=...)."""
+    path = os.path.join(GOLDEN, f"ref_{cfg}_dynamic.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    frame, rig, tri, sp, pp = _inputs(cfg)
+    r = st.reconstruct(frame, rig, tri, sp, pp, dynamic_only=True)
+    check_against_reference(r, _ref(f"ref_{cfg}_dynamic"), f"{cfg} dynamic_only")
