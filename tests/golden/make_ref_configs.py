@@ -270,10 +270,10 @@ def make_config(cfg):
 
 
 def make_forced(name):
-    """Forced 5 iterations: occ320_noisy golden scene and C1."""
+    """Forced 5 iterations: occ320_noisy golden scene, C1 and C2."""
     iters = 5
-    if name == "C1":
-        frame, rig, tri, sp, pp = bench_inputs("C1")
+    if name in CONFIGS:
+        frame, rig, tri, sp, pp = bench_inputs(name)
     else:  # the occ320_noisy golden scene (make_golden.py main)
         sys.path.insert(0, HERE)
         from make_golden import rendered  # noqa: E402
@@ -332,6 +332,8 @@ def main(args):
             make_forced("C1")
         elif a == "C4rows":
             make_c4rows()
+        elif a == "forcedC2":
+            make_forced("C2")
         elif a.endswith("dynamic") and a[:2] in CONFIGS:
             make_dynamic(a[:2])
         else:

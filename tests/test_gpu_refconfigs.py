@@ -129,6 +129,20 @@ def test_c1_forced_iterations_match_reference(st):
     check_against_reference(r, ref, "C1 forced-5")
 
 
+def test_c2_forced_iterations_match_reference(st):
+    """The forced-5 bench mode at the headline config C2 against the
+    reference's own m_step / e_step_at composed 5 times."""
+    path = os.path.join(GOLDEN, "forced_C2.npz")
+    if not os.path.exists(path):
+        pytest.skip("forced_C2.npz not generated")
+    frame, rig, tri, sp, pp = _inputs("C2")
+    r = st.reconstruct(frame, rig, tri, sp, pp, forced_iters=5)
+    ref = _ref("forced_C2")
+    assert r.stats.iterations_run == 5
+    ref["stats"]["converged_after"] = None
+    check_against_reference(r, ref, "C2 forced-5")
+
+
 def test_occ320_forced_iterations_match_reference(st):
     from golden_io import load
     from test_gpu_parity import _Rig, _Tri, _frame, _params
@@ -175,10 +189,10 @@ def test_c4_rows_m_and_e_step_match_reference(st):
           f"margins {str(z['margins'])}")
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
 def test_dynamic_only_matches_reference(st, cfg):
     """The person-only mode (solver.py:449-452 with the copy
-    mask of pipeline.py:250-260) at C1 and C2, whole frames, against the
+    mask of pipeline.py:250-260) at C1, C2 and C3, whole frames, against the
     reference's em_solve(dynamic_only=True) + synthesize(copy_mask=...)."""
     path = os.path.join(GOLDEN, f"ref_{cfg}_dynamic.npz")
     if not os.path.exists(path):
