@@ -200,3 +200,32 @@ def test_dynamic_only_matches_reference(st, cfg):
     frame, rig, tri, sp, pp = _inputs(cfg)
     r = st.reconstruct(frame, rig, tri, sp, pp, dynamic_only=True)
     check_against_reference(r, _ref(f"ref_{cfg}_dynamic"), f"{cfg} dynamic_only")
+
+
+def test_c4_whole_frame_matches_reference_digests(st):
+    """C4 (3840x2160, K = 9, d_max 128), the whole frame, against the
+    reference's em_solve + synthesize run on the same inputs
+    (tests/golden/ref_C4_digests.json: sha256 of every output array, the
+    EMStats): every output byte-identical."""
+    import hashlib
+    path = os.path.join(GOLDEN, "ref_C4_digests.json")
+    if not os.path.exists(path):
+        pytest.skip("ref_C4_digests.json not generated")
+    ref = json.load(open(path))
+    frame, rig, tri, sp, pp = _inputs("C4")
+    r = st.reconstruct(frame, rig, tri, sp, pp)
+
+    def dg(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    got = dict(values=dg(r.disparity.values), status=dg(r.disparity.status),
+               static_bits=dg(r.segmentation.static_bits),
+               valid_bits=dg(r.segmentation.valid_bits), image=dg(r.image),
+               provenance=dg(r.provenance), n_rays=dg(r.n_rays))
+    for k, v in got.items():
+        assert v == ref[k], k
+    rs = ref["stats"]
+    assert r.stats.iterations_run == rs["iterations_run"]
+    assert r.stats.converged_after == rs["converged_after"]
+    assert list(r.stats.changed_fraction) == list(rs["changed_fraction"])
+    np.testing.assert_allclose(r.stats.mean_energy, rs["mean_energy"], rtol=1e-14, atol=0)
+    np.testing.assert_allclose(r.stats.prev_energy, rs["prev_energy"], rtol=1e-14, atol=0)
