@@ -1,7 +1,10 @@
 """Reference C4 whole frame (em_solve + synthesize) -> sha256 digests of every output
 array and the EMStats (build container; ~40 min on 8 cores):
 
-    OPENBLAS_NUM_THREADS=8 python tests/golden/make_ref_c4_digests.py
+    OPENBLAS_NUM_THREADS=8 python tests/golden/make_ref_c4_digests.py [dynamic]
+
+`dynamic`: the person-only mode (em_solve(dynamic_only=True) + synthesize
+with the copy mask, pipeline.py:250-260) -> ref_C4_dynamic_digests.json.
 """
 import hashlib, json, os, sys, time
 import numpy as np
@@ -14,9 +17,12 @@ import seethrough as st
 t0 = time.time()
 frame, rig, tri, sp, pp = M.bench_inputs("C4")
 t1 = time.time()
-dmap, seg, stats = st.em_solve(frame, rig, tri, params=sp, prior_params=pp)
+dyn = "dynamic" in sys.argv[1:]
+dmap, seg, stats = st.em_solve(frame, rig, tri, params=sp, prior_params=pp, dynamic_only=dyn)
 t2 = time.time()
-img, prov, nr = st.synthesize(frame, rig, dmap, seg, min_static_rays=sp.min_static_rays, median_radius=1)
+copy_mask = frame.priors[rig.ref_index] >= sp.threshold if dyn else None
+img, prov, nr = st.synthesize(frame, rig, dmap, seg, min_static_rays=sp.min_static_rays,
+                              median_radius=1, copy_mask=copy_mask)
 t3 = time.time()
 def dg(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
@@ -26,5 +32,6 @@ out = dict(values=dg(dmap.values), status=dg(dmap.status), static_bits=dg(seg.st
                       mean_energy=stats.mean_energy, prev_energy=stats.prev_energy,
                       changed_fraction=stats.changed_fraction),
            seconds=dict(inputs=t1 - t0, solve=t2 - t1, refocus=t3 - t2))
-json.dump(out, open(os.path.join(HERE, "ref_C4_digests.json"), "w"), indent=1)
+name = "ref_C4_dynamic_digests.json" if dyn else "ref_C4_digests.json"
+json.dump(out, open(os.path.join(HERE, name), "w"), indent=1)
 print(json.dumps(out["seconds"]), flush=True)

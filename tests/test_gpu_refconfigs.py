@@ -202,18 +202,20 @@ def test_dynamic_only_matches_reference(st, cfg):
     check_against_reference(r, _ref(f"ref_{cfg}_dynamic"), f"{cfg} dynamic_only")
 
 
-def test_c4_whole_frame_matches_reference_digests(st):
-    """C4 (3840x2160, K = 9, d_max 128), the whole frame, against the
-    reference's em_solve + synthesize run on the same inputs
-    (tests/golden/ref_C4_digests.json: sha256 of every output array, the
-    EMStats): every output byte-identical."""
+@pytest.mark.parametrize("name,dyn", [("ref_C4_digests.json", False),
+                                      ("ref_C4_dynamic_digests.json", True)])
+def test_c4_whole_frame_matches_reference_digests(st, name, dyn):
+    """C4 (3840x2160, K = 9, d_max 128), the whole frame (and the person-only
+    mode), against the reference's em_solve + synthesize run on the same
+    inputs (tests/golden/ref_C4*_digests.json, make_ref_c4_digests.py:
+    sha256 of every output array, the EMStats): every output byte-identical."""
     import hashlib
-    path = os.path.join(GOLDEN, "ref_C4_digests.json")
+    path = os.path.join(GOLDEN, name)
     if not os.path.exists(path):
-        pytest.skip("ref_C4_digests.json not generated")
+        pytest.skip(f"{name} not generated")
     ref = json.load(open(path))
     frame, rig, tri, sp, pp = _inputs("C4")
-    r = st.reconstruct(frame, rig, tri, sp, pp)
+    r = st.reconstruct(frame, rig, tri, sp, pp, dynamic_only=dyn)
 
     def dg(a):
         return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
